@@ -1,0 +1,230 @@
+"""ctypes binding of libpm2l_b200.so (include/pm2l.h).
+
+The library is loaded from the package directory (built in-tree by
+``_build.build()``).  There is no CPU fallback: if the library is missing or
+no CUDA device is visible, every compute entry point raises
+``BackendUnavailable`` instead of silently computing elsewhere.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .errors import BackendUnavailable, DeviceError, ValidationError
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpm2l_b200.so")
+
+PM2L_OK, PM2L_ERR_INVALID, PM2L_ERR_CUDA, PM2L_ERR_NOMEM, PM2L_ERR_NODEVICE = 0, -1, -2, -3, -4
+
+_p = C.c_void_p
+_i64 = C.c_int64
+_i32 = C.c_int
+
+
+class TablesView(C.Structure):
+    """Mirror of pm2l_tables_view."""
+    _fields_ = [
+        ("n_records", _i64), ("exact_keys", _p), ("exact_coords", _p), ("exact_curve", _p),
+        ("log_m", _p), ("log_n", _p), ("log_k", _p), ("cand_curve", _p),
+        ("n_curves", _i64), ("sample_offsets", _p), ("sample_dims", _p), ("sample_thrs", _p),
+        ("ref_dim", _p), ("ref_dur", _p), ("ref_thr", _p), ("ref_waves", _p),
+        ("tile_m", _p), ("tile_n", _p), ("split_k", _p), ("blocks_per_wave", _p),
+        ("family_rowblock", _p),
+    ]
+
+
+#: every symbol include/pm2l.h declares, with (restype, argtypes)
+SIGNATURES = {
+    "pm2l_abi_version": (_i32, []),
+    "pm2l_last_error": (C.c_char_p, []),
+    "pm2l_device_count": (_i32, []),
+    "pm2l_tables_create": (_i32, [C.POINTER(TablesView), _i32, C.POINTER(_p)]),
+    "pm2l_tables_destroy": (_i32, [_p]),
+    "pm2l_tables_groups": (_i64, [_p]),
+    "pm2l_grid_predict": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
+                                 _p, _p, _p, _p, _p]),
+    "pm2l_grid_plan_create": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
+                                     C.POINTER(_p)]),
+    "pm2l_grid_plan_launch": (_i32, [_p, _p, _p, _p, _p, _p, _i32, _p]),
+    "pm2l_grid_plan_info": (_i32, [_p, C.POINTER(_i64)]),
+    "pm2l_grid_plan_destroy": (_i32, [_p]),
+    "pm2l_nan_scan": (_i32, [_p, _i64, _p, _p]),
+    "pm2l_grid_predict_all_curves": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64,
+                                            _i64, _i64, _p, _p]),
+    "pm2l_points_predict": (_i32, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
+    "pm2l_points_predict_curve": (_i32, [_p, _p, _p, _i64, _p, _p, _p, _p]),
+    "pm2l_membound_predict": (_i32, [_p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p]),
+    "pm2l_segment_fsum": (_i32, [_p, _p, _i64, _p, _p]),
+    "pm2l_predict_grid_slice": (_i32, [_p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
+                                       _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _i64,
+                                       _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load(required: bool = True):
+    """The loaded CDLL (or None when missing and not required)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(_LIB_PATH):
+                if not required:
+                    return None
+                raise BackendUnavailable(
+                    f"{_LIB_PATH} is not built (run __graft_entry__.build() or "
+                    f"python -m paper_2603_00549_b200._build); there is no CPU fallback")
+            lib = C.CDLL(_LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def device_count() -> int:
+    lib = load(required=False)
+    return 0 if lib is None else int(lib.pm2l_device_count())
+
+
+def check(rc: int, what: str) -> None:
+    if rc == PM2L_OK:
+        return
+    msg = load().pm2l_last_error().decode("utf-8", "replace")
+    if rc == PM2L_ERR_NODEVICE:
+        raise BackendUnavailable(f"{what}: {msg}")
+    if rc == PM2L_ERR_INVALID:
+        raise ValidationError(f"{what}: {msg}")
+    raise DeviceError(f"{what}: {msg} (status {rc})")
+
+
+def require_gpu():
+    """Load the library and make sure a CUDA device is visible."""
+    lib = load()
+    if lib.pm2l_device_count() < 1:
+        raise BackendUnavailable("no CUDA device visible: the B200 build has no CPU fallback")
+    return lib
+
+
+def ptr(a) -> int:
+    """Address of a numpy array / torch tensor (0 for None)."""
+    if a is None:
+        return 0
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    return int(a.data_ptr())
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class DeviceTables:
+    """Owning wrapper of a pm2l_tables handle (HBM-resident staged tables)."""
+
+    def __init__(self, tables: dict, device: int = 0):
+        lib = require_gpu()
+        keep = {}
+
+        def arr(name, dtype):
+            a = tables.get(name)
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dtype)
+            keep[name] = a
+            return a.ctypes.data
+
+        view = TablesView()
+        view.n_records = len(tables["cand_curve"])
+        view.exact_keys = arr("exact_keys", np.uint64) if tables.get("exact_coords") is None else None
+        view.exact_coords = arr("exact_coords", np.uint64)
+        view.exact_curve = arr("exact_curve" if tables.get("exact_coords") is None
+                               else "exact_coords_curve", np.int64)
+        for name in ("log_m", "log_n", "log_k"):
+            setattr(view, name, arr(name, np.float64))
+        view.cand_curve = arr("cand_curve", np.int64)
+        view.n_curves = len(tables["sample_offsets"]) - 1
+        view.sample_offsets = arr("sample_offsets", np.int64)
+        view.sample_dims = arr("sample_dims", np.float64)
+        view.sample_thrs = arr("sample_thrs", np.float64)
+        for name in ("ref_dim", "ref_dur", "ref_thr", "ref_waves"):
+            setattr(view, name, arr(name, np.float64))
+        for name in ("tile_m", "tile_n", "split_k", "blocks_per_wave"):
+            setattr(view, name, arr(name, np.uint64))
+        view.family_rowblock = arr("family_rowblock", np.uint8)
+        handle = C.c_void_p()
+        check(lib.pm2l_tables_create(C.byref(view), device, C.byref(handle)), "pm2l_tables_create")
+        self._lib = lib
+        self.handle = handle
+        self.device = device
+        self.n_curves = int(view.n_curves)
+        self.n_records = int(view.n_records)
+
+    @property
+    def groups(self) -> int:
+        return int(self._lib.pm2l_tables_groups(self.handle))
+
+    def close(self):
+        if self.handle:
+            self._lib.pm2l_tables_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GridPlan:
+    """Owning wrapper of pm2l_grid_plan: a grid slice staged once, launched
+    many times (kernels only)."""
+
+    def __init__(self, tables: DeviceTables, axes, b_lo: int = 0, b_hi=None):
+        lib = require_gpu()
+        arrs = [np.ascontiguousarray(a, dtype=np.uint64) for a in axes]
+        b_hi = len(arrs[0]) if b_hi is None else b_hi
+        handle = C.c_void_p()
+        args = []
+        for a in arrs:
+            args += [a.ctypes.data, len(a)]
+        check(lib.pm2l_grid_plan_create(tables.handle, *args, b_lo, b_hi, C.byref(handle)),
+              "pm2l_grid_plan_create")
+        self._lib = lib
+        self._tables = tables  # keep alive
+        self.handle = handle
+        info = (_i64 * 4)()
+        check(lib.pm2l_grid_plan_info(handle, info), "pm2l_grid_plan_info")
+        self.cardinality, self.n_fixups, self.workspace_bytes, self.staged_bytes = \
+            (int(x) for x in info)
+
+    def launch(self, out_lat, curve=None, blocks=None, waves=None, nan_stats=None,
+               stages: int = 7, stream=None):
+        check(self._lib.pm2l_grid_plan_launch(
+            self.handle, ptr(out_lat), ptr(curve), ptr(blocks), ptr(waves), ptr(nan_stats),
+            stages, stream_handle(stream)), "pm2l_grid_plan_launch")
+
+    def close(self):
+        if self.handle:
+            self._lib.pm2l_grid_plan_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

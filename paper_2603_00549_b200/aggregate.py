@@ -1,0 +1,246 @@
+"""Whole-model latency: per-layer predictions + exact per-model totals.
+
+Drop-in for ``ModelPredictor`` / ``predict_model`` (pm2lat/aggregate.py:105-196),
+plus ``predict_models`` for batches of graphs (the NAS whole-model sweep).
+All layer latencies come from the GPU, batched across every layer of every
+graph: compute layers are resolved (``points_kernel``) and predicted
+(``points_curve_kernel``), utility layers go through ``membound_kernel``,
+and the totals are the correctly-rounded sums of each model's layers
+(``segment_fsum_kernel``, bit-identical to ``math.fsum``, aggregate.py:193).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .compute import (CLAMP_ABOVE, CLAMP_BELOW, MATCH_EXACT, MATCH_NEAREST, ConfigResolver,
+                      WaveModel, _check_pair)
+from .core import (COMPUTE_FAMILIES, FAMILY_LINEAR, DType, KernelKey, LayerSpec, ModelGraph,
+                   Prediction, TransposeMode, is_utility_family, utility_kernel_name)
+from .errors import InsufficientData, PredictionError, UnresolvedLayer
+from .ingest import Dataset
+from .membound import DEFAULT_LAUNCH_FLOOR_US, MemBoundModel, fit
+
+PREDICTOR_COMPUTE = "compute"
+PREDICTOR_MEMBOUND = "membound"
+DEFAULT_TRANSPOSE = {FAMILY_LINEAR: TransposeMode.TN}
+
+
+def default_transpose(family: str) -> TransposeMode:
+    return DEFAULT_TRANSPOSE.get(family, TransposeMode.NN)
+
+
+@dataclass(frozen=True)
+class LayerPrediction:
+    layer_id: str
+    prediction: Prediction
+    predictor_kind: str
+
+
+@dataclass(frozen=True)
+class ModelPrediction:
+    model_name: str
+    total_latency_us: float
+    per_layer: Tuple[LayerPrediction, ...]
+    flags: Tuple[Tuple[str, str], ...]
+
+    def to_json_obj(self) -> dict:
+        return {"model_name": self.model_name, "total_latency_us": self.total_latency_us,
+                "per_layer": [{"layer_id": lp.layer_id, "latency_us": lp.prediction.latency_us,
+                               "predictor_kind": lp.predictor_kind,
+                               "components": dict(lp.prediction.components)}
+                              for lp in self.per_layer],
+                "flags": [{"layer_id": lid, "flag": f} for lid, f in self.flags]}
+
+
+class ModelPredictor:
+    """Dataset + lookup structures (resolver, fitted membound models)."""
+
+    def __init__(self, dataset: Dataset, wm: Optional[WaveModel] = None,
+                 membound_floor_us: float = DEFAULT_LAUNCH_FLOOR_US):
+        self.dataset = dataset
+        self.wm = wm or WaveModel(sm_count=dataset.device.sm_count)
+        self.floor_us = membound_floor_us
+        self.resolver = ConfigResolver(dataset.config_map, dataset=dataset, wm=self.wm)
+        self._membound: Dict[Tuple[str, DType], MemBoundModel] = {
+            (m.kernel_name, m.dtype): m for m in dataset.membound_models}
+        self._curves = None
+
+    def membound_model(self, kernel_name: str, dtype: DType) -> MemBoundModel:
+        got = self._membound.get((kernel_name, dtype))
+        if got is not None:
+            return got
+        recs = [(r.features, r.latency_us) for r in self.dataset.membound_records
+                if r.kernel_name == kernel_name and r.dtype == dtype]
+        if not recs:
+            raise UnresolvedLayer(f"no fitted model or records for utility kernel "
+                                  f"{kernel_name!r} ({dtype.value})")
+        try:
+            model = fit(recs, kernel_name, dtype, train_device_id=self.dataset.device.device_id)
+        except InsufficientData as exc:
+            raise UnresolvedLayer(str(exc)) from None
+        self._membound[(kernel_name, dtype)] = model
+        return model
+
+    def all_curves(self):
+        if self._curves is None:
+            self._curves = list(self.dataset.curves.values())
+            self._curve_pos = {c.kernel: i for i, c in enumerate(self._curves)}
+        return self._curves
+
+    def predict_layers(self, layers: Sequence[LayerSpec]):
+        """Device batch over layers: [(Prediction, kind, flags)] in order.
+        Raises like the reference on the first unresolvable layer."""
+        from .compute import predict_curve_batch
+        from .membound import predict_membound_batch
+        n = len(layers)
+        out: List[Optional[tuple]] = [None] * n
+        errors: Dict[int, Exception] = {}   # the reference raises at the FIRST bad layer
+
+        def wrap(i, exc):
+            if isinstance(exc, UnresolvedLayer):
+                return exc
+            return type(exc)(f"layer {layers[i].layer_id!r}: {exc}")
+
+        by_triple: Dict[tuple, List[int]] = {}
+        util_idx: List[int] = []
+        for i, layer in enumerate(layers):
+            if is_utility_family(layer.family):
+                if layer.features is None:
+                    errors[i] = UnresolvedLayer(f"utility layer {layer.layer_id!r} carries no "
+                                                f"features")
+                else:
+                    util_idx.append(i)
+            elif layer.family not in COMPUTE_FAMILIES:
+                errors[i] = UnresolvedLayer(f"layer {layer.layer_id!r}: no predictor for family "
+                                            f"{layer.family!r}")
+            elif layer.shape is None:
+                errors[i] = UnresolvedLayer(f"compute layer {layer.layer_id!r} carries no shape")
+            else:
+                tr = layer.transpose_mode or default_transpose(layer.family)
+                by_triple.setdefault((layer.family, layer.dtype, tr), []).append(i)
+        # ---- compute layers: device resolution per triple
+        resolved: Dict[int, tuple] = {}
+        for triple, idx in by_triple.items():
+            try:
+                rec, match, dist = self.resolver.resolve_batch(
+                    *triple, [layers[i].shape.as_tuple() for i in idx])
+            except PredictionError as exc:
+                for i in idx:
+                    errors[i] = wrap(i, exc)
+                continue
+            recs = self.resolver.triple_tables(*triple)[0]
+            for j, i in enumerate(idx):
+                key = recs[int(rec[j])].chosen_key
+                resolved[i] = (key, MATCH_EXACT if match[j] == 0 else MATCH_NEAREST)
+        curves = self.all_curves()
+        compute_idx, cids = [], []
+        for i in sorted(resolved):
+            key, _ = resolved[i]
+            if key not in self._curve_pos:
+                errors[i] = UnresolvedLayer(
+                    f"layer {layers[i].layer_id!r}: resolved kernel has no throughput curve "
+                    f"(family={layers[i].family}, algo={key.algorithm_id})")
+                continue
+            try:
+                _check_pair(key, curves[self._curve_pos[key]])
+            except PredictionError as exc:
+                errors[i] = wrap(i, exc)
+                continue
+            compute_idx.append(i)
+            cids.append(self._curve_pos[key])
+        # ---- utility layers: fitted (or on-demand refit) membound models
+        models: List[MemBoundModel] = []
+        pos: Dict[tuple, int] = {}
+        util_ok, mids = [], []
+        for i in util_idx:
+            name = utility_kernel_name(layers[i].family)
+            mk = (name, layers[i].dtype)
+            try:
+                if mk not in pos:
+                    models.append(self.membound_model(name, layers[i].dtype))
+                    pos[mk] = len(models) - 1
+            except PredictionError as exc:
+                errors[i] = wrap(i, exc)
+                continue
+            util_ok.append(i)
+            mids.append(pos[mk])
+        if errors:
+            raise errors[min(errors)]
+        if compute_idx:
+            lat, waves, det = predict_curve_batch([layers[i].shape.as_tuple() for i in compute_idx],
+                                                  curves, cids, self.wm, detail=True)
+            for j, i in enumerate(compute_idx):
+                key, match = resolved[i]
+                c = curves[cids[j]]
+                k = layers[i].shape.k
+                dims = c.dim_values()
+                clamp = CLAMP_BELOW if k < dims[0] else CLAMP_ABOVE if k > dims[-1] else None
+                comps = {"base_us": float(det[j, 0]), "ref_duration_us": c.ref_duration_us,
+                         "varying_value": k, "ref_dim_value": c.ref_dim_value,
+                         "new_throughput_gflops": float(det[j, 1]),
+                         "ref_throughput_gflops": c.ref_throughput, "waves": int(waves[j]),
+                         "ref_waves": c.ref_waves, "wave_scale": float(det[j, 2]),
+                         "blocks_per_wave": self.wm.for_curve(c).blocks_per_wave,
+                         "clamp": clamp, "config_match": match}
+                flags = (["nearest_config"] if match == MATCH_NEAREST else []) + \
+                    ([clamp] if clamp else [])
+                out[i] = (Prediction(float(lat[j]), key, comps), PREDICTOR_COMPUTE, flags)
+        if util_ok:
+            feats = [layers[i].features.as_vector() for i in util_ok]
+            lat, floored = predict_membound_batch(models, feats, mids,
+                                                  [self.floor_us] * len(models))
+            raw, _ = predict_membound_batch(models, feats, mids, [-np.inf] * len(models))
+            for j, i in enumerate(util_ok):
+                key = KernelKey.for_utility(models[mids[j]].kernel_name, layers[i].dtype)
+                comps = {"raw_us": float(raw[j]), "floor_us": self.floor_us,
+                         "floored": bool(floored[j])}
+                out[i] = (Prediction(float(lat[j]), key, comps), PREDICTOR_MEMBOUND,
+                          ["floored"] if floored[j] else [])
+        return out
+
+    def predict_layer(self, layer: LayerSpec):
+        return self.predict_layers([layer])[0]
+
+
+def segment_fsum(values: np.ndarray, offsets: np.ndarray) -> np.ndarray:
+    """Per-segment correctly rounded sums on the GPU (== math.fsum)."""
+    from . import _device, _native
+    dev = _device.device()
+    v = _device.to_device(np.ascontiguousarray(values, dtype=np.float64), dev)
+    o = _device.to_device(np.ascontiguousarray(offsets, dtype=np.int64), dev)
+    nseg = len(offsets) - 1
+    out = _device.empty(max(nseg, 0), "float64", dev)
+    _native.check(_native.load().pm2l_segment_fsum(_native.ptr(v), _native.ptr(o), nseg,
+                                                   _native.ptr(out), _device.stream()),
+                  "pm2l_segment_fsum")
+    return _device.to_numpy(out)
+
+
+def predict_models(graphs: Sequence[ModelGraph], dataset: Dataset,
+                   wm: Optional[WaveModel] = None,
+                   membound_floor_us: float = DEFAULT_LAUNCH_FLOOR_US) -> List[ModelPrediction]:
+    """predict_model over many graphs with one device batch per stage."""
+    predictor = ModelPredictor(dataset, wm, membound_floor_us)
+    layers = [layer for g in graphs for layer in g.layers]
+    offsets = np.zeros(len(graphs) + 1, dtype=np.int64)
+    np.cumsum([len(g.layers) for g in graphs], out=offsets[1:])
+    res = predictor.predict_layers(layers)
+    totals = segment_fsum(np.array([r[0].latency_us for r in res], np.float64), offsets)
+    out = []
+    for gi, g in enumerate(graphs):
+        lo, hi = int(offsets[gi]), int(offsets[gi + 1])
+        per = tuple(LayerPrediction(layers[i].layer_id, res[i][0], res[i][1])
+                    for i in range(lo, hi))
+        flags = tuple((layers[i].layer_id, f) for i in range(lo, hi) for f in res[i][2])
+        out.append(ModelPrediction(g.model_name, float(totals[gi]), per, flags))
+    return out
+
+
+def predict_model(graph: ModelGraph, dataset: Dataset, wm: Optional[WaveModel] = None,
+                  membound_floor_us: float = DEFAULT_LAUNCH_FLOOR_US) -> ModelPrediction:
+    """Predict every layer and sum exactly (aggregate.py:173-196)."""
+    return predict_models([graph], dataset, wm, membound_floor_us)[0]

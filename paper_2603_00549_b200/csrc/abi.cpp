@@ -1,0 +1,493 @@
+// C entry points (include/pm2l.h): handle management, per-call staging,
+// device selection, and the reference-FFI drop-in pm2l_predict_grid_slice.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/pm2l.h"
+#include "pm2l_internal.h"
+
+using namespace pm2l;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(PM2L_ERR_CUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                                 cudaGetErrorString(e) + ")");
+}
+
+#define PM2L_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+  } while (0)
+
+// Growable device / pinned host buffers.
+struct DeviceBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t reserve(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    size_t want = std::max(need, size_t(4096));
+    cudaError_t e = cudaMalloc(&ptr, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+struct PinnedBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t reserve(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    size_t want = std::max(need, size_t(4096));
+    cudaError_t e = cudaMallocHost(&ptr, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+int check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(PM2L_ERR_NODEVICE,
+                "no CUDA device visible: the B200 build has no CPU fallback");
+  return PM2L_OK;
+}
+
+// libm log2 of every integer below kLutN, per device (explicit-descriptor mode).
+constexpr int64_t kLutN = int64_t(1) << 22;
+std::mutex g_lut_mu;
+std::unordered_map<int, double*> g_lut;
+
+int get_lut(int device, double** out) {
+  std::lock_guard<std::mutex> lk(g_lut_mu);
+  auto it = g_lut.find(device);
+  if (it != g_lut.end()) {
+    *out = it->second;
+    return PM2L_OK;
+  }
+  std::vector<double> host(kLutN);
+  host[0] = -INFINITY;
+  for (int64_t v = 1; v < kLutN; ++v) host[v] = std::log2(double(v));
+  double* d = nullptr;
+  PM2L_CUDA(cudaMalloc(&d, kLutN * sizeof(double)));
+  PM2L_CUDA(cudaMemcpy(d, host.data(), kLutN * sizeof(double), cudaMemcpyHostToDevice));
+  g_lut[device] = d;
+  *out = d;
+  return PM2L_OK;
+}
+
+}  // namespace
+
+struct pm2l_tables {
+  int device = 0;
+  TablesHost host;
+  TablesDev dev;
+  DeviceBuf blob;
+  // per-call staging (guarded by mu; reused once the previous call's work
+  // has drained, tracked by `done`)
+  std::mutex mu;
+  PinnedBuf grid_pinned;
+  DeviceBuf grid_dev;
+  DeviceBuf workspace;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+};
+
+namespace {
+
+int stage_grid(pm2l_tables* t, const uint64_t* const axes[4], const int64_t lens[4],
+               int64_t b_lo, int64_t b_hi, cudaStream_t s, GridDev* g) {
+  GridHost gh;
+  std::string err = build_grid(t->host, axes, lens, b_lo, b_hi, &gh);
+  if (!err.empty()) return fail(PM2L_ERR_INVALID, err);
+  if (t->pending) {
+    PM2L_CUDA(cudaEventSynchronize(t->done));
+    t->pending = false;
+  }
+  PM2L_CUDA(t->grid_pinned.reserve(gh.blob.size()));
+  PM2L_CUDA(t->grid_dev.reserve(gh.blob.size()));
+  std::memcpy(t->grid_pinned.ptr, gh.blob.data(), gh.blob.size());
+  PM2L_CUDA(cudaMemcpyAsync(t->grid_dev.ptr, t->grid_pinned.ptr, gh.blob.size(),
+                            cudaMemcpyHostToDevice, s));
+  *g = rebase(gh.dev_offsets, t->grid_dev.ptr);
+  return PM2L_OK;
+}
+
+int finish_call(pm2l_tables* t, cudaStream_t s) {
+  PM2L_CUDA(cudaEventRecord(t->done, s));
+  t->pending = true;
+  return PM2L_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int pm2l_abi_version(void) { return PM2L_ABI_VERSION; }
+
+const char* pm2l_last_error(void) { return g_error.c_str(); }
+
+int pm2l_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int pm2l_tables_create(const pm2l_tables_view* view, int device, pm2l_tables** out) {
+  if (!out) return fail(PM2L_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  if (int rc = check_device()) return rc;
+  std::unique_ptr<pm2l_tables> t(new pm2l_tables());
+  t->device = device;
+  std::string err = build_tables(view, &t->host);
+  if (!err.empty()) return fail(PM2L_ERR_INVALID, err);
+  DeviceGuard guard(device);
+  PM2L_CUDA(t->blob.reserve(std::max<size_t>(t->host.blob.size(), 256)));
+  if (!t->host.blob.empty())
+    PM2L_CUDA(cudaMemcpy(t->blob.ptr, t->host.blob.data(), t->host.blob.size(),
+                         cudaMemcpyHostToDevice));
+  t->dev = rebase(t->host.dev_offsets, t->blob.ptr);
+  PM2L_CUDA(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
+  *out = t.release();
+  return PM2L_OK;
+}
+
+int pm2l_tables_destroy(pm2l_tables* t) {
+  if (!t) return PM2L_OK;
+  {
+    DeviceGuard guard(t->device);
+    if (t->pending) cudaEventSynchronize(t->done);
+    if (t->done) cudaEventDestroy(t->done);
+    t->blob.release();
+    t->grid_dev.release();
+    t->workspace.release();
+    t->grid_pinned.release();
+  }
+  delete t;
+  return PM2L_OK;
+}
+
+int64_t pm2l_tables_groups(const pm2l_tables* t) { return t ? t->dev.G : -1; }
+
+int pm2l_grid_predict(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_batch,
+                      const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals, int64_t n_n,
+                      const uint64_t* k_vals, int64_t n_k, int64_t b_lo, int64_t b_hi,
+                      double* out_lat, int32_t* out_curve, uint64_t* out_blocks,
+                      uint64_t* out_waves, void* stream) {
+  if (!t) return fail(PM2L_ERR_INVALID, "null tables");
+  const bool any_v = out_curve || out_blocks || out_waves;
+  if (any_v && !(out_curve && out_blocks && out_waves))
+    return fail(PM2L_ERR_INVALID, "out_curve/out_blocks/out_waves must be all set or all NULL");
+  std::lock_guard<std::mutex> lk(t->mu);
+  DeviceGuard guard(t->device);
+  const uint64_t* axes[4] = {batch_vals, m_vals, n_vals, k_vals};
+  const int64_t lens[4] = {n_batch, n_m, n_n, n_k};
+  if (n_m * n_n * n_k * (b_hi - b_lo) > 0 && !out_lat)
+    return fail(PM2L_ERR_INVALID, "null out_lat");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GridDev g;
+  if (int rc = stage_grid(t, axes, lens, b_lo, b_hi, s, &g)) return rc;
+  const int64_t ws = grid_workspace_elems(t->dev, g);
+  if (ws > 0) PM2L_CUDA(t->workspace.reserve(size_t(ws) * sizeof(double)));
+  LaunchOut o{out_lat, out_curve, out_blocks, out_waves};
+  const int rc = launch_grid(t->dev, g, t->host.max_group,
+                             ws > 0 ? static_cast<double*>(t->workspace.ptr) : nullptr, ws, o, s);
+  if (rc) return cuda_fail(cudaError_t(rc), "grid kernel launch");
+  return finish_call(t, s);
+}
+
+struct pm2l_grid_plan {
+  pm2l_tables* tables = nullptr;
+  GridDev grid;
+  DeviceBuf blob;
+  DeviceBuf workspace;
+  int64_t ws_elems = 0;
+  int64_t staged_bytes = 0;
+};
+
+int pm2l_grid_plan_create(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_batch,
+                          const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals,
+                          int64_t n_n, const uint64_t* k_vals, int64_t n_k, int64_t b_lo,
+                          int64_t b_hi, pm2l_grid_plan** out) {
+  if (!t || !out) return fail(PM2L_ERR_INVALID, "null tables/output handle");
+  *out = nullptr;
+  DeviceGuard guard(t->device);
+  const uint64_t* axes[4] = {batch_vals, m_vals, n_vals, k_vals};
+  const int64_t lens[4] = {n_batch, n_m, n_n, n_k};
+  GridHost gh;
+  std::string err = build_grid(t->host, axes, lens, b_lo, b_hi, &gh);
+  if (!err.empty()) return fail(PM2L_ERR_INVALID, err);
+  std::unique_ptr<pm2l_grid_plan> p(new pm2l_grid_plan());
+  p->tables = t;
+  PM2L_CUDA(p->blob.reserve(gh.blob.size()));
+  PM2L_CUDA(cudaMemcpy(p->blob.ptr, gh.blob.data(), gh.blob.size(), cudaMemcpyHostToDevice));
+  p->grid = rebase(gh.dev_offsets, p->blob.ptr);
+  p->staged_bytes = int64_t(gh.blob.size());
+  p->ws_elems = grid_workspace_elems(t->dev, p->grid);
+  if (p->ws_elems > 0) PM2L_CUDA(p->workspace.reserve(size_t(p->ws_elems) * sizeof(double)));
+  *out = p.release();
+  return PM2L_OK;
+}
+
+int pm2l_grid_plan_launch(pm2l_grid_plan* p, double* out_lat, int32_t* out_curve,
+                          uint64_t* out_blocks, uint64_t* out_waves, uint64_t* nan_stats,
+                          int stages, void* stream) {
+  if (!p) return fail(PM2L_ERR_INVALID, "null plan");
+  const bool any_v = out_curve || out_blocks || out_waves;
+  if (any_v && !(out_curve && out_blocks && out_waves))
+    return fail(PM2L_ERR_INVALID, "out_curve/out_blocks/out_waves must be all set or all NULL");
+  const GridDev& g = p->grid;
+  if ((g.b_hi - g.b_lo) * g.nM * g.nN * g.nK > 0 && !out_lat)
+    return fail(PM2L_ERR_INVALID, "null out_lat");
+  DeviceGuard guard(p->tables->device);
+  LaunchOut o{out_lat, out_curve, out_blocks, out_waves,
+              reinterpret_cast<unsigned long long*>(nan_stats)};
+  const int rc = launch_grid(p->tables->dev, g, p->tables->host.max_group,
+                             p->ws_elems > 0 ? static_cast<double*>(p->workspace.ptr) : nullptr,
+                             p->ws_elems, o, stream, stages ? stages : kStageAll);
+  if (rc) return cuda_fail(cudaError_t(rc), "grid plan launch");
+  return PM2L_OK;
+}
+
+int pm2l_grid_plan_info(const pm2l_grid_plan* p, int64_t* info) {
+  if (!p || !info) return fail(PM2L_ERR_INVALID, "null plan/info");
+  const GridDev& g = p->grid;
+  info[0] = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
+  info[1] = g.n_fix;
+  info[2] = p->ws_elems * int64_t(sizeof(double));
+  info[3] = p->staged_bytes;
+  return PM2L_OK;
+}
+
+int pm2l_grid_plan_destroy(pm2l_grid_plan* p) {
+  if (!p) return PM2L_OK;
+  {
+    DeviceGuard guard(p->tables->device);
+    cudaDeviceSynchronize();
+    p->blob.release();
+    p->workspace.release();
+  }
+  delete p;
+  return PM2L_OK;
+}
+
+int pm2l_nan_scan(const double* lat, int64_t n, uint64_t* first, void* stream) {
+  if (n < 0 || (n > 0 && (!lat || !first))) return fail(PM2L_ERR_INVALID, "bad nan_scan args");
+  if (int rc = check_device()) return rc;
+  const int rc = launch_nan_scan(lat, n, reinterpret_cast<unsigned long long*>(first), stream);
+  if (rc) return cuda_fail(cudaError_t(rc), "nan scan launch");
+  return PM2L_OK;
+}
+
+int pm2l_grid_predict_all_curves(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_batch,
+                                 const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals,
+                                 int64_t n_n, const uint64_t* k_vals, int64_t n_k, int64_t b_lo,
+                                 int64_t b_hi, double* out_lat, void* stream) {
+  if (!t) return fail(PM2L_ERR_INVALID, "null tables");
+  std::lock_guard<std::mutex> lk(t->mu);
+  DeviceGuard guard(t->device);
+  const uint64_t* axes[4] = {batch_vals, m_vals, n_vals, k_vals};
+  const int64_t lens[4] = {n_batch, n_m, n_n, n_k};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GridDev g;
+  if (int rc = stage_grid(t, axes, lens, b_lo, b_hi, s, &g)) return rc;
+  const int64_t ws = int64_t(t->dev.C) * n_k;
+  PM2L_CUDA(t->workspace.reserve(size_t(std::max<int64_t>(ws, 1)) * sizeof(double)));
+  const int rc = launch_grid_all_curves(t->dev, g, static_cast<double*>(t->workspace.ptr),
+                                        out_lat, s);
+  if (rc) return cuda_fail(cudaError_t(rc), "all-curves kernel launch");
+  return finish_call(t, s);
+}
+
+int pm2l_points_predict(pm2l_tables* t, const uint32_t* shapes, int64_t n, double* out_lat,
+                        int32_t* out_curve, uint32_t* out_waves, int8_t* out_match,
+                        int32_t* out_record, double* out_dist, void* stream) {
+  if (!t) return fail(PM2L_ERR_INVALID, "null tables");
+  if (n < 0) return fail(PM2L_ERR_INVALID, "negative count");
+  if (n > 0 && (!shapes || !out_lat)) return fail(PM2L_ERR_INVALID, "null shapes/out_lat");
+  DeviceGuard guard(t->device);
+  double* lut = nullptr;
+  if (int rc = get_lut(t->device, &lut)) return rc;
+  const int rc = launch_points(t->dev, shapes, n, lut, kLutN, out_lat, out_curve, out_waves,
+                               out_match, out_record, out_dist, stream);
+  if (rc) return cuda_fail(cudaError_t(rc), "points kernel launch");
+  return PM2L_OK;
+}
+
+int pm2l_points_predict_curve(pm2l_tables* t, const uint32_t* shapes, const int32_t* curve_ids,
+                              int64_t n, double* out_lat, uint32_t* out_waves,
+                              double* out_detail, void* stream) {
+  if (!t) return fail(PM2L_ERR_INVALID, "null tables");
+  if (n < 0) return fail(PM2L_ERR_INVALID, "negative count");
+  if (n > 0 && (!shapes || !curve_ids || !out_lat))
+    return fail(PM2L_ERR_INVALID, "null shapes/curve_ids/out_lat");
+  DeviceGuard guard(t->device);
+  const int rc = launch_points_curve(t->dev, shapes, curve_ids, n, out_lat, out_waves, out_detail,
+                                     stream);
+  if (rc) return cuda_fail(cudaError_t(rc), "points-curve kernel launch");
+  return PM2L_OK;
+}
+
+int pm2l_membound_predict(const double* features, const int32_t* model_ids, int64_t n,
+                          const double* weights, const double* intercepts, const double* floors,
+                          int64_t n_models, double* out_lat, uint8_t* out_floored, void* stream) {
+  if (n < 0 || n_models < 0) return fail(PM2L_ERR_INVALID, "negative count");
+  if (n > 0 && (!features || !model_ids || !out_lat || !weights || !intercepts || !floors))
+    return fail(PM2L_ERR_INVALID, "null membound argument");
+  if (int rc = check_device()) return rc;
+  const int rc = launch_membound(features, model_ids, n, weights, intercepts, floors, n_models,
+                                 out_lat, out_floored, stream);
+  if (rc) return cuda_fail(cudaError_t(rc), "membound kernel launch");
+  return PM2L_OK;
+}
+
+int pm2l_segment_fsum(const double* values, const int64_t* offsets, int64_t n_segments,
+                      double* out_totals, void* stream) {
+  if (n_segments < 0) return fail(PM2L_ERR_INVALID, "negative count");
+  if (n_segments > 0 && (!values || !offsets || !out_totals))
+    return fail(PM2L_ERR_INVALID, "null fsum argument");
+  if (int rc = check_device()) return rc;
+  const int rc = launch_segment_fsum(values, offsets, n_segments, out_totals, stream);
+  if (rc) return cuda_fail(cudaError_t(rc), "fsum kernel launch");
+  return PM2L_OK;
+}
+
+// ------------------------------------------------------------------ drop-in
+namespace {
+
+uint64_t fnv(uint64_t h, const void* p, size_t n) {
+  const uint8_t* b = static_cast<const uint8_t*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+  return h;
+}
+
+struct SliceCache {
+  std::mutex mu;
+  std::unordered_map<uint64_t, pm2l_tables*> tables;  // (content hash ^ device) -> staged
+  std::unordered_map<int, DeviceBuf> out;             // per device output buffers
+  std::unordered_map<int, cudaStream_t> stream;
+};
+SliceCache g_slice;
+
+}  // namespace
+
+int pm2l_predict_grid_slice(
+    const uint64_t* batch_vals, int64_t n_batch, const uint64_t* m_vals, int64_t n_m,
+    const uint64_t* n_vals, int64_t n_n, const uint64_t* k_vals, int64_t n_k, int64_t b_lo,
+    int64_t b_hi, const uint64_t* exact_keys, const int64_t* exact_curve, int64_t n_records,
+    const double* log_m, const double* log_n, const double* log_k, const int64_t* cand_curve,
+    const int64_t* sample_offsets, const double* sample_dims, const double* sample_thrs,
+    int64_t n_curves, const double* ref_dim, const double* ref_dur, const double* ref_thr,
+    const double* ref_waves, const uint64_t* tile_m, const uint64_t* tile_n,
+    const uint64_t* split_k, const uint64_t* blocks_per_wave, const uint8_t* family_rowblock,
+    double* out) {
+  if (int rc = check_device()) return rc;
+  if (n_records < 0 || n_curves < 0 || !sample_offsets)
+    return fail(PM2L_ERR_INVALID, "bad table sizes");
+  int device = 0;
+  PM2L_CUDA(cudaGetDevice(&device));
+  pm2l_tables_view v{};
+  v.n_records = n_records;
+  v.exact_keys = exact_keys;
+  v.exact_curve = exact_curve;
+  v.log_m = log_m; v.log_n = log_n; v.log_k = log_k;
+  v.cand_curve = cand_curve;
+  v.n_curves = n_curves;
+  v.sample_offsets = sample_offsets;
+  v.sample_dims = sample_dims; v.sample_thrs = sample_thrs;
+  v.ref_dim = ref_dim; v.ref_dur = ref_dur; v.ref_thr = ref_thr; v.ref_waves = ref_waves;
+  v.tile_m = tile_m; v.tile_n = tile_n; v.split_k = split_k;
+  v.blocks_per_wave = blocks_per_wave; v.family_rowblock = family_rowblock;
+
+  const int64_t S = sample_offsets[n_curves];
+  uint64_t h = 0xcbf29ce484222325ull ^ uint64_t(device);
+  const size_t R = size_t(n_records), C = size_t(n_curves);
+  h = fnv(h, &n_records, 8); h = fnv(h, &n_curves, 8);
+  if (R) {
+    h = fnv(h, exact_keys, 8 * R); h = fnv(h, exact_curve, 8 * R);
+    h = fnv(h, log_m, 8 * R); h = fnv(h, log_n, 8 * R); h = fnv(h, log_k, 8 * R);
+    h = fnv(h, cand_curve, 8 * R);
+  }
+  h = fnv(h, sample_offsets, 8 * (C + 1));
+  if (S > 0) { h = fnv(h, sample_dims, 8 * S); h = fnv(h, sample_thrs, 8 * S); }
+  if (C) {
+    h = fnv(h, ref_dim, 8 * C); h = fnv(h, ref_dur, 8 * C); h = fnv(h, ref_thr, 8 * C);
+    h = fnv(h, ref_waves, 8 * C); h = fnv(h, tile_m, 8 * C); h = fnv(h, tile_n, 8 * C);
+    h = fnv(h, split_k, 8 * C); h = fnv(h, blocks_per_wave, 8 * C);
+    h = fnv(h, family_rowblock, C);
+  }
+
+  std::lock_guard<std::mutex> lk(g_slice.mu);
+  pm2l_tables*& t = g_slice.tables[h];
+  if (!t) {
+    if (int rc = pm2l_tables_create(&v, device, &t)) {
+      g_slice.tables.erase(h);
+      return rc;
+    }
+  }
+  cudaStream_t& s = g_slice.stream[device];
+  if (!s) PM2L_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const int64_t count = (b_hi - b_lo) * n_m * n_n * n_k;
+  if (count < 0) return fail(PM2L_ERR_INVALID, "batch slice out of range");
+  if (count == 0) return PM2L_OK;
+  if (!out) return fail(PM2L_ERR_INVALID, "null out");
+  DeviceBuf& ob = g_slice.out[device];
+  PM2L_CUDA(ob.reserve(size_t(count) * sizeof(double)));
+  double* d_out = static_cast<double*>(ob.ptr);
+  if (int rc = pm2l_grid_predict(t, batch_vals, n_batch, m_vals, n_m, n_vals, n_n, k_vals, n_k,
+                                 b_lo, b_hi, d_out, nullptr, nullptr, nullptr, s))
+    return rc;
+  PM2L_CUDA(cudaMemcpyAsync(out, d_out, size_t(count) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  PM2L_CUDA(cudaStreamSynchronize(s));
+  return PM2L_OK;
+}
+
+}  // extern "C"

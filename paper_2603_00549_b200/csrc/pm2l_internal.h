@@ -1,0 +1,128 @@
+// Internal layout shared by the host planner (tables.cpp, abi.cpp) and the
+// sm_100a kernels (kernels.cu).  Not part of the public ABI (include/pm2l.h).
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/pm2l.h"
+#include <string>
+#include <vector>
+
+namespace pm2l {
+
+// ---------------------------------------------------------------------------
+// HBM-resident staged tables of one (family, dtype, transpose) triple.
+//
+// Candidates are regrouped by their distinct log2(k) value ("k-groups"):
+// the nearest-config distance of candidate i is  max(D_i(m,n), |lk_i - qk|)
+// with D_i = max(|lm_i - qm|, |ln_i - qn|), so inside one group the k term is
+// shared and the argmin over the group reduces to a prefix-minimum staircase
+// of D_i over the candidates in scan order (built per (m, n) row in shared
+// memory).  Original scan indices are kept so ties break exactly as the
+// reference's strict '<' scan (_kernels.pyx:29-47).
+struct TablesDev {
+  int32_t R = 0;        // candidate records
+  int32_t C = 0;        // curves
+  int32_t G = 0;        // k-groups
+  int32_t n_exact = 0;  // exact records (== R)
+  int32_t all_gemm = 1; // no row-block curve referenced
+  int32_t n_samples = 0;
+  // per curve [C]
+  const double* ref_dim = nullptr;
+  const double* ref_dur = nullptr;
+  const double* ref_thr = nullptr;
+  const double* ref_waves = nullptr;
+  const uint64_t* tile_m = nullptr;
+  const uint64_t* tile_n = nullptr;
+  const uint64_t* split_k = nullptr;
+  const uint64_t* bpw = nullptr;     // blocks per wave (sm_count * blocks_per_sm)
+  const uint8_t* rowblock = nullptr;
+  const int32_t* s_off = nullptr;    // [C+1] sample offsets
+  const double* s_dims = nullptr;
+  const double* s_thrs = nullptr;
+  // candidates in group order [R]
+  const double* g_lm = nullptr;
+  const double* g_ln = nullptr;
+  const int32_t* g_idx = nullptr;    // original scan index
+  const int32_t* cand_curve = nullptr; // by ORIGINAL index [R]
+  // groups [G]
+  const double* grp_lk = nullptr;
+  const int32_t* grp_start = nullptr;
+  const int32_t* grp_size = nullptr;
+  // exact records [n_exact], unpacked, sorted by (b,m,n,k)
+  const uint64_t* ex_coord = nullptr; // 4 per record
+  const int32_t* ex_curve = nullptr;
+  const int32_t* ex_rec = nullptr;    // position in the caller's exact arrays
+};
+
+// Per-launch grid description (device pointers into one per-call upload).
+struct GridDev {
+  int64_t nB = 0, nM = 0, nN = 0, nK = 0;  // full axis lengths
+  int64_t b_lo = 0, b_hi = 0;              // slice of the batch axis
+  const uint64_t* B = nullptr;
+  const uint64_t* M = nullptr;
+  const uint64_t* N = nullptr;
+  const uint64_t* K = nullptr;
+  const double* logM = nullptr;   // libm log2 of each axis value (host computed)
+  const double* logN = nullptr;
+  const double* logK = nullptr;
+  // exact-hit fix-ups: slice-relative flat index + coordinates + curve
+  int64_t n_fix = 0;
+  const int64_t* fix_pos = nullptr;
+  const uint64_t* fix_coord = nullptr;  // 4 per fix-up
+  const int32_t* fix_curve = nullptr;
+};
+
+// Host-side image of the staged tables (one contiguous byte blob whose
+// internal pointers are rebased onto the device copy).
+struct TablesHost {
+  std::vector<uint8_t> blob;
+  TablesDev dev_offsets;  // pointers hold byte OFFSETS into blob
+  int64_t max_group = 0;
+};
+
+std::string build_tables(const pm2l_tables_view* v, TablesHost* out);
+TablesDev rebase(const TablesDev& offsets, const void* base);
+
+struct GridHost {
+  std::vector<uint8_t> blob;
+  GridDev dev_offsets;
+};
+std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
+                       const int64_t lens[4], int64_t b_lo, int64_t b_hi, GridHost* out);
+GridDev rebase(const GridDev& offsets, const void* base);
+
+// Kernel launchers (kernels.cu).  Return a CUDA error code (0 = success).
+struct LaunchOut {
+  double* lat = nullptr;
+  int32_t* curve = nullptr;
+  uint64_t* blocks = nullptr;
+  uint64_t* waves = nullptr;
+  // unresolved-point statistics: [0] = min slice-relative flat index of a NaN
+  // (UINT64_MAX if none), [1] = NaN count, [2] = dirty flag (an exact-hit
+  // fix-up removed a NaN; [0] must be re-derived by launch_nan_scan).
+  // Caller initialises to {UINT64_MAX, 0, 0}.
+  unsigned long long* nan_stats = nullptr;
+};
+enum : int { kStageBase = 1, kStageGrid = 2, kStageFixup = 4, kStageAll = 7 };
+int launch_grid(const TablesDev& t, const GridDev& g, int64_t max_group,
+                double* workspace, int64_t workspace_elems, const LaunchOut& out,
+                void* stream, int stages = kStageAll);
+int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g);
+int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* workspace,
+                           double* out, void* stream);
+int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n,
+                  const double* log_lut, int64_t lut_n, double* out_lat, int32_t* out_curve,
+                  uint32_t* out_waves, int8_t* out_match, int32_t* out_record, double* out_dist,
+                  void* stream);
+int launch_points_curve(const TablesDev& t, const uint32_t* shapes, const int32_t* curves,
+                        int64_t n, double* out_lat, uint32_t* out_waves, double* out_detail,
+                        void* stream);
+int launch_membound(const double* f, const int32_t* mid, int64_t n, const double* w,
+                    const double* b, const double* floors, int64_t n_models, double* out,
+                    uint8_t* floored, void* stream);
+int launch_nan_scan(const double* v, int64_t n, unsigned long long* first, void* stream);
+int launch_segment_fsum(const double* v, const int64_t* off, int64_t nseg, double* out,
+                        void* stream);
+
+}  // namespace pm2l

@@ -1,0 +1,283 @@
+// Host-side planner: turns the reference's flat tables (PreparedGrid.tables(),
+// pm2lat/nascache.py:174-241) into the HBM layout the sm_100a kernels use,
+// and builds the per-call grid description (axis values, host libm log2 of
+// every axis value, exact-hit fix-up list).
+//
+// Nothing here computes a latency; it only reorganises inputs.  log2 comes
+// from the host libm, exactly as the Cython kernel (_kernels.pyx:101,104,112)
+// and the Python resolver's math.log2 (compute.py:261) obtain it — device
+// log2 differs by an ulp on some integers and is never used.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/pm2l.h"
+#include "pm2l_internal.h"
+
+namespace pm2l {
+namespace {
+
+// Append-only byte blob with 256-byte aligned sections; section pointers are
+// recorded as offsets and rebased onto the device copy later.
+class Blob {
+ public:
+  template <class T>
+  const T* add(const T* src, size_t count) {
+    size_t off = (bytes_.size() + 255) & ~size_t(255);
+    bytes_.resize(off + count * sizeof(T));
+    if (count) std::memcpy(bytes_.data() + off, src, count * sizeof(T));
+    return reinterpret_cast<const T*>(off);
+  }
+  template <class T>
+  const T* add(const std::vector<T>& v) { return add(v.data(), v.size()); }
+  std::vector<uint8_t>& bytes() { return bytes_; }
+
+ private:
+  std::vector<uint8_t> bytes_;
+};
+
+template <class T>
+const T* shift(const T* off, const void* base) {
+  return reinterpret_cast<const T*>(static_cast<const uint8_t*>(base) +
+                                    reinterpret_cast<uintptr_t>(off));
+}
+
+}  // namespace
+
+std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
+  if (!v) return "null tables view";
+  const int64_t R = v->n_records, C = v->n_curves;
+  if (R < 0 || C < 0) return "negative table size";
+  if (R > (int64_t(1) << 30) || C > (int64_t(1) << 30)) return "tables too large";
+  if (R > 0 && (!v->log_m || !v->log_n || !v->log_k || !v->cand_curve || !v->exact_curve))
+    return "missing candidate arrays";
+  if (R > 0 && !v->exact_keys && !v->exact_coords) return "need exact_keys or exact_coords";
+  if (!v->sample_offsets) return "missing sample_offsets";
+  if (C > 0 && (!v->ref_dim || !v->ref_dur || !v->ref_thr || !v->ref_waves || !v->tile_m ||
+                !v->tile_n || !v->split_k || !v->blocks_per_wave || !v->family_rowblock))
+    return "missing curve arrays";
+  if (v->sample_offsets[0] != 0) return "sample_offsets[0] must be 0";
+  for (int64_t c = 0; c < C; ++c)
+    if (v->sample_offsets[c + 1] < v->sample_offsets[c]) return "sample_offsets not monotone";
+  const int64_t S = v->sample_offsets[C];
+  if (S > 0 && (!v->sample_dims || !v->sample_thrs)) return "missing samples";
+  if (S >= (int64_t(1) << 31)) return "too many samples";
+
+  std::vector<uint8_t> referenced(C, 0);
+  auto check_curve = [&](int64_t c) -> bool {
+    if (c < -1 || c >= C) return false;
+    if (c >= 0) referenced[c] = 1;
+    return true;
+  };
+  for (int64_t i = 0; i < R; ++i)
+    if (!check_curve(v->cand_curve[i]) || !check_curve(v->exact_curve[i]))
+      return "curve index out of range";
+  int32_t all_gemm = 1;
+  for (int64_t c = 0; c < C; ++c) {
+    if (!referenced[c]) continue;
+    if (v->sample_offsets[c + 1] - v->sample_offsets[c] < 1)
+      return "a referenced curve has no samples";
+    if (v->tile_m[c] < 1 || v->blocks_per_wave[c] < 1) return "tile_m and blocks_per_wave must be >= 1";
+    if (!v->family_rowblock[c] && (v->tile_n[c] < 1 || v->split_k[c] < 1))
+      return "tile_n and split_k must be >= 1";
+    if (!(v->ref_dim[c] > 0) || !(v->ref_waves[c] > 0)) return "ref_dim/ref_waves must be > 0";
+    if (v->family_rowblock[c]) all_gemm = 0;
+  }
+  for (int64_t i = 0; i < R; ++i)
+    if (!std::isfinite(v->log_m[i]) || !std::isfinite(v->log_n[i]) || !std::isfinite(v->log_k[i]))
+      return "candidate logs must be finite";
+
+  // --- k-groups: distinct log_k values ascending, members in scan order
+  std::vector<int32_t> order(R);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return v->log_k[a] < v->log_k[b]; });
+  std::vector<double> grp_lk, g_lm(R), g_ln(R);
+  std::vector<int32_t> grp_start, grp_size, g_idx(R);
+  int64_t max_group = 0;
+  for (int64_t p = 0; p < R; ++p) {
+    int32_t i = order[p];
+    if (p == 0 || v->log_k[i] != grp_lk.back()) {
+      grp_lk.push_back(v->log_k[i]);
+      grp_start.push_back(int32_t(p));
+      grp_size.push_back(0);
+    }
+    grp_size.back() += 1;
+    max_group = std::max<int64_t>(max_group, grp_size.back());
+    g_lm[p] = v->log_m[i];
+    g_ln[p] = v->log_n[i];
+    g_idx[p] = i;  // stable sort keeps ascending scan order inside a group
+  }
+  std::vector<int32_t> cand_curve(R);
+  for (int64_t i = 0; i < R; ++i) cand_curve[i] = int32_t(v->cand_curve[i]);
+
+  // --- exact records, unpacked and sorted by (b, m, n, k)
+  std::vector<std::array<uint64_t, 6>> ex(R);
+  for (int64_t i = 0; i < R; ++i) {
+    uint64_t b, m, n, k;
+    if (v->exact_coords) {
+      b = v->exact_coords[4 * i]; m = v->exact_coords[4 * i + 1];
+      n = v->exact_coords[4 * i + 2]; k = v->exact_coords[4 * i + 3];
+    } else {
+      const uint64_t key = v->exact_keys[i];  // nascache.py:188 packing
+      b = key >> 48; m = (key >> 32) & 0xFFFF; n = (key >> 16) & 0xFFFF; k = key & 0xFFFF;
+    }
+    ex[i] = {b, m, n, k, uint64_t(int64_t(v->exact_curve[i])), uint64_t(i)};
+  }
+  std::stable_sort(ex.begin(), ex.end(), [](const auto& a, const auto& b) {
+    return std::lexicographical_compare(a.begin(), a.begin() + 4, b.begin(), b.begin() + 4);
+  });
+  std::vector<uint64_t> ex_coord(4 * R);
+  std::vector<int32_t> ex_curve(R), ex_rec(R);
+  for (int64_t i = 0; i < R; ++i) {
+    for (int j = 0; j < 4; ++j) ex_coord[4 * i + j] = ex[i][j];
+    ex_curve[i] = int32_t(int64_t(ex[i][4]));
+    ex_rec[i] = int32_t(ex[i][5]);
+  }
+
+  std::vector<int32_t> s_off(C + 1);
+  for (int64_t c = 0; c <= C; ++c) s_off[c] = int32_t(v->sample_offsets[c]);
+  std::vector<uint8_t> rowblock(C);
+  for (int64_t c = 0; c < C; ++c) rowblock[c] = v->family_rowblock[c] ? 1 : 0;
+
+  Blob blob;
+  TablesDev& t = out->dev_offsets;
+  t = TablesDev{};
+  t.R = int32_t(R); t.C = int32_t(C); t.G = int32_t(grp_lk.size());
+  t.n_exact = int32_t(R); t.all_gemm = all_gemm; t.n_samples = int32_t(S);
+  t.ref_dim = blob.add(v->ref_dim, C);
+  t.ref_dur = blob.add(v->ref_dur, C);
+  t.ref_thr = blob.add(v->ref_thr, C);
+  t.ref_waves = blob.add(v->ref_waves, C);
+  t.tile_m = blob.add(v->tile_m, C);
+  t.tile_n = blob.add(v->tile_n, C);
+  t.split_k = blob.add(v->split_k, C);
+  t.bpw = blob.add(v->blocks_per_wave, C);
+  t.rowblock = blob.add(rowblock);
+  t.s_off = blob.add(s_off);
+  t.s_dims = blob.add(v->sample_dims, S);
+  t.s_thrs = blob.add(v->sample_thrs, S);
+  t.g_lm = blob.add(g_lm);
+  t.g_ln = blob.add(g_ln);
+  t.g_idx = blob.add(g_idx);
+  t.cand_curve = blob.add(cand_curve);
+  t.grp_lk = blob.add(grp_lk);
+  t.grp_start = blob.add(grp_start);
+  t.grp_size = blob.add(grp_size);
+  t.ex_coord = blob.add(ex_coord);
+  t.ex_curve = blob.add(ex_curve);
+  t.ex_rec = blob.add(ex_rec);
+  out->blob.swap(blob.bytes());
+  out->max_group = max_group;
+  return "";
+}
+
+TablesDev rebase(const TablesDev& o, const void* base) {
+  TablesDev t = o;
+  t.ref_dim = shift(o.ref_dim, base); t.ref_dur = shift(o.ref_dur, base);
+  t.ref_thr = shift(o.ref_thr, base); t.ref_waves = shift(o.ref_waves, base);
+  t.tile_m = shift(o.tile_m, base); t.tile_n = shift(o.tile_n, base);
+  t.split_k = shift(o.split_k, base); t.bpw = shift(o.bpw, base);
+  t.rowblock = shift(o.rowblock, base); t.s_off = shift(o.s_off, base);
+  t.s_dims = shift(o.s_dims, base); t.s_thrs = shift(o.s_thrs, base);
+  t.g_lm = shift(o.g_lm, base); t.g_ln = shift(o.g_ln, base);
+  t.g_idx = shift(o.g_idx, base); t.cand_curve = shift(o.cand_curve, base);
+  t.grp_lk = shift(o.grp_lk, base); t.grp_start = shift(o.grp_start, base);
+  t.grp_size = shift(o.grp_size, base);
+  t.ex_coord = shift(o.ex_coord, base); t.ex_curve = shift(o.ex_curve, base);
+  t.ex_rec = shift(o.ex_rec, base);
+  return t;
+}
+
+std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
+                       const int64_t lens[4], int64_t b_lo, int64_t b_hi, GridHost* out) {
+  for (int a = 0; a < 4; ++a) {
+    if (lens[a] < 0) return "negative axis length";
+    if (lens[a] > 0 && !axes[a]) return "null axis array";
+    for (int64_t i = 0; i < lens[a]; ++i)
+      if (axes[a][i] == 0) return "grid coordinates must be >= 1";
+  }
+  if (b_lo < 0 || b_hi < b_lo || b_hi > lens[0]) return "batch slice out of range";
+  const int64_t nM = lens[1], nN = lens[2], nK = lens[3];
+  std::vector<double> logs[3];
+  for (int a = 1; a < 4; ++a) {
+    logs[a - 1].resize(lens[a]);
+    for (int64_t i = 0; i < lens[a]; ++i) logs[a - 1][i] = std::log2(double(axes[a][i]));
+  }
+
+  // exact-hit fix-ups: every grid point whose (b, m, n, k) equals a recorded
+  // shape takes the recorded kernel (_kernels.pyx:107-110) instead of the
+  // nearest one.  Axes may contain duplicates (the raw FFI allows it), so
+  // each value maps to all of its indices.
+  std::unordered_multimap<uint64_t, int64_t> where[4];
+  for (int a = 0; a < 4; ++a) {
+    int64_t lo = a == 0 ? b_lo : 0, hi = a == 0 ? b_hi : lens[a];
+    for (int64_t i = lo; i < hi; ++i) where[a].emplace(axes[a][i], i);
+  }
+  const TablesDev& t = th.dev_offsets;
+  const uint64_t* exc = reinterpret_cast<const uint64_t*>(
+      th.blob.data() + reinterpret_cast<uintptr_t>(t.ex_coord));
+  const int32_t* exv = reinterpret_cast<const int32_t*>(
+      th.blob.data() + reinterpret_cast<uintptr_t>(t.ex_curve));
+  std::map<int64_t, std::pair<std::array<uint64_t, 4>, int32_t>> fix;
+  for (int32_t r = 0; r < t.n_exact; ++r) {
+    const uint64_t* c = exc + 4 * r;
+    auto rb = where[0].equal_range(c[0]);
+    if (rb.first == rb.second) continue;
+    auto rm = where[1].equal_range(c[1]);
+    if (rm.first == rm.second) continue;
+    auto rn = where[2].equal_range(c[2]);
+    if (rn.first == rn.second) continue;
+    auto rk = where[3].equal_range(c[3]);
+    for (auto ib = rb.first; ib != rb.second; ++ib)
+      for (auto im = rm.first; im != rm.second; ++im)
+        for (auto jn = rn.first; jn != rn.second; ++jn)
+          for (auto ik = rk.first; ik != rk.second; ++ik) {
+            int64_t pos = (((ib->second - b_lo) * nM + im->second) * nN + jn->second) * nK +
+                          ik->second;
+            fix[pos] = {{c[0], c[1], c[2], c[3]}, exv[r]};
+          }
+  }
+  std::vector<int64_t> fix_pos;
+  std::vector<uint64_t> fix_coord;
+  std::vector<int32_t> fix_curve;
+  for (auto& [pos, val] : fix) {
+    fix_pos.push_back(pos);
+    for (int j = 0; j < 4; ++j) fix_coord.push_back(val.first[j]);
+    fix_curve.push_back(val.second);
+  }
+
+  Blob blob;
+  GridDev& g = out->dev_offsets;
+  g = GridDev{};
+  g.nB = lens[0]; g.nM = nM; g.nN = nN; g.nK = nK; g.b_lo = b_lo; g.b_hi = b_hi;
+  g.B = blob.add(axes[0], lens[0]);
+  g.M = blob.add(axes[1], nM);
+  g.N = blob.add(axes[2], nN);
+  g.K = blob.add(axes[3], nK);
+  g.logM = blob.add(logs[0]);
+  g.logN = blob.add(logs[1]);
+  g.logK = blob.add(logs[2]);
+  g.n_fix = int64_t(fix_pos.size());
+  g.fix_pos = blob.add(fix_pos);
+  g.fix_coord = blob.add(fix_coord);
+  g.fix_curve = blob.add(fix_curve);
+  out->blob.swap(blob.bytes());
+  return "";
+}
+
+GridDev rebase(const GridDev& o, const void* base) {
+  GridDev g = o;
+  g.B = shift(o.B, base); g.M = shift(o.M, base); g.N = shift(o.N, base);
+  g.K = shift(o.K, base); g.logM = shift(o.logM, base); g.logN = shift(o.logN, base);
+  g.logK = shift(o.logK, base); g.fix_pos = shift(o.fix_pos, base);
+  g.fix_coord = shift(o.fix_coord, base); g.fix_curve = shift(o.fix_curve, base);
+  return g;
+}
+
+}  // namespace pm2l
