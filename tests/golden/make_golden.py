@@ -82,12 +82,19 @@ def main():
     }
     datasets["fp32_full"] = oracle.with_membound_fixture(datasets["fp32"], count=32, seed=23)
     fingerprints = {}
-    for name, ds in datasets.items():
+    from pm2lat.ingest import load_dataset
+    for name, ds in list(datasets.items()):
         obj = dataset_to_json_obj(ds)
-        with open(os.path.join(HERE, "datasets", f"{name}.json"), "w") as fh:
+        path = os.path.join(HERE, "datasets", f"{name}.json")
+        with open(path, "w") as fh:
             json.dump(obj, fh, sort_keys=True, separators=(",", ":"))
             fh.write("\n")
         fingerprints[name] = ds.fingerprint()
+        # every golden below is computed from the dataset AS LOADED from the
+        # committed file (canonical record order), exactly what a consumer of
+        # the shipped tables -- and the B200 build's tests -- see
+        datasets[name] = load_dataset(path)
+        assert datasets[name].fingerprint() == fingerprints[name]
 
     # ------------------------------------------------------------ grids
     def rng_axes(seed, nb, nm, nn, nk, lo=1, hi=20000):

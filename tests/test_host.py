@@ -208,3 +208,18 @@ def test_cpu_host_has_no_fallback():
     assert _native.load().pm2l_predict_grid_slice(
         *([None, 0] * 4), 0, 0, None, None, 0, None, None, None, None, None, None, None, 0,
         None, None, None, None, None, None, None, None, None, None) == _native.PM2L_ERR_NODEVICE
+
+
+def test_membound_fit_matches_reference_fit():
+    """The on-demand OLS refit used by predict_model reproduces the
+    reference's fitted weights bit for bit (same numpy/LAPACK)."""
+    from conftest import golden_npz
+    from paper_2603_00549_b200.aggregate import ModelPredictor
+    from paper_2603_00549_b200.core import DType
+    z = golden_npz("membound")
+    mp = ModelPredictor(dataset("fp32_full"))
+    for i, name in enumerate(("softmax", "gelu", "add")):
+        m = mp.membound_model(name, DType.FP32)
+        assert np.array_equal(np.array(m.weights), z["weights"][i])
+        assert m.intercept == z["intercept"][i]
+        assert m.max_rel_err == z["max_rel_err"][i]
