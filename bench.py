@@ -129,6 +129,11 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def wait_first_sample(self, timeout: float = 5.0):
+        t_end = time.perf_counter() + timeout
+        while self.proc is not None and not self.lines and time.perf_counter() < t_end:
+            time.sleep(0.02)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
@@ -159,7 +164,8 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window": "timed steps + 1 s soak of the same step"}
 
 
 def measured_peak_hbm():
@@ -247,6 +253,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
+        clk.wait_first_sample()
         for k in range(args.steps):
             flush.zero_()
             step(events[k])
@@ -254,6 +261,15 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        # the timed steps last ~1 ms, shorter than nvidia-smi's sampling
+        # period: keep the same step running for a 1 s soak so the samples
+        # reflect the clocks under this load
+        t_end = time.perf_counter() + 1.0
+        while time.perf_counter() < t_end:
+            for _ in range(50):
+                flush.zero_()
+                step()
+            torch.cuda.synchronize()
     step_ms = [e[0].elapsed_time(e[3]) for e in events]
     grid_ms = [e[1].elapsed_time(e[2]) for e in events]
     base_ms = [e[0].elapsed_time(e[1]) for e in events]

@@ -124,7 +124,17 @@ struct GridLaunch {
 };
 
 struct SmemLayout {
-  int64_t off_D, off_sD, off_sI, off_gMin, off_gLk, off_gStart, off_gLen, off_T, off_W, total;
+  int64_t off_D, off_sD, off_sI, off_grp, off_T, off_W, total;
+};
+
+// Per-row, per-k-group state in shared memory (32 B: one LDS.128 reads lk+dmin).
+struct __align__(16) GroupRow {
+  double lk;        // log2 k of the group
+  uint64_t dmin;    // min over members of D_i(m, n) (as ordered bits)
+  int32_t sstart;   // staircase start (== group start in group order)
+  int32_t last;     // scan index of the first member attaining dmin
+  int32_t len;      // staircase length
+  int32_t pad;
 };
 
 __host__ __device__ inline SmemLayout smem_layout(int R, int G, int C, int64_t bper, int mode) {
@@ -138,10 +148,7 @@ __host__ __device__ inline SmemLayout smem_layout(int R, int G, int C, int64_t b
   L.off_D = take(8ll * R);
   L.off_sD = take(8ll * R);
   L.off_sI = take(4ll * R);
-  L.off_gMin = take(8ll * G);
-  L.off_gLk = take(8ll * G);
-  L.off_gStart = take(4ll * G);
-  L.off_gLen = take(4ll * G);
+  L.off_grp = take(int64_t(sizeof(GroupRow)) * G);
   L.off_T = take(mode <= 1 ? 8ll * C : 0);
   L.off_W = take(mode == 0 ? 8ll * C * bper : 0);
   L.total = o;
@@ -149,36 +156,64 @@ __host__ __device__ inline SmemLayout smem_layout(int R, int G, int C, int64_t b
 }
 
 // Nearest-config argmin for one query k given the row's staircases.
-// Returns the ORIGINAL candidate scan index (or INT32_MAX when R == 0).
-__device__ __forceinline__ int nearest_in_row(int G, double qk, const uint64_t* __restrict__ sD,
-                                              const int32_t* __restrict__ sI,
-                                              const uint64_t* __restrict__ gMin,
-                                              const double* __restrict__ gLk,
-                                              const int32_t* __restrict__ gStart) {
-  uint64_t best_d = ~0ull;
+//
+// dist(i) = max(D_i, dk_g(i)) with dk_g = |lk_g - qk|.  Groups are sorted by
+// lk, so dk_g grows monotonically (IEEE subtraction is monotone) when moving
+// away from qk's insertion point `start`: sweep right, then left, stopping a
+// side as soon as dk_g exceeds the running best (no member of that group or
+// any farther group can reach it).  The minimum scan index among all members
+// attaining the final best is then read off the staircases of the tying
+// groups: the first staircase entry with D <= best (O(1) when best == dmin).
+// Returns the ORIGINAL candidate scan index (INT32_MAX when G == 0).
+__device__ __forceinline__ int stair_index(const GroupRow& gr, uint64_t best,
+                                           const uint64_t* __restrict__ sD,
+                                           const int32_t* __restrict__ sI) {
+  if (best == gr.dmin) return gr.last;
+  int s = gr.sstart;
+  while (sD[s] > best) ++s;
+  return sI[s];
+}
+
+template <bool G32>
+__device__ __forceinline__ int nearest_in_row(int G, double qk, int start,
+                                              const GroupRow* __restrict__ grp,
+                                              const uint64_t* __restrict__ sD,
+                                              const int32_t* __restrict__ sI) {
+  uint64_t best = ~0ull;
+  uint32_t mask = 0;
   int best_i = 0x7FFFFFFF;
-  for (int g = 0; g < G; ++g) {
-    const uint64_t dk = abs_bits(__dsub_rn(gLk[g], qk));
-    const uint64_t gm = gMin[g];
+  auto visit = [&](int g) -> bool {
+    const double2 lkd = *reinterpret_cast<const double2*>(&grp[g]);
+    const uint64_t dk = abs_bits(__dsub_rn(lkd.x, qk));
+    if (dk > best) return false;
+    const uint64_t gm = static_cast<uint64_t>(__double_as_longlong(lkd.y));
     const uint64_t dg = dk > gm ? dk : gm;
-    if (dg <= best_d) {
-      // first staircase entry with D <= dg: the smallest scan index of this
-      // group whose distance max(D_i, dk) equals dg (the group minimum)
-      int s = gStart[g];
-      while (sD[s] > dg) ++s;
-      const int idx = sI[s];
-      if (dg < best_d) {
-        best_d = dg;
-        best_i = idx;
-      } else if (idx < best_i) {
-        best_i = idx;
-      }
+    if (G32) {
+      if (dg < best) { best = dg; mask = 1u << g; }
+      else if (dg == best) mask |= 1u << g;
+    } else if (dg <= best) {
+      const int idx = stair_index(grp[g], dg, sD, sI);
+      if (dg < best || idx < best_i) best_i = idx;
+      best = dg;
+    }
+    return true;
+  };
+  for (int g = start; g < G; ++g)
+    if (!visit(g)) break;
+  for (int g = start - 1; g >= 0; --g)
+    if (!visit(g)) break;
+  if (G32) {
+    while (mask) {
+      const int g = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int idx = stair_index(grp[g], best, sD, sI);
+      best_i = idx < best_i ? idx : best_i;
     }
   }
   return best_i;
 }
 
-template <bool VERIFY, int MODE>
+template <bool VERIFY, int MODE, bool G32>
 __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
                                                         const double* __restrict__ base_tab,
                                                         LaunchOut out) {
@@ -187,10 +222,7 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
   uint64_t* sDv = reinterpret_cast<uint64_t*>(smem + L.off_D);
   uint64_t* sD = reinterpret_cast<uint64_t*>(smem + L.off_sD);
   int32_t* sI = reinterpret_cast<int32_t*>(smem + L.off_sI);
-  uint64_t* gMin = reinterpret_cast<uint64_t*>(smem + L.off_gMin);
-  double* gLk = reinterpret_cast<double*>(smem + L.off_gLk);
-  int32_t* gStart = reinterpret_cast<int32_t*>(smem + L.off_gStart);
-  int32_t* gLen = reinterpret_cast<int32_t*>(smem + L.off_gLen);
+  GroupRow* grp = reinterpret_cast<GroupRow*>(smem + L.off_grp);
   uint64_t* Tmn = reinterpret_cast<uint64_t*>(smem + L.off_T);
   double* W = reinterpret_cast<double*>(smem + L.off_W);
 
@@ -214,8 +246,8 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
     sDv[j] = a > b ? a : b;
   }
   for (int j = tid; j < t.G; j += blockDim.x) {
-    gLk[j] = t.grp_lk[j];
-    gStart[j] = t.grp_start[j];
+    grp[j].lk = t.grp_lk[j];
+    grp[j].sstart = t.grp_start[j];
   }
   if (MODE <= 1) {
     for (int c = tid; c < t.C; c += blockDim.x)
@@ -253,9 +285,11 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
       const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
       if (tail < carry) carry = tail;
     }
+    __syncwarp();
     if (lane == 0) {
-      gMin[gi] = carry;
-      gLen[gi] = len;
+      grp[gi].dmin = carry;
+      grp[gi].len = len;
+      grp[gi].last = len ? sI[start + len - 1] : 0x7FFFFFFF;
     }
   }
   // 3. wave-scale table: W[ib][c] = waves(b, m, n, c) / ref_waves[c]
@@ -280,7 +314,7 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
     const int64_t ik = k0 + int64_t(j) * blockDim.x + tid;
     if (ik >= g.nK) break;
     const double qk = g.logK[ik];
-    const int best = nearest_in_row(t.G, qk, sD, sI, gMin, gLk, gStart);
+    const int best = nearest_in_row<G32>(t.G, qk, g.kstart[ik], grp, sD, sI);
     const int ci = (best < t.R) ? t.cand_curve[best] : -1;
     double* o = out.lat + (ib0 - g.b_lo) * plane + row_off + ik;
     if (ci < 0) {
@@ -759,7 +793,7 @@ int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g) {
 template <bool V, int M>
 static cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
                                  const double* base, const LaunchOut& out, cudaStream_t s) {
-  auto* fn = grid_kernel<V, M>;
+  auto* fn = t.G <= 32 ? grid_kernel<V, M, true> : grid_kernel<V, M, false>;
   if (gl.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gl.smem));
     if (e != cudaSuccess) return e;

@@ -66,6 +66,7 @@ struct GridDev {
   const double* logM = nullptr;   // libm log2 of each axis value (host computed)
   const double* logN = nullptr;
   const double* logK = nullptr;
+  const int32_t* kstart = nullptr;  // per k: #groups with grp_lk < logK (sweep start)
   // exact-hit fix-ups: slice-relative flat index + coordinates + curve
   int64_t n_fix = 0;
   const int64_t* fix_pos = nullptr;

@@ -210,6 +210,14 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
     for (int64_t i = 0; i < lens[a]; ++i) logs[a - 1][i] = std::log2(double(axes[a][i]));
   }
 
+  // per k: insertion point of log2(k) among the (ascending) group lk values
+  const TablesDev& tt = th.dev_offsets;
+  const double* glk = reinterpret_cast<const double*>(
+      th.blob.data() + reinterpret_cast<uintptr_t>(tt.grp_lk));
+  std::vector<int32_t> kstart(nK);
+  for (int64_t i = 0; i < nK; ++i)
+    kstart[i] = int32_t(std::lower_bound(glk, glk + tt.G, logs[2][i]) - glk);
+
   // exact-hit fix-ups: every grid point whose (b, m, n, k) equals a recorded
   // shape takes the recorded kernel (_kernels.pyx:107-110) instead of the
   // nearest one.  Axes may contain duplicates (the raw FFI allows it), so
@@ -263,6 +271,7 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   g.logM = blob.add(logs[0]);
   g.logN = blob.add(logs[1]);
   g.logK = blob.add(logs[2]);
+  g.kstart = blob.add(kstart);
   g.n_fix = int64_t(fix_pos.size());
   g.fix_pos = blob.add(fix_pos);
   g.fix_coord = blob.add(fix_coord);
@@ -275,7 +284,8 @@ GridDev rebase(const GridDev& o, const void* base) {
   GridDev g = o;
   g.B = shift(o.B, base); g.M = shift(o.M, base); g.N = shift(o.N, base);
   g.K = shift(o.K, base); g.logM = shift(o.logM, base); g.logN = shift(o.logN, base);
-  g.logK = shift(o.logK, base); g.fix_pos = shift(o.fix_pos, base);
+  g.logK = shift(o.logK, base); g.kstart = shift(o.kstart, base);
+  g.fix_pos = shift(o.fix_pos, base);
   g.fix_coord = shift(o.fix_coord, base); g.fix_curve = shift(o.fix_curve, base);
   return g;
 }

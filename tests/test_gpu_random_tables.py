@@ -1,0 +1,110 @@
+"""Randomised tables (not from a dataset): many k-groups (> 32 exercises the
+general nearest path), coordinate lattices that force distance ties, records
+whose kernel has no curve (NaN), row-block and GEMM curves — GPU grid and
+explicit-descriptor kernels against the C oracle, bit for bit."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def random_tables(rng, R, C, n_k_values, rowblock=False, wide=False):
+    pool_m = rng.choice(np.arange(1, 5000), size=12, replace=False)
+    pool_n = rng.choice(np.arange(1, 5000), size=12, replace=False)
+    pool_k = rng.choice(np.arange(1, 70000 if wide else 20000), size=n_k_values, replace=False)
+    coords = set()
+    while len(coords) < R:
+        coords.add((int(rng.integers(1, 5)), int(rng.choice(pool_m)), int(rng.choice(pool_n)),
+                    int(rng.choice(pool_k))))
+    coords = sorted(coords, key=lambda c: (c[1], c[2], c[3], c[0]))
+    co = np.array(coords, np.uint64)
+    cand = rng.integers(-1, C, size=R).astype(np.int64)   # some kernels without curves
+    t = {"exact_coords": co, "exact_coords_curve": cand.copy(), "cand_curve": cand,
+         "log_m": np.log2(co[:, 1].astype(np.float64)), "log_n": np.log2(co[:, 2].astype(np.float64)),
+         "log_k": np.log2(co[:, 3].astype(np.float64))}
+    import math
+    for name, col in (("log_m", 1), ("log_n", 2), ("log_k", 3)):
+        t[name] = np.array([math.log2(int(v)) for v in co[:, col]], np.float64)
+    offs = [0]
+    dims, thrs = [], []
+    for c in range(C):
+        ns = int(rng.integers(2, 12))
+        d = np.sort(rng.choice(np.arange(1, 20000), size=ns, replace=False)).astype(np.float64)
+        dims += list(d)
+        thrs += list(rng.uniform(1.0, 900.0, ns))
+        offs.append(len(dims))
+    t.update(sample_offsets=np.array(offs, np.int64), sample_dims=np.array(dims),
+             sample_thrs=np.array(thrs),
+             ref_dim=np.array([dims[offs[c + 1] - 1] for c in range(C)]),
+             ref_dur=rng.uniform(1.0, 500.0, C), ref_waves=rng.integers(1, 9, C).astype(np.float64),
+             tile_m=rng.choice([16, 32, 64, 128, 256], C).astype(np.uint64),
+             tile_n=rng.choice([16, 32, 64, 128, 256], C).astype(np.uint64),
+             split_k=rng.choice([1, 1, 2, 4], C).astype(np.uint64),
+             blocks_per_wave=rng.choice([30, 132, 148, 296], C).astype(np.uint64),
+             family_rowblock=np.full(C, 1 if rowblock else 0, np.uint8))
+    t["ref_thr"] = np.array([thrs[offs[c + 1] - 1] for c in range(C)])
+    t["exact_keys"] = None
+    return t, pool_m, pool_n, pool_k
+
+
+@pytest.mark.parametrize("seed,R,C,nkv,rowblock", [
+    (1, 40, 5, 3, False), (2, 300, 20, 40, False), (3, 900, 60, 120, False),
+    (4, 200, 7, 9, True), (5, 64, 3, 64, False), (6, 1500, 30, 33, False)])
+def test_random_tables_grid(gpu, seed, R, C, nkv, rowblock):
+    import torch
+    from paper_2603_00549_b200 import _native
+    rng = np.random.default_rng(seed)
+    t, pm, pn, pk = random_tables(rng, R, C, nkv, rowblock)
+    dt = _native.DeviceTables(t, 0)
+    # axes mix recorded values (exact hits, exact distance ties) and others
+    B = np.array(sorted({1, 2, 3, 4, 7}), np.uint64)
+    M = np.array(sorted(set(rng.choice(pm, 5).tolist()) | set(rng.integers(1, 6000, 5).tolist())), np.uint64)
+    N = np.array(sorted(set(rng.choice(pn, 5).tolist()) | set(rng.integers(1, 6000, 5).tolist())), np.uint64)
+    K = np.array(sorted(set(rng.choice(pk, 30).tolist()) | set(rng.integers(1, 30000, 300).tolist())), np.uint64)
+    plan = _native.GridPlan(dt, (B, M, N, K))
+    n = plan.cardinality
+    dev = torch.device("cuda")
+    lat = torch.empty(n, dtype=torch.float64, device=dev)
+    cur = torch.empty(n, dtype=torch.int32, device=dev)
+    blk = torch.empty(n, dtype=torch.int64, device=dev)
+    wav = torch.empty(n, dtype=torch.int64, device=dev)
+    stats = torch.tensor([-1, 0, 0], dtype=torch.int64, device=dev)
+    plan.launch(lat, cur, blk, wav, nan_stats=stats)
+    o_lat, o_cur, o_blk, o_wav = oracle.grid(t, (B, M, N, K), use_coords=True)
+    assert np.array_equal(lat.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+    assert np.array_equal(cur.cpu().numpy(), o_cur)
+    assert np.array_equal(wav.cpu().numpy().view(np.uint64), o_wav)
+    assert np.array_equal(blk.cpu().numpy().view(np.uint64), o_blk)
+    fast = torch.empty(n, dtype=torch.float64, device=dev)
+    stats2 = torch.tensor([-1, 0, 0], dtype=torch.int64, device=dev)
+    plan.launch(fast, nan_stats=stats2)
+    assert np.array_equal(fast.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+    nan = np.isnan(o_lat)
+    for st in (stats, stats2):
+        st = st.cpu().numpy()
+        assert st[1] == nan.sum()
+        first = int(np.argmax(nan)) if nan.any() else -1
+        if st[2] == 0:
+            assert st[0] == first
+    # explicit-descriptor kernel on the same tables
+    pts = np.array(np.meshgrid(B, M, N, K, indexing="ij")).reshape(4, -1).T.astype(np.uint32)
+    sel = rng.choice(len(pts), min(len(pts), 5000), replace=False)
+    shapes = np.ascontiguousarray(pts[sel])
+    d_s = torch.from_numpy(shapes).to(dev)
+    m = len(sel)
+    outs = [torch.empty(m, dtype=dt_, device=dev) for dt_ in
+            (torch.float64, torch.int32, torch.int32, torch.int8, torch.int32, torch.float64)]
+    _native.check(_native.load().pm2l_points_predict(
+        dt.handle, d_s.data_ptr(), m, *[o.data_ptr() for o in outs], _native.stream_handle()),
+        "points")
+    ref = oracle.points(t, shapes)
+    got = [o.cpu().numpy() for o in outs]
+    assert np.array_equal(got[0].view(np.uint64), ref[0].view(np.uint64))
+    assert np.array_equal(got[1], ref[1])
+    assert np.array_equal(got[3], ref[3])
+    assert np.array_equal(got[4], ref[4])
+    assert np.array_equal(got[5].view(np.uint64), ref[5].view(np.uint64))
+    assert dt.groups == len(np.unique(t["log_k"]))
