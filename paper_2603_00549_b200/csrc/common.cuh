@@ -1,0 +1,108 @@
+// Device helpers shared by the sm_100a kernels: the reference's canonical
+// per-point arithmetic (pm2lat/compute.py:78-138, _kernels.pyx:50-73,119-132).
+//
+// Every FP64 operation on the latency path is an explicit round-to-nearest
+// intrinsic (__dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn), which nvcc never
+// contracts into DFMA; the library is also built with -fmad=false.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pm2l_internal.h"
+
+namespace pm2l {
+namespace dev {
+
+constexpr uint64_t kAbsMask = 0x7FFFFFFFFFFFFFFFull;
+constexpr long long kQuietNaN = 0x7FF8000000000000ll;  // the reference's NAN bits
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(kQuietNaN); }
+
+// |x| as ordered integer bits (for x finite, compare == double compare)
+__device__ __forceinline__ uint64_t abs_bits(double x) {
+  return static_cast<uint64_t>(__double_as_longlong(x)) & kAbsMask;
+}
+
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+// (a + b - 1) / b in u64 exactly as the Cython kernel writes it
+// (_kernels.pyx:124,126,127); 32-bit hardware path when both operands fit.
+__device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) {
+  const uint64_t num = a + b - 1;
+  if ((num | b) <= 0xFFFFFFFFull) return uint64_t(uint32_t(num) / uint32_t(b));
+  return num / b;
+}
+
+// compute._interpolate_detail / _kernels._interp over samples [lo, hi):
+// clamp outside the sampled range, exact at samples, linear between
+// neighbours: t = (k - k1) / (k3 - k1); thr = t1 + t * (t3 - t1)  (no FMA).
+__device__ __forceinline__ double interp_samples(const double* __restrict__ d,
+                                                 const double* __restrict__ y, int lo, int hi,
+                                                 double nd) {
+  if (nd < d[lo]) return y[lo];
+  if (nd > d[hi - 1]) return y[hi - 1];
+  int left = lo, right = hi;
+  while (left < right) {
+    const int mid = (left + right) >> 1;
+    if (d[mid] < nd) left = mid + 1; else right = mid;
+  }
+  if (d[left] == nd) return y[left];
+  const double k1 = d[left - 1], k3 = d[left], t1 = y[left - 1], t3 = y[left];
+  const double tt = __ddiv_rn(__dsub_rn(nd, k1), __dsub_rn(k3, k1));
+  return __dadd_rn(t1, __dmul_rn(tt, __dsub_rn(t3, t1)));
+}
+
+__device__ __forceinline__ double interp_thr(const TablesDev& t, int c, double nd) {
+  return interp_samples(t.s_dims, t.s_thrs, t.s_off[c], t.s_off[c + 1], nd);
+}
+
+// compute._rescale first factor — depends on (curve, k) only:
+// base = (ref_dur * (k / ref_dim)) * (ref_thr / thr(k))   (left-associative)
+__device__ __forceinline__ double base_from_thr(const TablesDev& t, int c, double nd, double thr) {
+  return __dmul_rn(__dmul_rn(t.ref_dur[c], __ddiv_rn(nd, t.ref_dim[c])),
+                   __ddiv_rn(t.ref_thr[c], thr));
+}
+
+__device__ __forceinline__ double base_of(const TablesDev& t, int c, uint64_t k) {
+  const double nd = __ull2double_rn(k);
+  return base_from_thr(t, c, nd, interp_thr(t, c, nd));
+}
+
+// compute.block_count (78-99) in u64 (Cython semantics, _kernels.pyx:123-126).
+__device__ __forceinline__ uint64_t blocks_of(const TablesDev& t, int c, uint64_t b, uint64_t m,
+                                              uint64_t n, uint64_t k) {
+  const uint64_t tm = t.tile_m[c];
+  if (t.rowblock[c]) return ceil_div(b * k, tm);
+  return b * ceil_div(m, tm) * ceil_div(n, t.tile_n[c]) * t.split_k[c];
+}
+
+// waves / ref_waves  (compute.py:137, _kernels.pyx:132)
+__device__ __forceinline__ double wave_scale(const TablesDev& t, int c, uint64_t waves) {
+  return __ddiv_rn(__ull2double_rn(waves), t.ref_waves[c]);
+}
+
+struct PointResult {
+  double lat;
+  uint64_t blocks, waves;
+};
+
+// Full canonical per-point arithmetic for a known curve and its base.
+__device__ __forceinline__ PointResult predict_point(const TablesDev& t, int c, uint64_t b,
+                                                     uint64_t m, uint64_t n, uint64_t k,
+                                                     double base) {
+  PointResult r;
+  r.blocks = blocks_of(t, c, b, m, n, k);
+  r.waves = ceil_div(r.blocks, t.bpw[c]);
+  r.lat = __dmul_rn(base, wave_scale(t, c, r.waves));
+  return r;
+}
+
+__device__ __forceinline__ bool curve_valid(const TablesDev& t, int c) {
+  return t.s_off[c + 1] > t.s_off[c];
+}
+
+}  // namespace dev
+}  // namespace pm2l

@@ -1,0 +1,533 @@
+// Grid mode: the canonical (batch, m, n, k) sweep of predict_grid_slice
+// (pm2lat/_kernels.pyx:76-133, backend.py:49-88), plus "mode X" (every
+// candidate kernel per shape) and the unresolved-point scan.
+//
+// Decomposition.  One CTA per ((m, n) row, k tile, batch slab).  Everything
+// that does not depend on k is built once per CTA in shared memory:
+//   * D_j = max(|lm_j - qm|, |ln_j - qn|) for every member j of every member
+//     class, and its prefix-minimum staircase (warp scan + ballot);
+//   * per k-group: lk, the group minimum dmin and the scan index that attains
+//     it first;
+//   * Tmn[c] = ceil(m/tm)*ceil(n/tn)*split_k and the wave-scale table
+//     W[ib][c] = ceil(b*Tmn[c]/bpw) / ref_waves  (GEMM families).
+// Each thread then owns k values; per k it runs the outward k-group sweep
+// (nearest config), reads base(curve, k) from the per-launch base table and
+// writes one f64 per batch value with coalesced stores: the only per-point
+// arithmetic is one DMUL.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace pm2l {
+namespace {
+
+using namespace dev;
+
+// ----------------------------------------------------------- base table
+// base[c][ik] for every curve c and k value; one CTA per (curve, k chunk)
+// with the curve's samples staged in shared memory.
+constexpr int kMaxSmemSamples = 256;
+
+__global__ void __launch_bounds__(256) base_table_kernel(TablesDev t, const uint64_t* __restrict__ K,
+                                                         int nK, double* __restrict__ base) {
+  __shared__ double sd[kMaxSmemSamples], sy[kMaxSmemSamples];
+  const int c = blockIdx.y;
+  const int lo = t.s_off[c], hi = t.s_off[c + 1], ns = hi - lo;
+  if (ns <= 0) {
+    for (int ik = blockIdx.x * blockDim.x + threadIdx.x; ik < nK; ik += gridDim.x * blockDim.x)
+      base[int64_t(c) * nK + ik] = 0.0;
+    return;
+  }
+  const bool staged = ns <= kMaxSmemSamples;
+  if (staged) {
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+      sd[j] = t.s_dims[lo + j];
+      sy[j] = t.s_thrs[lo + j];
+    }
+  }
+  __syncthreads();
+  for (int ik = blockIdx.x * blockDim.x + threadIdx.x; ik < nK; ik += gridDim.x * blockDim.x) {
+    const double nd = __ull2double_rn(K[ik]);
+    const double thr = staged ? interp_samples(sd, sy, 0, ns, nd)
+                              : interp_samples(t.s_dims, t.s_thrs, lo, hi, nd);
+    base[int64_t(c) * nK + ik] = base_from_thr(t, c, nd, thr);
+  }
+}
+
+// ------------------------------------------------------------ grid kernel
+struct GridLaunch {
+  int kpt;       // k values per thread
+  int ktiles;    // k tiles per row  (gridDim.y)
+  int nbs;       // batch slabs      (gridDim.z)
+  int bper;      // batch values per slab
+  int mode;      // 0: GEMM + W table, 1: GEMM per point, 2: general (row-block)
+  int64_t smem;
+};
+
+struct __align__(16) GroupRow {
+  double lk;      // log2 k of the group
+  uint64_t dmin;  // min over members of D (ordered bits) — from the class
+  int32_t sstart; // class staircase start (smem index)
+  int32_t last;   // scan index attaining dmin first
+  int32_t gbase;  // group start in group order (member position -> g_idx)
+  int32_t pad;
+};
+
+struct ClassRow {
+  uint64_t dmin;
+  int32_t sstart, len, lastpos, pad;
+};
+
+struct SmemLayout {
+  int64_t D, sD, sP, gidx, ccur, grp, cls, T, W, total;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(const TablesDev& t, int bper, int mode) {
+  SmemLayout L;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = o;
+    o = (o + bytes + 15) & ~int64_t(15);
+    return at;
+  };
+  L.D = take(8ll * t.CM);
+  L.sD = take(8ll * t.CM);
+  L.sP = take(4ll * t.CM);
+  L.gidx = take(4ll * t.R);
+  L.ccur = take(4ll * t.R);
+  L.grp = take(int64_t(sizeof(GroupRow)) * t.G);
+  L.cls = take(int64_t(sizeof(ClassRow)) * t.NC);
+  L.T = take(mode <= 1 ? 8ll * t.C : 0);
+  L.W = take(mode == 0 ? 8ll * t.C * bper : 0);
+  L.total = o;
+  return L;
+}
+
+// Scan index of the first member of group gr whose distance equals `best`
+// (the group attains best): the first staircase entry with D <= best.
+__device__ __forceinline__ int stair_index(const GroupRow& gr, uint64_t best,
+                                           const uint64_t* __restrict__ sD,
+                                           const int32_t* __restrict__ sP,
+                                           const int32_t* __restrict__ gidx) {
+  if (best == gr.dmin) return gr.last;
+  int s = gr.sstart;
+  while (sD[s] > best) ++s;
+  return gidx[gr.gbase + sP[s]];
+}
+
+// Nearest-config argmin for one query k (_kernels.pyx:29-47 semantics).
+// dist(i) = max(D_i, dk_g(i)), dk_g = |lk_g - qk|.  Groups are sorted by lk,
+// so dk_g grows monotonically (IEEE subtraction is monotone) moving away from
+// qk's insertion point: sweep right then left, stopping a side as soon as
+// dk_g exceeds the running best.  Ties (equal distance) resolve to the
+// smallest scan index among every member attaining the final best.
+// Returns the ORIGINAL candidate scan index (INT32_MAX when G == 0).
+template <bool G32>
+__device__ __forceinline__ int nearest_in_row(int G, double qk, int start,
+                                              const GroupRow* __restrict__ grp,
+                                              const uint64_t* __restrict__ sD,
+                                              const int32_t* __restrict__ sP,
+                                              const int32_t* __restrict__ gidx) {
+  uint64_t best = ~0ull;
+  uint32_t mask = 0;
+  int best_i = 0x7FFFFFFF;
+  auto visit = [&](int g) -> bool {
+    const double2 v = *reinterpret_cast<const double2*>(&grp[g]);
+    const uint64_t dk = abs_bits(__dsub_rn(v.x, qk));
+    if (dk > best) return false;
+    const uint64_t dg = umax64(dk, static_cast<uint64_t>(__double_as_longlong(v.y)));
+    if (G32) {
+      if (dg < best) { best = dg; mask = 1u << g; }
+      else if (dg == best) mask |= 1u << g;
+    } else if (dg <= best) {
+      const int idx = stair_index(grp[g], dg, sD, sP, gidx);
+      if (dg < best || idx < best_i) best_i = idx;
+      best = dg;
+    }
+    return true;
+  };
+  for (int g = start; g < G; ++g)
+    if (!visit(g)) break;
+  for (int g = start - 1; g >= 0; --g)
+    if (!visit(g)) break;
+  if (G32) {
+    while (mask) {
+      const int g = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int idx = stair_index(grp[g], best, sD, sP, gidx);
+      best_i = idx < best_i ? idx : best_i;
+    }
+  }
+  return best_i;
+}
+
+template <bool VERIFY, int MODE, bool G32>
+__global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
+                                                        const double* __restrict__ base_tab,
+                                                        LaunchOut out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const SmemLayout L = smem_layout(t, gl.bper, MODE);
+  uint64_t* Dv = reinterpret_cast<uint64_t*>(smem + L.D);
+  uint64_t* sD = reinterpret_cast<uint64_t*>(smem + L.sD);
+  int32_t* sP = reinterpret_cast<int32_t*>(smem + L.sP);
+  int32_t* gidx = reinterpret_cast<int32_t*>(smem + L.gidx);
+  int32_t* ccur = reinterpret_cast<int32_t*>(smem + L.ccur);
+  GroupRow* grp = reinterpret_cast<GroupRow*>(smem + L.grp);
+  ClassRow* cls = reinterpret_cast<ClassRow*>(smem + L.cls);
+  uint64_t* Tmn = reinterpret_cast<uint64_t*>(smem + L.T);
+  double* W = reinterpret_cast<double*>(smem + L.W);
+
+  const int row = blockIdx.x;
+  const int nN = int(g.nN), nK = int(g.nK);
+  const int im = row / nN, jn = row - im * nN;
+  const int ib0 = int(g.b_lo) + int(blockIdx.z) * gl.bper;
+  const int ib1 = min(int(g.b_hi), ib0 + gl.bper);
+  if (ib0 >= ib1) return;
+  const int nb = ib1 - ib0;
+  const uint64_t m = g.M[im], n = g.N[jn];
+  const double qm = g.logM[im], qn = g.logN[jn];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+
+  // 1. D for every class member; candidate tables into smem
+  for (int j = tid; j < t.CM; j += blockDim.x)
+    Dv[j] = umax64(abs_bits(__dsub_rn(t.cls_lm[j], qm)), abs_bits(__dsub_rn(t.cls_ln[j], qn)));
+  for (int j = tid; j < t.R; j += blockDim.x) {
+    gidx[j] = t.g_idx[j];
+    ccur[j] = t.cand_curve[j];
+  }
+  if (MODE <= 1) {
+    for (int c = tid; c < t.C; c += blockDim.x)
+      Tmn[c] = curve_valid(t, c)
+                   ? ceil_div(m, t.tile_m[c]) * ceil_div(n, t.tile_n[c]) * t.split_k[c]
+                   : 0;
+  }
+  __syncthreads();
+
+  // 2. per class: prefix-minimum staircase of D in member (scan) order
+  for (int ci = warp; ci < t.NC; ci += nwarps) {
+    const int start = t.cls_start[ci], size = t.cls_size[ci];
+    uint64_t carry = ~0ull;
+    int len = 0, lastpos = 0;
+    for (int base = 0; base < size; base += 32) {
+      const int j = base + lane;
+      const uint64_t d = j < size ? Dv[start + j] : ~0ull;
+      uint64_t pm = d;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
+        if (lane >= off && o < pm) pm = o;
+      }
+      uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
+      if (lane == 0) excl = ~0ull;
+      if (carry < excl) excl = carry;
+      const bool rec = (j < size) && (d < excl);
+      const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
+      if (rec) {
+        const int pos = start + len + __popc(mask & ((1u << lane) - 1u));
+        sD[pos] = d;
+        sP[pos] = j;
+      }
+      if (mask) lastpos = base + 31 - __clz(mask);
+      len += __popc(mask);
+      const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
+      if (tail < carry) carry = tail;
+    }
+    if (lane == 0) cls[ci] = ClassRow{carry, start, len, lastpos, 0};
+  }
+  // 3. wave-scale table W[ib][c] (GEMM families, independent of k)
+  if (MODE == 0) {
+    for (int e = tid; e < nb * t.C; e += blockDim.x) {
+      const int ib = e / t.C;
+      const int c = e - ib * t.C;
+      if (curve_valid(t, c)) W[e] = wave_scale(t, c, ceil_div(g.B[ib0 + ib] * Tmn[c], t.bpw[c]));
+    }
+  }
+  __syncthreads();
+  // 4. per group: lk, class minimum and the scan index attaining it first
+  for (int gi = tid; gi < t.G; gi += blockDim.x) {
+    const ClassRow cr = cls[t.grp_class[gi]];
+    const int gb = t.grp_start[gi];
+    grp[gi] = GroupRow{t.grp_lk[gi], cr.dmin, cr.sstart,
+                       cr.len ? gidx[gb + cr.lastpos] : 0x7FFFFFFF, gb, 0};
+  }
+  __syncthreads();
+
+  // 5. points: thread owns kpt k values (stride blockDim); every batch value
+  const int64_t plane = g.nM * g.nN * g.nK;
+  double* const obase = out.lat + int64_t(ib0 - g.b_lo) * plane + int64_t(row) * nK;
+  const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
+  for (int j = 0; j < gl.kpt; ++j) {
+    const int ik = k0 + j * int(blockDim.x) + tid;
+    if (ik >= nK) break;
+    const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
+    const int start = __double2loint(ki.y);
+    const int best = nearest_in_row<G32>(t.G, ki.x, start, grp, sD, sP, gidx);
+    const int ci = best < t.R ? ccur[best] : -1;
+    double* o = obase + ik;
+    if (ci < 0) {
+      if (out.nan_stats) {
+        atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
+        atomicAdd(out.nan_stats + 1, (unsigned long long)nb);
+      }
+      for (int ib = 0; ib < nb; ++ib, o += plane) {
+        *o = qnan();
+        if (VERIFY) {
+          const int64_t p = o - out.lat;
+          out.curve[p] = -1;
+          out.blocks[p] = 0;
+          out.waves[p] = 0;
+        }
+      }
+      continue;
+    }
+    const double base = base_tab ? base_tab[int64_t(ci) * nK + ik] : base_of(t, ci, g.K[ik]);
+    if (MODE == 0 && !VERIFY) {
+      const double* w = W + ci;
+      for (int ib = 0; ib < nb; ++ib, o += plane, w += t.C) *o = __dmul_rn(base, *w);
+      continue;
+    }
+    const uint64_t k = g.K[ik];
+    for (int ib = 0; ib < nb; ++ib, o += plane) {
+      double lat;
+      uint64_t blocks, waves;
+      if (MODE <= 1) {
+        blocks = g.B[ib0 + ib] * Tmn[ci];
+        waves = ceil_div(blocks, t.bpw[ci]);
+        lat = __dmul_rn(base, wave_scale(t, ci, waves));
+      } else {
+        const PointResult r = predict_point(t, ci, g.B[ib0 + ib], m, n, k, base);
+        lat = r.lat;
+        blocks = r.blocks;
+        waves = r.waves;
+      }
+      *o = lat;
+      if (VERIFY) {
+        const int64_t p = o - out.lat;
+        out.curve[p] = ci;
+        out.blocks[p] = blocks;
+        out.waves[p] = waves;
+      }
+    }
+  }
+}
+
+// Exact-record hits take priority over the nearest result (_kernels.pyx:107-110).
+template <bool VERIFY>
+__global__ void fixup_kernel(TablesDev t, GridDev g, LaunchOut out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= g.n_fix) return;
+  const int64_t p = g.fix_pos[i];
+  const uint64_t* c4 = g.fix_coord + 4 * i;
+  const int ci = g.fix_curve[i];
+  if (out.nan_stats) {
+    // the grid kernel counted this point by its nearest result; re-count it
+    // by its exact result.  A NaN that disappears may have been the minimum:
+    // flag the stats dirty so the caller re-derives it (pm2l_nan_scan).
+    const bool was_nan = out.lat[p] != out.lat[p];
+    if (was_nan && ci >= 0) {
+      atomicAdd(out.nan_stats + 1, ~0ull);  // -1
+      atomicOr(out.nan_stats + 2, 1ull);
+    }
+    if (!was_nan && ci < 0) {
+      atomicAdd(out.nan_stats + 1, 1ull);
+      atomicMin(out.nan_stats, (unsigned long long)p);
+    }
+  }
+  if (ci < 0) {
+    out.lat[p] = qnan();
+    if (VERIFY) { out.curve[p] = -1; out.blocks[p] = 0; out.waves[p] = 0; }
+    return;
+  }
+  const PointResult r = predict_point(t, ci, c4[0], c4[1], c4[2], c4[3], base_of(t, ci, c4[3]));
+  out.lat[p] = r.lat;
+  if (VERIFY) { out.curve[p] = ci; out.blocks[p] = r.blocks; out.waves[p] = r.waves; }
+}
+
+// ------------------------------------------------------- mode X (all curves)
+__global__ void __launch_bounds__(kThreads) all_curves_kernel(TablesDev t, GridDev g, GridLaunch gl,
+                                                              const double* __restrict__ base_tab,
+                                                              double* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* Tmn = reinterpret_cast<uint64_t*>(smem);
+  double* W = reinterpret_cast<double*>(smem + ((8ll * t.C + 15) & ~15ll));
+  const int row = blockIdx.x;
+  const int nN = int(g.nN), nK = int(g.nK);
+  const int im = row / nN, jn = row - im * nN;
+  const int ib0 = int(g.b_lo) + int(blockIdx.z) * gl.bper;
+  const int ib1 = min(int(g.b_hi), ib0 + gl.bper);
+  if (ib0 >= ib1) return;
+  const int nb = ib1 - ib0;
+  const uint64_t m = g.M[im], n = g.N[jn];
+  const int tid = threadIdx.x;
+  const bool table = gl.mode == 0;
+  if (table) {
+    for (int c = tid; c < t.C; c += blockDim.x)
+      Tmn[c] = curve_valid(t, c)
+                   ? ceil_div(m, t.tile_m[c]) * ceil_div(n, t.tile_n[c]) * t.split_k[c]
+                   : 0;
+    __syncthreads();
+    for (int e = tid; e < nb * t.C; e += blockDim.x) {
+      const int ib = e / t.C;
+      const int c = e - ib * t.C;
+      if (curve_valid(t, c)) W[e] = wave_scale(t, c, ceil_div(g.B[ib0 + ib] * Tmn[c], t.bpw[c]));
+    }
+    __syncthreads();
+  }
+  const int64_t slice = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
+  const int64_t plane = g.nM * g.nN * g.nK;
+  const int64_t row_off = int64_t(ib0 - g.b_lo) * plane + int64_t(row) * nK;
+  const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
+  for (int j = 0; j < gl.kpt; ++j) {
+    const int ik = k0 + j * int(blockDim.x) + tid;
+    if (ik >= nK) break;
+    const uint64_t k = g.K[ik];
+    for (int c = 0; c < t.C; ++c) {
+      const double base = base_tab[int64_t(c) * nK + ik];
+      const bool valid = curve_valid(t, c);
+      double* o = out + int64_t(c) * slice + row_off + ik;
+      for (int ib = 0; ib < nb; ++ib, o += plane) {
+        double lat;
+        if (!valid) lat = qnan();
+        else if (table) lat = __dmul_rn(base, W[ib * t.C + c]);
+        else lat = predict_point(t, c, g.B[ib0 + ib], m, n, k, base).lat;
+        __stcs(o, lat);
+      }
+    }
+  }
+}
+
+__global__ void nan_scan_kernel(const double* __restrict__ v, int64_t n,
+                                unsigned long long* __restrict__ first) {
+  unsigned long long mine = ~0ull;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (v[i] != v[i]) { mine = (unsigned long long)i; break; }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xFFFFFFFFu, mine, o);
+    mine = x < mine ? x : mine;
+  }
+  if ((threadIdx.x & 31) == 0 && mine != ~0ull) atomicMin(first, mine);
+}
+
+GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
+  GridLaunch gl{};
+  const int64_t rows = g.nM * g.nN;
+  const int64_t nb = g.b_hi - g.b_lo;
+  const int64_t target = 148 * 8;
+  auto ktiles_for = [&](int kpt) {
+    return int((g.nK + int64_t(kpt) * kThreads - 1) / (int64_t(kpt) * kThreads));
+  };
+  gl.kpt = 4;
+  gl.ktiles = ktiles_for(gl.kpt);
+  while (gl.kpt > 1 && rows * gl.ktiles < target) {
+    gl.kpt >>= 1;
+    gl.ktiles = ktiles_for(gl.kpt);
+  }
+  const int64_t ctas = rows * gl.ktiles;
+  int64_t nbs = 1;
+  if (ctas < target && nb > 1) nbs = std::min<int64_t>(nb, (target + ctas - 1) / ctas);
+  gl.bper = int((nb + nbs - 1) / nbs);
+  gl.nbs = int((nb + gl.bper - 1) / gl.bper);
+  if (all_curves) {
+    gl.mode = (t.all_gemm && 8ll * t.C * (gl.bper + 1) <= 96 * 1024) ? 0 : 2;
+    gl.smem = gl.mode == 0 ? ((8ll * t.C + 15) & ~15ll) + 8ll * t.C * gl.bper : 0;
+    return gl;
+  }
+  if (!t.all_gemm) gl.mode = 2;
+  else if (8ll * t.C * gl.bper <= 48 * 1024 && t.C <= 4 * g.nK) gl.mode = 0;
+  else gl.mode = 1;
+  gl.smem = smem_layout(t, gl.bper, gl.mode).total;
+  return gl;
+}
+
+bool grid_dims_ok(const GridDev& g, const GridLaunch& gl) {
+  return g.nM * g.nN <= 0x7FFFFFFFll && gl.ktiles <= 65535 && gl.nbs <= 65535 &&
+         g.nK <= 0x3FFFFFFFll && g.nB <= 0x7FFFFFFFll;
+}
+
+template <bool V, int M>
+cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
+                          const double* base, const LaunchOut& out, cudaStream_t s) {
+  auto* fn = t.G <= 32 ? grid_kernel<V, M, true> : grid_kernel<V, M, false>;
+  if (gl.smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gl.smem));
+    if (e != cudaSuccess) return e;
+  }
+  const dim3 grid(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
+  fn<<<grid, kThreads, gl.smem, s>>>(t, g, gl, base, out);
+  return cudaGetLastError();
+}
+
+void launch_base_table(const TablesDev& t, const GridDev& g, double* ws, cudaStream_t s) {
+  const int chunks = int(std::min<int64_t>((g.nK + 255) / 256, 64));
+  base_table_kernel<<<dim3(chunks, t.C), 256, 0, s>>>(t, g.K, int(g.nK), ws);
+}
+
+}  // namespace
+
+int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g) {
+  const int64_t e = int64_t(t.C) * g.nK;
+  return e <= (int64_t(1) << 25) ? e : 0;  // base table only when <= 256 MiB
+}
+
+int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, double* ws,
+                int64_t ws_elems, const LaunchOut& out, void* stream, int stages) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
+  if (card == 0) return 0;
+  const GridLaunch gl = plan_grid(t, g, false);
+  if (gl.smem > 227 * 1024 || !grid_dims_ok(g, gl)) return int(cudaErrorInvalidValue);
+  const double* base = nullptr;
+  if (ws && ws_elems >= int64_t(t.C) * g.nK && t.C > 0 && t.C <= 65535) {
+    if (stages & kStageBase) launch_base_table(t, g, ws, s);
+    base = ws;
+  }
+  const bool v = out.curve != nullptr;
+  cudaError_t e = cudaSuccess;
+  if (stages & kStageGrid) {
+    if (v) {
+      e = gl.mode == 0 ? launch_grid_t<true, 0>(t, g, gl, base, out, s)
+          : gl.mode == 1 ? launch_grid_t<true, 1>(t, g, gl, base, out, s)
+                         : launch_grid_t<true, 2>(t, g, gl, base, out, s);
+    } else {
+      e = gl.mode == 0 ? launch_grid_t<false, 0>(t, g, gl, base, out, s)
+          : gl.mode == 1 ? launch_grid_t<false, 1>(t, g, gl, base, out, s)
+                         : launch_grid_t<false, 2>(t, g, gl, base, out, s);
+    }
+  }
+  if (e != cudaSuccess) return int(e);
+  if (g.n_fix > 0 && (stages & kStageFixup)) {
+    const int nb = int((g.n_fix + 127) / 128);
+    if (v) fixup_kernel<true><<<nb, 128, 0, s>>>(t, g, out);
+    else fixup_kernel<false><<<nb, 128, 0, s>>>(t, g, out);
+  }
+  return int(cudaGetLastError());
+}
+
+int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* ws, double* out,
+                           void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
+  if (card == 0 || t.C == 0) return 0;
+  const GridLaunch gl = plan_grid(t, g, true);
+  if (!grid_dims_ok(g, gl) || t.C > 65535) return int(cudaErrorInvalidValue);
+  launch_base_table(t, g, ws, s);
+  if (gl.smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(all_curves_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(gl.smem));
+    if (e != cudaSuccess) return int(e);
+  }
+  const dim3 grid(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
+  all_curves_kernel<<<grid, kThreads, gl.smem, s>>>(t, g, gl, ws, out);
+  return int(cudaGetLastError());
+}
+
+int launch_nan_scan(const double* v, int64_t n, unsigned long long* first, void* stream) {
+  if (n == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int nb = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  nan_scan_kernel<<<nb, 256, 0, s>>>(v, n, first);
+  return int(cudaGetLastError());
+}
+
+}  // namespace pm2l

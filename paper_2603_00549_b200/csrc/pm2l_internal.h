@@ -49,10 +49,28 @@ struct TablesDev {
   const double* grp_lk = nullptr;
   const int32_t* grp_start = nullptr;
   const int32_t* grp_size = nullptr;
+  const int32_t* grp_class = nullptr;
+  // member classes: groups whose member (log m, log n) sequences are equal
+  // share one D sequence and one staircase per (m, n) row (the shipped
+  // presets collect every kernel at every sample k, so all k-groups of a
+  // triple fall into ONE class).  NC classes, CM members in total.
+  int32_t NC = 0;
+  int32_t CM = 0;
+  const int32_t* cls_start = nullptr;  // [NC] into cls_lm / cls_ln
+  const int32_t* cls_size = nullptr;   // [NC]
+  const double* cls_lm = nullptr;      // [CM]
+  const double* cls_ln = nullptr;      // [CM]
   // exact records [n_exact], unpacked, sorted by (b,m,n,k)
   const uint64_t* ex_coord = nullptr; // 4 per record
   const int32_t* ex_curve = nullptr;
   const int32_t* ex_rec = nullptr;    // position in the caller's exact arrays
+};
+
+// Per-k sweep info, 16 B (one 128-bit load in the grid kernel).
+struct alignas(16) KInfo {
+  double qk;      // libm log2(k)
+  int32_t start;  // #k-groups with grp_lk < qk (outward sweep start)
+  int32_t pad;
 };
 
 // Per-launch grid description (device pointers into one per-call upload).
@@ -66,7 +84,8 @@ struct GridDev {
   const double* logM = nullptr;   // libm log2 of each axis value (host computed)
   const double* logN = nullptr;
   const double* logK = nullptr;
-  const int32_t* kstart = nullptr;  // per k: #groups with grp_lk < logK (sweep start)
+  // per k: {log2 k, sweep start = #groups with grp_lk < log2 k}, 16 B each
+  const KInfo* kinfo = nullptr;
   // exact-hit fix-ups: slice-relative flat index + coordinates + curve
   int64_t n_fix = 0;
   const int64_t* fix_pos = nullptr;

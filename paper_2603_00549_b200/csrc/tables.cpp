@@ -11,6 +11,8 @@
 #include <array>
 #include <cmath>
 #include <cstring>
+#include <utility>
+#include <vector>
 #include <map>
 #include <numeric>
 #include <string>
@@ -113,6 +115,33 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
     g_ln[p] = v->log_n[i];
     g_idx[p] = i;  // stable sort keeps ascending scan order inside a group
   }
+  // --- member classes (groups with identical (lm, ln) member sequences)
+  std::vector<int32_t> grp_class(grp_lk.size()), cls_start, cls_size;
+  std::vector<double> cls_lm, cls_ln;
+  {
+    std::map<std::vector<std::pair<uint64_t, uint64_t>>, int32_t> seen;
+    for (size_t gi = 0; gi < grp_lk.size(); ++gi) {
+      std::vector<std::pair<uint64_t, uint64_t>> sig;
+      for (int32_t p = grp_start[gi]; p < grp_start[gi] + grp_size[gi]; ++p) {
+        uint64_t a, b;
+        std::memcpy(&a, &g_lm[p], 8);
+        std::memcpy(&b, &g_ln[p], 8);
+        sig.emplace_back(a, b);
+      }
+      auto it = seen.find(sig);
+      if (it == seen.end()) {
+        const int32_t id = int32_t(cls_start.size());
+        cls_start.push_back(int32_t(cls_lm.size()));
+        cls_size.push_back(grp_size[gi]);
+        for (int32_t p = grp_start[gi]; p < grp_start[gi] + grp_size[gi]; ++p) {
+          cls_lm.push_back(g_lm[p]);
+          cls_ln.push_back(g_ln[p]);
+        }
+        it = seen.emplace(std::move(sig), id).first;
+      }
+      grp_class[gi] = it->second;
+    }
+  }
   std::vector<int32_t> cand_curve(R);
   for (int64_t i = 0; i < R; ++i) cand_curve[i] = int32_t(v->cand_curve[i]);
 
@@ -169,6 +198,13 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.grp_lk = blob.add(grp_lk);
   t.grp_start = blob.add(grp_start);
   t.grp_size = blob.add(grp_size);
+  t.grp_class = blob.add(grp_class);
+  t.NC = int32_t(cls_start.size());
+  t.CM = int32_t(cls_lm.size());
+  t.cls_start = blob.add(cls_start);
+  t.cls_size = blob.add(cls_size);
+  t.cls_lm = blob.add(cls_lm);
+  t.cls_ln = blob.add(cls_ln);
   t.ex_coord = blob.add(ex_coord);
   t.ex_curve = blob.add(ex_curve);
   t.ex_rec = blob.add(ex_rec);
@@ -188,7 +224,9 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.g_lm = shift(o.g_lm, base); t.g_ln = shift(o.g_ln, base);
   t.g_idx = shift(o.g_idx, base); t.cand_curve = shift(o.cand_curve, base);
   t.grp_lk = shift(o.grp_lk, base); t.grp_start = shift(o.grp_start, base);
-  t.grp_size = shift(o.grp_size, base);
+  t.grp_size = shift(o.grp_size, base); t.grp_class = shift(o.grp_class, base);
+  t.cls_start = shift(o.cls_start, base); t.cls_size = shift(o.cls_size, base);
+  t.cls_lm = shift(o.cls_lm, base); t.cls_ln = shift(o.cls_ln, base);
   t.ex_coord = shift(o.ex_coord, base); t.ex_curve = shift(o.ex_curve, base);
   t.ex_rec = shift(o.ex_rec, base);
   return t;
@@ -214,9 +252,9 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   const TablesDev& tt = th.dev_offsets;
   const double* glk = reinterpret_cast<const double*>(
       th.blob.data() + reinterpret_cast<uintptr_t>(tt.grp_lk));
-  std::vector<int32_t> kstart(nK);
+  std::vector<KInfo> kinfo(nK);
   for (int64_t i = 0; i < nK; ++i)
-    kstart[i] = int32_t(std::lower_bound(glk, glk + tt.G, logs[2][i]) - glk);
+    kinfo[i] = {logs[2][i], int32_t(std::lower_bound(glk, glk + tt.G, logs[2][i]) - glk), 0};
 
   // exact-hit fix-ups: every grid point whose (b, m, n, k) equals a recorded
   // shape takes the recorded kernel (_kernels.pyx:107-110) instead of the
@@ -271,7 +309,7 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   g.logM = blob.add(logs[0]);
   g.logN = blob.add(logs[1]);
   g.logK = blob.add(logs[2]);
-  g.kstart = blob.add(kstart);
+  g.kinfo = blob.add(kinfo);
   g.n_fix = int64_t(fix_pos.size());
   g.fix_pos = blob.add(fix_pos);
   g.fix_coord = blob.add(fix_coord);
@@ -284,7 +322,7 @@ GridDev rebase(const GridDev& o, const void* base) {
   GridDev g = o;
   g.B = shift(o.B, base); g.M = shift(o.M, base); g.N = shift(o.N, base);
   g.K = shift(o.K, base); g.logM = shift(o.logM, base); g.logN = shift(o.logN, base);
-  g.logK = shift(o.logK, base); g.kstart = shift(o.kstart, base);
+  g.logK = shift(o.logK, base); g.kinfo = shift(o.kinfo, base);
   g.fix_pos = shift(o.fix_pos, base);
   g.fix_coord = shift(o.fix_coord, base); g.fix_curve = shift(o.fix_curve, base);
   return g;
