@@ -61,6 +61,9 @@ struct GridLaunch {
   int nbs;       // batch slabs      (gridDim.z)
   int bper;      // batch values per slab
   int mode;      // 0: GEMM + W table, 1: GEMM per point, 2: general (row-block)
+  int near;      // 0: general sweep, 1: sweep + tie mask (G <= 32), 2: one member class
+  // shared-memory layout (byte offsets), computed on the host
+  int off_D, off_sD, off_sP, off_grp, off_cls, off_T, off_W;
   int64_t smem;
 };
 
@@ -78,29 +81,21 @@ struct ClassRow {
   int32_t sstart, len, lastpos, pad;
 };
 
-struct SmemLayout {
-  int64_t D, sD, sP, gidx, ccur, grp, cls, T, W, total;
-};
-
-__host__ __device__ inline SmemLayout smem_layout(const TablesDev& t, int bper, int mode) {
-  SmemLayout L;
+void layout(const TablesDev& t, GridLaunch& gl) {
   int64_t o = 0;
   auto take = [&](int64_t bytes) {
     const int64_t at = o;
     o = (o + bytes + 15) & ~int64_t(15);
-    return at;
+    return int(at);
   };
-  L.D = take(8ll * t.CM);
-  L.sD = take(8ll * t.CM);
-  L.sP = take(4ll * t.CM);
-  L.gidx = take(4ll * t.R);
-  L.ccur = take(4ll * t.R);
-  L.grp = take(int64_t(sizeof(GroupRow)) * t.G);
-  L.cls = take(int64_t(sizeof(ClassRow)) * t.NC);
-  L.T = take(mode <= 1 ? 8ll * t.C : 0);
-  L.W = take(mode == 0 ? 8ll * t.C * bper : 0);
-  L.total = o;
-  return L;
+  gl.off_D = take(8ll * t.CM);
+  gl.off_sD = take(8ll * t.CM);
+  gl.off_sP = take(4ll * t.CM);
+  gl.off_grp = take(gl.near == 2 ? 0 : int64_t(sizeof(GroupRow)) * t.G);
+  gl.off_cls = take(int64_t(sizeof(ClassRow)) * t.NC);
+  gl.off_T = take(gl.mode <= 1 ? 8ll * t.C : 0);
+  gl.off_W = take(gl.mode == 0 ? 8ll * t.C * gl.bper : 0);
+  gl.smem = o;
 }
 
 // Scan index of the first member of group gr whose distance equals `best`
@@ -123,11 +118,11 @@ __device__ __forceinline__ int stair_index(const GroupRow& gr, uint64_t best,
 // smallest scan index among every member attaining the final best.
 // Returns the ORIGINAL candidate scan index (INT32_MAX when G == 0).
 template <bool G32>
-__device__ __forceinline__ int nearest_in_row(int G, double qk, int start,
-                                              const GroupRow* __restrict__ grp,
-                                              const uint64_t* __restrict__ sD,
-                                              const int32_t* __restrict__ sP,
-                                              const int32_t* __restrict__ gidx) {
+__device__ __forceinline__ int nearest_sweep(int G, double qk, int start,
+                                             const GroupRow* __restrict__ grp,
+                                             const uint64_t* __restrict__ sD,
+                                             const int32_t* __restrict__ sP,
+                                             const int32_t* __restrict__ gidx) {
   uint64_t best = ~0ull;
   uint32_t mask = 0;
   int best_i = 0x7FFFFFFF;
@@ -161,21 +156,58 @@ __device__ __forceinline__ int nearest_in_row(int G, double qk, int start,
   return best_i;
 }
 
-template <bool VERIFY, int MODE, bool G32>
+// One member class (every kernel recorded at every sample k — the shipped
+// presets): all groups share D, dmin and the staircase, and between tied
+// groups the one with the smaller lk has the smaller scan index (same (m, n)
+// at the same member position, then k decides; host-verified: coordinates
+// < 2^44 so equal logs imply equal coordinates).  Hence
+//   best = max(dmin, min(dk_left, dk_right))   (nearest groups to qk)
+//   winner = the leftmost group attaining best, member = staircase(best).
+__device__ __forceinline__ int nearest_one_class(int G, double qk, int start,
+                                                 const double* __restrict__ glk,
+                                                 const int32_t* __restrict__ gstart,
+                                                 const int32_t* __restrict__ gidx, uint64_t dmin,
+                                                 int lastpos, const uint64_t* __restrict__ sD,
+                                                 const int32_t* __restrict__ sP) {
+  auto dk = [&](int g) { return abs_bits(__dsub_rn(glk[g], qk)); };
+  const uint64_t dkL = start > 0 ? dk(start - 1) : ~0ull;
+  const uint64_t dkR = start < G ? dk(start) : ~0ull;
+  const uint64_t mn = dkL < dkR ? dkL : dkR;
+  int g, pos;
+  if (mn <= dmin) {            // best == dmin: every group with dk <= dmin ties
+    if (dkL <= dmin) {
+      g = start - 1;
+      while (g > 0 && dk(g - 1) <= dmin) --g;
+    } else {
+      g = start;
+    }
+    pos = lastpos;
+  } else {                     // best == mn > dmin
+    if (dkL == mn) {
+      g = start - 1;
+      while (g > 0 && dk(g - 1) == mn) --g;
+    } else {
+      g = start;
+    }
+    int s = 0;
+    while (sD[s] > mn) ++s;
+    pos = sP[s];
+  }
+  return gidx[gstart[g] + pos];
+}
+
+template <bool VERIFY, int MODE, int NEAR>
 __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
                                                         const double* __restrict__ base_tab,
                                                         LaunchOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const SmemLayout L = smem_layout(t, gl.bper, MODE);
-  uint64_t* Dv = reinterpret_cast<uint64_t*>(smem + L.D);
-  uint64_t* sD = reinterpret_cast<uint64_t*>(smem + L.sD);
-  int32_t* sP = reinterpret_cast<int32_t*>(smem + L.sP);
-  int32_t* gidx = reinterpret_cast<int32_t*>(smem + L.gidx);
-  int32_t* ccur = reinterpret_cast<int32_t*>(smem + L.ccur);
-  GroupRow* grp = reinterpret_cast<GroupRow*>(smem + L.grp);
-  ClassRow* cls = reinterpret_cast<ClassRow*>(smem + L.cls);
-  uint64_t* Tmn = reinterpret_cast<uint64_t*>(smem + L.T);
-  double* W = reinterpret_cast<double*>(smem + L.W);
+  uint64_t* Dv = reinterpret_cast<uint64_t*>(smem + gl.off_D);
+  uint64_t* sD = reinterpret_cast<uint64_t*>(smem + gl.off_sD);
+  int32_t* sP = reinterpret_cast<int32_t*>(smem + gl.off_sP);
+  GroupRow* grp = reinterpret_cast<GroupRow*>(smem + gl.off_grp);
+  ClassRow* cls = reinterpret_cast<ClassRow*>(smem + gl.off_cls);
+  uint64_t* Tmn = reinterpret_cast<uint64_t*>(smem + gl.off_T);
+  double* W = reinterpret_cast<double*>(smem + gl.off_W);
 
   const int row = blockIdx.x;
   const int nN = int(g.nN), nK = int(g.nK);
@@ -188,13 +220,9 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
   const double qm = g.logM[im], qn = g.logN[jn];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 
-  // 1. D for every class member; candidate tables into smem
+  // 1. D for every class member (k-independent part of the distance)
   for (int j = tid; j < t.CM; j += blockDim.x)
     Dv[j] = umax64(abs_bits(__dsub_rn(t.cls_lm[j], qm)), abs_bits(__dsub_rn(t.cls_ln[j], qn)));
-  for (int j = tid; j < t.R; j += blockDim.x) {
-    gidx[j] = t.g_idx[j];
-    ccur[j] = t.cand_curve[j];
-  }
   if (MODE <= 1) {
     for (int c = tid; c < t.C; c += blockDim.x)
       Tmn[c] = curve_valid(t, c)
@@ -244,13 +272,21 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
   }
   __syncthreads();
   // 4. per group: lk, class minimum and the scan index attaining it first
-  for (int gi = tid; gi < t.G; gi += blockDim.x) {
-    const ClassRow cr = cls[t.grp_class[gi]];
-    const int gb = t.grp_start[gi];
-    grp[gi] = GroupRow{t.grp_lk[gi], cr.dmin, cr.sstart,
-                       cr.len ? gidx[gb + cr.lastpos] : 0x7FFFFFFF, gb, 0};
+  if (NEAR != 2) {
+    for (int gi = tid; gi < t.G; gi += blockDim.x) {
+      const ClassRow cr = cls[t.grp_class[gi]];
+      const int gb = t.grp_start[gi];
+      grp[gi] = GroupRow{t.grp_lk[gi], cr.dmin, cr.sstart,
+                         cr.len ? t.g_idx[gb + cr.lastpos] : 0x7FFFFFFF, gb, 0};
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  uint64_t dmin1 = 0;
+  int lastpos1 = 0;
+  if (NEAR == 2) {
+    dmin1 = cls[0].dmin;
+    lastpos1 = cls[0].lastpos;
+  }
 
   // 5. points: thread owns kpt k values (stride blockDim); every batch value
   const int64_t plane = g.nM * g.nN * g.nK;
@@ -261,8 +297,13 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
     if (ik >= nK) break;
     const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
     const int start = __double2loint(ki.y);
-    const int best = nearest_in_row<G32>(t.G, ki.x, start, grp, sD, sP, gidx);
-    const int ci = best < t.R ? ccur[best] : -1;
+    int best;
+    if (NEAR == 2)
+      best = nearest_one_class(t.G, ki.x, start, t.grp_lk, t.grp_start, t.g_idx, dmin1, lastpos1,
+                               sD, sP);
+    else
+      best = nearest_sweep<NEAR == 1>(t.G, ki.x, start, grp, sD, sP, t.g_idx);
+    const int ci = best < t.R ? t.cand_curve[best] : -1;
     double* o = obase + ik;
     if (ci < 0) {
       if (out.nan_stats) {
@@ -280,9 +321,10 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
       }
       continue;
     }
-    const double base = base_tab ? base_tab[int64_t(ci) * nK + ik] : base_of(t, ci, g.K[ik]);
+    const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
     if (MODE == 0 && !VERIFY) {
       const double* w = W + ci;
+#pragma unroll 4
       for (int ib = 0; ib < nb; ++ib, o += plane, w += t.C) *o = __dmul_rn(base, *w);
       continue;
     }
@@ -436,7 +478,8 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   if (!t.all_gemm) gl.mode = 2;
   else if (8ll * t.C * gl.bper <= 48 * 1024 && t.C <= 4 * g.nK) gl.mode = 0;
   else gl.mode = 1;
-  gl.smem = smem_layout(t, gl.bper, gl.mode).total;
+  gl.near = (t.NC == 1 && t.lowest_wins) ? 2 : (t.G <= 32 ? 1 : 0);
+  layout(t, gl);
   return gl;
 }
 
@@ -448,7 +491,8 @@ bool grid_dims_ok(const GridDev& g, const GridLaunch& gl) {
 template <bool V, int M>
 cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
                           const double* base, const LaunchOut& out, cudaStream_t s) {
-  auto* fn = t.G <= 32 ? grid_kernel<V, M, true> : grid_kernel<V, M, false>;
+  auto* fn = gl.near == 2 ? grid_kernel<V, M, 2> : gl.near == 1 ? grid_kernel<V, M, 1>
+                                                                 : grid_kernel<V, M, 0>;
   if (gl.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gl.smem));
     if (e != cudaSuccess) return e;
@@ -476,7 +520,8 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
   if (card == 0) return 0;
   const GridLaunch gl = plan_grid(t, g, false);
-  if (gl.smem > 227 * 1024 || !grid_dims_ok(g, gl)) return int(cudaErrorInvalidValue);
+  if (gl.smem > 227 * 1024 || !grid_dims_ok(g, gl) || int64_t(t.C) * g.nK > 0x7FFFFFFFll)
+    return int(cudaErrorInvalidValue);
   const double* base = nullptr;
   if (ws && ws_elems >= int64_t(t.C) * g.nK && t.C > 0 && t.C <= 65535) {
     if (stages & kStageBase) launch_base_table(t, g, ws, s);

@@ -179,6 +179,14 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t = TablesDev{};
   t.R = int32_t(R); t.C = int32_t(C); t.G = int32_t(grp_lk.size());
   t.n_exact = int32_t(R); t.all_gemm = all_gemm; t.n_samples = int32_t(S);
+  {
+    // log2 is injective on integers below 2^44 at double precision, so equal
+    // candidate logs there imply equal coordinates (grid.cu one-class path)
+    bool small = true;
+    for (int64_t i = 0; i < R; ++i)
+      small = small && v->log_m[i] < 44.0 && v->log_n[i] < 44.0 && v->log_k[i] < 44.0;
+    t.lowest_wins = small ? 1 : 0;
+  }
   t.ref_dim = blob.add(v->ref_dim, C);
   t.ref_dur = blob.add(v->ref_dur, C);
   t.ref_thr = blob.add(v->ref_thr, C);

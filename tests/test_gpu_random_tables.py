@@ -11,11 +11,17 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def random_tables(rng, R, C, n_k_values, rowblock=False, wide=False):
+def random_tables(rng, R, C, n_k_values, rowblock=False, wide=False, lattice=False):
     pool_m = rng.choice(np.arange(1, 5000), size=12, replace=False)
     pool_n = rng.choice(np.arange(1, 5000), size=12, replace=False)
     pool_k = rng.choice(np.arange(1, 70000 if wide else 20000), size=n_k_values, replace=False)
     coords = set()
+    if lattice:
+        # every (b, m, n) collected at every k: one member class (the presets' shape)
+        mn = set()
+        while len(mn) * n_k_values < R:
+            mn.add((int(rng.integers(1, 5)), int(rng.choice(pool_m)), int(rng.choice(pool_n))))
+        coords = {(b, m, n, int(k)) for (b, m, n) in mn for k in pool_k}
     while len(coords) < R:
         coords.add((int(rng.integers(1, 5)), int(rng.choice(pool_m)), int(rng.choice(pool_n)),
                     int(rng.choice(pool_k))))
@@ -50,14 +56,17 @@ def random_tables(rng, R, C, n_k_values, rowblock=False, wide=False):
     return t, pool_m, pool_n, pool_k
 
 
-@pytest.mark.parametrize("seed,R,C,nkv,rowblock", [
-    (1, 40, 5, 3, False), (2, 300, 20, 40, False), (3, 900, 60, 120, False),
-    (4, 200, 7, 9, True), (5, 64, 3, 64, False), (6, 1500, 30, 33, False)])
-def test_random_tables_grid(gpu, seed, R, C, nkv, rowblock):
+@pytest.mark.parametrize("seed,R,C,nkv,rowblock,lattice", [
+    (1, 40, 5, 3, False, False), (2, 300, 20, 40, False, False),
+    (3, 900, 60, 120, False, False), (4, 200, 7, 9, True, False),
+    (5, 64, 3, 64, False, False), (6, 1500, 30, 33, False, False),
+    (7, 90, 6, 9, False, True), (8, 540, 60, 9, False, True), (9, 400, 12, 40, False, True),
+    (10, 60, 4, 5, True, True)])
+def test_random_tables_grid(gpu, seed, R, C, nkv, rowblock, lattice):
     import torch
     from paper_2603_00549_b200 import _native
     rng = np.random.default_rng(seed)
-    t, pm, pn, pk = random_tables(rng, R, C, nkv, rowblock)
+    t, pm, pn, pk = random_tables(rng, R, C, nkv, rowblock, lattice=lattice)
     dt = _native.DeviceTables(t, 0)
     # axes mix recorded values (exact hits, exact distance ties) and others
     B = np.array(sorted({1, 2, 3, 4, 7}), np.uint64)
