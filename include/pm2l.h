@@ -46,6 +46,8 @@ enum {
 
 /* ------------------------------------------------------------------ misc */
 int pm2l_abi_version(void);
+/* Hash of the sources the library was built from (build-staleness check). */
+const char* pm2l_source_hash(void);
 const char* pm2l_last_error(void);
 /* Number of visible CUDA devices (0 on a CPU-only host; never an error). */
 int pm2l_device_count(void);

@@ -36,6 +36,17 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def source_hash() -> str:
+    """sha256 over every source/header compiled into the library; embedded in
+    the .so (pm2l_source_hash) so a stale binary is refused at load time."""
+    import hashlib
+    h = hashlib.sha256()
+    for p in SOURCES + HEADERS:
+        with open(os.path.join(PKG, p), "rb") as fh:
+            h.update(p.encode() + b"\0" + fh.read())
+    return h.hexdigest()[:32]
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB_PATH):
         return True
@@ -47,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB_PATH
     tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, *SOURCES, "-o", tmp]
+    cmd = [nvcc(), *NVCC_FLAGS, f"-DPM2L_SOURCE_HASH=\"{source_hash()}\"", *SOURCES, "-o", tmp]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -40,6 +40,7 @@ class TablesView(C.Structure):
 #: every symbol include/pm2l.h declares, with (restype, argtypes)
 SIGNATURES = {
     "pm2l_abi_version": (_i32, []),
+    "pm2l_source_hash": (C.c_char_p, []),
     "pm2l_last_error": (C.c_char_p, []),
     "pm2l_device_count": (_i32, []),
     "pm2l_tables_create": (_i32, [C.POINTER(TablesView), _i32, C.POINTER(_p)]),
@@ -88,6 +89,16 @@ def load(required: bool = True):
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
+            from . import _build
+            try:
+                want = _build.source_hash()
+            except OSError:      # sources not shipped: nothing to compare against
+                want = None
+            got = lib.pm2l_source_hash().decode()
+            if want is not None and got != want:
+                raise BackendUnavailable(
+                    f"{_LIB_PATH} was built from different sources ({got} != {want}); "
+                    f"rebuild with __graft_entry__.build()")
             _lib = lib
     return _lib
 

@@ -170,6 +170,11 @@ extern "C" {
 
 int pm2l_abi_version(void) { return PM2L_ABI_VERSION; }
 
+#ifndef PM2L_SOURCE_HASH
+#define PM2L_SOURCE_HASH "unknown"
+#endif
+const char* pm2l_source_hash(void) { return PM2L_SOURCE_HASH; }
+
 const char* pm2l_last_error(void) { return g_error.c_str(); }
 
 int pm2l_device_count(void) {
