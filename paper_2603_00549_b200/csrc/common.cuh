@@ -81,7 +81,8 @@ __device__ __forceinline__ uint64_t blocks_of(const TablesDev& t, int c, uint64_
 
 // waves / ref_waves  (compute.py:137, _kernels.pyx:132)
 __device__ __forceinline__ double wave_scale(const TablesDev& t, int c, uint64_t waves) {
-  return __ddiv_rn(__ull2double_rn(waves), t.ref_waves[c]);
+  const double w = __ull2double_rn(waves), rw = t.ref_waves[c];
+  return rw == 1.0 ? w : __ddiv_rn(w, rw);  // x / 1.0 == x exactly (IEEE)
 }
 
 struct PointResult {

@@ -63,7 +63,7 @@ struct GridLaunch {
   int mode;      // 0: GEMM + W table, 1: GEMM per point, 2: general (row-block)
   int near;      // 0: general sweep, 1: sweep + tie mask (G <= 32), 2: one member class
   // shared-memory layout (byte offsets), computed on the host
-  int off_D, off_sD, off_sP, off_grp, off_cls, off_T, off_W;
+  int off_D, off_sD, off_sP, off_grp, off_cls, off_T, off_W, off_gcur, off_glk, off_gst;
   int64_t smem;
 };
 
@@ -95,6 +95,9 @@ void layout(const TablesDev& t, GridLaunch& gl) {
   gl.off_cls = take(int64_t(sizeof(ClassRow)) * t.NC);
   gl.off_T = take(gl.mode <= 1 ? 8ll * t.C : 0);
   gl.off_W = take(gl.mode == 0 ? 8ll * t.C * gl.bper : 0);
+  gl.off_gcur = take(4ll * t.R);
+  gl.off_glk = take(gl.near == 2 ? 8ll * t.G : 0);
+  gl.off_gst = take(gl.near == 2 ? 4ll * t.G : 0);
   gl.smem = o;
 }
 
@@ -163,12 +166,10 @@ __device__ __forceinline__ int nearest_sweep(int G, double qk, int start,
 // < 2^44 so equal logs imply equal coordinates).  Hence
 //   best = max(dmin, min(dk_left, dk_right))   (nearest groups to qk)
 //   winner = the leftmost group attaining best, member = staircase(best).
-__device__ __forceinline__ int nearest_one_class(int G, double qk, int start,
-                                                 const double* __restrict__ glk,
-                                                 const int32_t* __restrict__ gstart,
-                                                 const int32_t* __restrict__ gidx, uint64_t dmin,
-                                                 int lastpos, const uint64_t* __restrict__ sD,
-                                                 const int32_t* __restrict__ sP) {
+__device__ __forceinline__ int2 nearest_one_class(int G, double qk, int start,
+                                                  const double* __restrict__ glk, uint64_t dmin,
+                                                  int lastpos, const uint64_t* __restrict__ sD,
+                                                  const int32_t* __restrict__ sP) {
   auto dk = [&](int g) { return abs_bits(__dsub_rn(glk[g], qk)); };
   const uint64_t dkL = start > 0 ? dk(start - 1) : ~0ull;
   const uint64_t dkR = start < G ? dk(start) : ~0ull;
@@ -193,7 +194,7 @@ __device__ __forceinline__ int nearest_one_class(int G, double qk, int start,
     while (sD[s] > mn) ++s;
     pos = sP[s];
   }
-  return gidx[gstart[g] + pos];
+  return make_int2(g, pos);
 }
 
 template <bool VERIFY, int MODE, int NEAR>
@@ -208,146 +209,163 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
   ClassRow* cls = reinterpret_cast<ClassRow*>(smem + gl.off_cls);
   uint64_t* Tmn = reinterpret_cast<uint64_t*>(smem + gl.off_T);
   double* W = reinterpret_cast<double*>(smem + gl.off_W);
+  int32_t* gcur = reinterpret_cast<int32_t*>(smem + gl.off_gcur);
+  double* glk = reinterpret_cast<double*>(smem + gl.off_glk);
+  int32_t* gst = reinterpret_cast<int32_t*>(smem + gl.off_gst);
 
-  const int row = blockIdx.x;
-  const int nN = int(g.nN), nK = int(g.nK);
-  const int im = row / nN, jn = row - im * nN;
+  const int nN = int(g.nN), nK = int(g.nK), rows = int(g.nM * g.nN);
   const int ib0 = int(g.b_lo) + int(blockIdx.z) * gl.bper;
   const int ib1 = min(int(g.b_hi), ib0 + gl.bper);
   if (ib0 >= ib1) return;
   const int nb = ib1 - ib0;
-  const uint64_t m = g.M[im], n = g.N[jn];
-  const double qm = g.logM[im], qn = g.logN[jn];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-
-  // 1. D for every class member (k-independent part of the distance)
-  for (int j = tid; j < t.CM; j += blockDim.x)
-    Dv[j] = umax64(abs_bits(__dsub_rn(t.cls_lm[j], qm)), abs_bits(__dsub_rn(t.cls_ln[j], qn)));
-  if (MODE <= 1) {
-    for (int c = tid; c < t.C; c += blockDim.x)
-      Tmn[c] = curve_valid(t, c)
-                   ? ceil_div(m, t.tile_m[c]) * ceil_div(n, t.tile_n[c]) * t.split_k[c]
-                   : 0;
-  }
-  __syncthreads();
-
-  // 2. per class: prefix-minimum staircase of D in member (scan) order
-  for (int ci = warp; ci < t.NC; ci += nwarps) {
-    const int start = t.cls_start[ci], size = t.cls_size[ci];
-    uint64_t carry = ~0ull;
-    int len = 0, lastpos = 0;
-    for (int base = 0; base < size; base += 32) {
-      const int j = base + lane;
-      const uint64_t d = j < size ? Dv[start + j] : ~0ull;
-      uint64_t pm = d;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
-        if (lane >= off && o < pm) pm = o;
-      }
-      uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
-      if (lane == 0) excl = ~0ull;
-      if (carry < excl) excl = carry;
-      const bool rec = (j < size) && (d < excl);
-      const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
-      if (rec) {
-        const int pos = start + len + __popc(mask & ((1u << lane) - 1u));
-        sD[pos] = d;
-        sP[pos] = j;
-      }
-      if (mask) lastpos = base + 31 - __clz(mask);
-      len += __popc(mask);
-      const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
-      if (tail < carry) carry = tail;
-    }
-    if (lane == 0) cls[ci] = ClassRow{carry, start, len, lastpos, 0};
-  }
-  // 3. wave-scale table W[ib][c] (GEMM families, independent of k)
-  if (MODE == 0) {
-    for (int e = tid; e < nb * t.C; e += blockDim.x) {
-      const int ib = e / t.C;
-      const int c = e - ib * t.C;
-      if (curve_valid(t, c)) W[e] = wave_scale(t, c, ceil_div(g.B[ib0 + ib] * Tmn[c], t.bpw[c]));
-    }
-  }
-  __syncthreads();
-  // 4. per group: lk, class minimum and the scan index attaining it first
-  if (NEAR != 2) {
-    for (int gi = tid; gi < t.G; gi += blockDim.x) {
-      const ClassRow cr = cls[t.grp_class[gi]];
-      const int gb = t.grp_start[gi];
-      grp[gi] = GroupRow{t.grp_lk[gi], cr.dmin, cr.sstart,
-                         cr.len ? t.g_idx[gb + cr.lastpos] : 0x7FFFFFFF, gb, 0};
-    }
-    __syncthreads();
-  }
-  uint64_t dmin1 = 0;
-  int lastpos1 = 0;
-  if (NEAR == 2) {
-    dmin1 = cls[0].dmin;
-    lastpos1 = cls[0].lastpos;
-  }
-
-  // 5. points: thread owns kpt k values (stride blockDim); every batch value
   const int64_t plane = g.nM * g.nN * g.nK;
-  double* const obase = out.lat + int64_t(ib0 - g.b_lo) * plane + int64_t(row) * nK;
   const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
-  for (int j = 0; j < gl.kpt; ++j) {
-    const int ik = k0 + j * int(blockDim.x) + tid;
-    if (ik >= nK) break;
-    const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
-    const int start = __double2loint(ki.y);
-    int best;
-    if (NEAR == 2)
-      best = nearest_one_class(t.G, ki.x, start, t.grp_lk, t.grp_start, t.g_idx, dmin1, lastpos1,
-                               sD, sP);
-    else
-      best = nearest_sweep<NEAR == 1>(t.G, ki.x, start, grp, sD, sP, t.g_idx);
-    const int ci = best < t.R ? t.cand_curve[best] : -1;
-    double* o = obase + ik;
-    if (ci < 0) {
-      if (out.nan_stats) {
-        atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
-        atomicAdd(out.nan_stats + 1, (unsigned long long)nb);
-      }
-      for (int ib = 0; ib < nb; ++ib, o += plane) {
-        *o = qnan();
-        if (VERIFY) {
-          const int64_t p = o - out.lat;
-          out.curve[p] = -1;
-          out.blocks[p] = 0;
-          out.waves[p] = 0;
+
+  // row-independent tables: curve of every candidate in group order, and
+  // (one-class path) the group lk / start arrays
+  for (int j = tid; j < t.R; j += blockDim.x) gcur[j] = t.g_curve[j];
+  if (NEAR == 2) {
+    for (int j = tid; j < t.G; j += blockDim.x) {
+      glk[j] = t.grp_lk[j];
+      gst[j] = t.grp_start[j];
+    }
+  }
+
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int im = row / nN, jn = row - im * nN;
+    const uint64_t m = g.M[im], n = g.N[jn];
+    const double qm = g.logM[im], qn = g.logN[jn];
+    __syncthreads();  // previous row's readers are done with shared memory
+
+    // 1. D for every class member (the k-independent part of the distance)
+    for (int j = tid; j < t.CM; j += blockDim.x)
+      Dv[j] = umax64(abs_bits(__dsub_rn(t.cls_lm[j], qm)), abs_bits(__dsub_rn(t.cls_ln[j], qn)));
+    // 2. tiles per (m, n) and the wave-scale table W[ib][c] (GEMM families)
+    if (MODE <= 1) {
+      for (int c = tid; c < t.C; c += blockDim.x) {
+        if (!curve_valid(t, c)) continue;
+        const uint64_t tmn = ceil_div(m, t.tile_m[c]) * ceil_div(n, t.tile_n[c]) * t.split_k[c];
+        Tmn[c] = tmn;
+        if (MODE == 0) {
+          const uint64_t bpw = t.bpw[c];
+          for (int ib = 0; ib < nb; ++ib)
+            W[ib * t.C + c] = wave_scale(t, c, ceil_div(g.B[ib0 + ib] * tmn, bpw));
         }
       }
-      continue;
     }
-    const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
-    if (MODE == 0 && !VERIFY) {
-      const double* w = W + ci;
-#pragma unroll 4
-      for (int ib = 0; ib < nb; ++ib, o += plane, w += t.C) *o = __dmul_rn(base, *w);
-      continue;
-    }
-    const uint64_t k = g.K[ik];
-    for (int ib = 0; ib < nb; ++ib, o += plane) {
-      double lat;
-      uint64_t blocks, waves;
-      if (MODE <= 1) {
-        blocks = g.B[ib0 + ib] * Tmn[ci];
-        waves = ceil_div(blocks, t.bpw[ci]);
-        lat = __dmul_rn(base, wave_scale(t, ci, waves));
-      } else {
-        const PointResult r = predict_point(t, ci, g.B[ib0 + ib], m, n, k, base);
-        lat = r.lat;
-        blocks = r.blocks;
-        waves = r.waves;
+    __syncthreads();
+
+    // 3. per class: prefix-minimum staircase of D in member (scan) order
+    for (int ci = warp; ci < t.NC; ci += nwarps) {
+      const int start = t.cls_start[ci], size = t.cls_size[ci];
+      uint64_t carry = ~0ull;
+      int len = 0, lastpos = 0;
+      for (int base = 0; base < size; base += 32) {
+        const int j = base + lane;
+        const uint64_t d = j < size ? Dv[start + j] : ~0ull;
+        uint64_t pm = d;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
+          if (lane >= off && o < pm) pm = o;
+        }
+        uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
+        if (lane == 0) excl = ~0ull;
+        if (carry < excl) excl = carry;
+        const bool rec = (j < size) && (d < excl);
+        const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
+        if (rec) {
+          const int pos = start + len + __popc(mask & ((1u << lane) - 1u));
+          sD[pos] = d;
+          sP[pos] = j;
+        }
+        if (mask) lastpos = base + 31 - __clz(mask);
+        len += __popc(mask);
+        const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
+        if (tail < carry) carry = tail;
       }
-      *o = lat;
-      if (VERIFY) {
-        const int64_t p = o - out.lat;
-        out.curve[p] = ci;
-        out.blocks[p] = blocks;
-        out.waves[p] = waves;
+      if (lane == 0) cls[ci] = ClassRow{carry, start, len, lastpos, 0};
+    }
+    __syncthreads();
+    // 4. per group: lk, class minimum and the scan index attaining it first
+    if (NEAR != 2) {
+      for (int gi = tid; gi < t.G; gi += blockDim.x) {
+        const ClassRow cr = cls[t.grp_class[gi]];
+        const int gb = t.grp_start[gi];
+        grp[gi] = GroupRow{t.grp_lk[gi], cr.dmin, cr.sstart,
+                           cr.len ? t.g_idx[gb + cr.lastpos] : 0x7FFFFFFF, gb, 0};
+      }
+      __syncthreads();
+    }
+    uint64_t dmin1 = 0;
+    int lastpos1 = 0;
+    if (NEAR == 2) {
+      dmin1 = cls[0].dmin;
+      lastpos1 = cls[0].lastpos;
+    }
+
+    // 5. points: thread owns kpt k values (stride blockDim); every batch value
+    double* const obase = out.lat + int64_t(ib0 - g.b_lo) * plane + int64_t(row) * nK;
+    for (int j = 0; j < gl.kpt; ++j) {
+      const int ik = k0 + j * int(blockDim.x) + tid;
+      if (ik >= nK) break;
+      const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
+      const int start = __double2loint(ki.y);
+      int ci;
+      if (NEAR == 2) {
+        // group g, member position p -> curve of that candidate (smem)
+        const int2 gp = nearest_one_class(t.G, ki.x, start, glk, dmin1, lastpos1, sD, sP);
+        ci = gcur[gst[gp.x] + gp.y];
+      } else {
+        const int best = nearest_sweep<NEAR == 1>(t.G, ki.x, start, grp, sD, sP, t.g_idx);
+        ci = best < t.R ? t.cand_curve[best] : -1;
+      }
+      double* o = obase + ik;
+      if (ci < 0) {
+        if (out.nan_stats) {
+          atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
+          atomicAdd(out.nan_stats + 1, (unsigned long long)nb);
+        }
+        for (int ib = 0; ib < nb; ++ib, o += plane) {
+          *o = qnan();
+          if (VERIFY) {
+            const int64_t p = o - out.lat;
+            out.curve[p] = -1;
+            out.blocks[p] = 0;
+            out.waves[p] = 0;
+          }
+        }
+        continue;
+      }
+      const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
+      if (MODE == 0 && !VERIFY) {
+        const double* w = W + ci;
+#pragma unroll 4
+        for (int ib = 0; ib < nb; ++ib, o += plane, w += t.C) *o = __dmul_rn(base, *w);
+        continue;
+      }
+      const uint64_t k = g.K[ik];
+      for (int ib = 0; ib < nb; ++ib, o += plane) {
+        double lat;
+        uint64_t blocks, waves;
+        if (MODE <= 1) {
+          blocks = g.B[ib0 + ib] * Tmn[ci];
+          waves = ceil_div(blocks, t.bpw[ci]);
+          lat = __dmul_rn(base, wave_scale(t, ci, waves));
+        } else {
+          const PointResult r = predict_point(t, ci, g.B[ib0 + ib], m, n, k, base);
+          lat = r.lat;
+          blocks = r.blocks;
+          waves = r.waves;
+        }
+        *o = lat;
+        if (VERIFY) {
+          const int64_t p = o - out.lat;
+          out.curve[p] = ci;
+          out.blocks[p] = blocks;
+          out.waves[p] = waves;
+        }
       }
     }
   }
@@ -497,7 +515,12 @@ cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gl.smem));
     if (e != cudaSuccess) return e;
   }
-  const dim3 grid(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
+  // persistent over rows: enough CTAs to fill every SM ~4 deep, each CTA
+  // loops over rows (per-CTA constants are loaded once)
+  const int64_t rows = g.nM * g.nN;
+  const int64_t per_row = int64_t(gl.ktiles) * gl.nbs;
+  const int64_t want = std::max<int64_t>(1, (148 * 4 * 2 + per_row - 1) / per_row);
+  const dim3 grid(unsigned(std::min<int64_t>(rows, want)), unsigned(gl.ktiles), unsigned(gl.nbs));
   fn<<<grid, kThreads, gl.smem, s>>>(t, g, gl, base, out);
   return cudaGetLastError();
 }

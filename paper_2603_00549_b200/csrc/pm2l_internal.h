@@ -46,6 +46,7 @@ struct TablesDev {
   const double* g_ln = nullptr;
   const int32_t* g_idx = nullptr;    // original scan index
   const int32_t* cand_curve = nullptr; // by ORIGINAL index [R]
+  const int32_t* g_curve = nullptr;    // curve of each candidate in GROUP order [R]
   // groups [G]
   const double* grp_lk = nullptr;
   const int32_t* grp_start = nullptr;

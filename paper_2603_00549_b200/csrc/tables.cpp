@@ -142,8 +142,9 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
       grp_class[gi] = it->second;
     }
   }
-  std::vector<int32_t> cand_curve(R);
+  std::vector<int32_t> cand_curve(R), g_curve(R);
   for (int64_t i = 0; i < R; ++i) cand_curve[i] = int32_t(v->cand_curve[i]);
+  for (int64_t p = 0; p < R; ++p) g_curve[p] = cand_curve[g_idx[p]];
 
   // --- exact records, unpacked and sorted by (b, m, n, k)
   std::vector<std::array<uint64_t, 6>> ex(R);
@@ -203,6 +204,7 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.g_ln = blob.add(g_ln);
   t.g_idx = blob.add(g_idx);
   t.cand_curve = blob.add(cand_curve);
+  t.g_curve = blob.add(g_curve);
   t.grp_lk = blob.add(grp_lk);
   t.grp_start = blob.add(grp_start);
   t.grp_size = blob.add(grp_size);
@@ -231,6 +233,7 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.s_dims = shift(o.s_dims, base); t.s_thrs = shift(o.s_thrs, base);
   t.g_lm = shift(o.g_lm, base); t.g_ln = shift(o.g_ln, base);
   t.g_idx = shift(o.g_idx, base); t.cand_curve = shift(o.cand_curve, base);
+  t.g_curve = shift(o.g_curve, base);
   t.grp_lk = shift(o.grp_lk, base); t.grp_start = shift(o.grp_start, base);
   t.grp_size = shift(o.grp_size, base); t.grp_class = shift(o.grp_class, base);
   t.cls_start = shift(o.cls_start, base); t.cls_size = shift(o.cls_size, base);
