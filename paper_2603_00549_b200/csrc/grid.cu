@@ -2,18 +2,17 @@
 // (pm2lat/_kernels.pyx:76-133, backend.py:49-88), plus "mode X" (every
 // candidate kernel per shape) and the unresolved-point scan.
 //
-// Decomposition.  One CTA per ((m, n) row, k tile, batch slab).  Everything
-// that does not depend on k is built once per CTA in shared memory:
-//   * D_j = max(|lm_j - qm|, |ln_j - qn|) for every member j of every member
-//     class, and its prefix-minimum staircase (warp scan + ballot);
-//   * per k-group: lk, the group minimum dmin and the scan index that attains
-//     it first;
-//   * Tmn[c] = ceil(m/tm)*ceil(n/tn)*split_k and the wave-scale table
-//     W[ib][c] = ceil(b*Tmn[c]/bpw) / ref_waves  (GEMM families).
-// Each thread then owns k values; per k it runs the outward k-group sweep
-// (nearest config), reads base(curve, k) from the per-launch base table and
-// writes one f64 per batch value with coalesced stores: the only per-point
-// arithmetic is one DMUL.
+// Per launch (all device-side, CUDA-graph capturable):
+//   base_table_kernel  base(c, k) = ref_dur*(k/ref_dim)*(ref_thr/thr(c,k)) for
+//                      every curve and k value (per-curve samples in smem)
+//   row_prep_kernel    one warp per (m, n) row: D_j = max(|lm_j-qm|, |ln_j-qn|)
+//                      for every class member and its prefix-minimum staircase
+//                      (warp scan + ballot), Tmn[c] = ceil(m/tm)*ceil(n/tn)*sk
+//                      and the wave-scale table W[ib][c] = waves / ref_waves
+//   grid_kernel        one thread per (row, k): nearest config (outward k-group
+//                      sweep over the row's staircases), then one DMUL and one
+//                      coalesced 8-byte store per batch value
+//   fixup_kernel       exact-record hits (take priority over nearest)
 #include <algorithm>
 
 #include "common.cuh"
@@ -62,55 +61,135 @@ struct GridLaunch {
   int bper;      // batch values per slab
   int mode;      // 0: GEMM + W table, 1: GEMM per point, 2: general (row-block)
   int near;      // 0: general sweep, 1: sweep + tie mask (G <= 32), 2: one member class
-  // shared-memory layout (byte offsets), computed on the host
-  int off_D, off_sD, off_sP, off_grp, off_cls, off_T, off_W, off_gcur, off_glk, off_gst;
-  int64_t smem;
 };
 
-struct __align__(16) GroupRow {
-  double lk;      // log2 k of the group
-  uint64_t dmin;  // min over members of D (ordered bits) — from the class
-  int32_t sstart; // class staircase start (smem index)
-  int32_t last;   // scan index attaining dmin first
-  int32_t gbase;  // group start in group order (member position -> g_idx)
-  int32_t pad;
-};
-
+// Per-row state written by row_prep_kernel (workspace, L2-resident).
 struct ClassRow {
-  uint64_t dmin;
-  int32_t sstart, len, lastpos, pad;
+  uint64_t dmin;    // min over the class members of D (ordered bits)
+  int32_t lastpos;  // member position attaining dmin first
+  int32_t len;      // staircase length
 };
 
-void layout(const TablesDev& t, GridLaunch& gl) {
+struct RowWs {
+  ClassRow* cls;   // [rows][NC]
+  uint64_t* sD;    // [rows][CM] staircase D (class segments at cls_start)
+  int32_t* sP;     // [rows][CM] staircase member positions
+  uint64_t* T;     // [rows][C]  tiles per (m, n)     (modes 0, 1)
+  double* W;       // [rows][nb][C] wave scale         (mode 0)
+};
+
+// Workspace layout (doubles): base table, then the row state.
+struct WsLayout {
+  int64_t base, cls, sD, sP, T, W, total;
+};
+
+WsLayout ws_layout(const TablesDev& t, const GridDev& g, const GridLaunch& gl) {
+  WsLayout L;
+  const int64_t rows = g.nM * g.nN, nb = g.b_hi - g.b_lo;
   int64_t o = 0;
-  auto take = [&](int64_t bytes) {
+  auto take = [&](int64_t doubles) {
     const int64_t at = o;
-    o = (o + bytes + 15) & ~int64_t(15);
-    return int(at);
+    o += (doubles + 31) & ~int64_t(31);  // 256-byte aligned sections
+    return at;
   };
-  gl.off_D = take(8ll * t.CM);
-  gl.off_sD = take(8ll * t.CM);
-  gl.off_sP = take(4ll * t.CM);
-  gl.off_grp = take(gl.near == 2 ? 0 : int64_t(sizeof(GroupRow)) * t.G);
-  gl.off_cls = take(int64_t(sizeof(ClassRow)) * t.NC);
-  gl.off_T = take(gl.mode <= 1 ? 8ll * t.C : 0);
-  gl.off_W = take(gl.mode == 0 ? 8ll * t.C * gl.bper : 0);
-  gl.off_gcur = take(4ll * t.R);
-  gl.off_glk = take(gl.near == 2 ? 8ll * t.G : 0);
-  gl.off_gst = take(gl.near == 2 ? 4ll * t.G : 0);
-  gl.smem = o;
+  L.base = take(int64_t(t.C) * g.nK);
+  L.cls = take(rows * t.NC * 2);
+  L.sD = take(rows * t.CM);
+  L.sP = take((rows * t.CM + 1) / 2);
+  L.T = take(gl.mode <= 1 ? rows * t.C : 0);
+  L.W = take(gl.mode == 0 ? rows * nb * t.C : 0);
+  L.total = o;
+  return L;
 }
 
-// Scan index of the first member of group gr whose distance equals `best`
+RowWs row_ws(const WsLayout& L, double* ws) {
+  return RowWs{reinterpret_cast<ClassRow*>(ws + L.cls), reinterpret_cast<uint64_t*>(ws + L.sD),
+               reinterpret_cast<int32_t*>(ws + L.sP), reinterpret_cast<uint64_t*>(ws + L.T),
+               ws + L.W};
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) row_prep_kernel(TablesDev t, GridDev g, RowWs ws) {
+  const int lane = threadIdx.x & 31;
+  const int row = int((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5);
+  const int rows = int(g.nM * g.nN);
+  if (row >= rows) return;
+  const int nN = int(g.nN);
+  const int im = row / nN, jn = row - im * nN;
+  const uint64_t m = g.M[im], n = g.N[jn];
+  const double qm = g.logM[im], qn = g.logN[jn];
+  uint64_t* sD = ws.sD + int64_t(row) * t.CM;
+  int32_t* sP = ws.sP + int64_t(row) * t.CM;
+  // prefix-minimum staircase of D per member class, in member (scan) order
+  for (int ci = 0; ci < t.NC; ++ci) {
+    const int start = t.cls_start[ci], size = t.cls_size[ci];
+    uint64_t carry = ~0ull;
+    int len = 0, lastpos = 0;
+    for (int base = 0; base < size; base += 32) {
+      const int j = base + lane;
+      const uint64_t d = j < size ? umax64(abs_bits(__dsub_rn(t.cls_lm[start + j], qm)),
+                                           abs_bits(__dsub_rn(t.cls_ln[start + j], qn)))
+                                  : ~0ull;
+      uint64_t pm = d;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
+        if (lane >= off && o < pm) pm = o;
+      }
+      uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
+      if (lane == 0) excl = ~0ull;
+      if (carry < excl) excl = carry;
+      const bool rec = (j < size) && (d < excl);
+      const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
+      if (rec) {
+        const int pos = start + len + __popc(mask & ((1u << lane) - 1u));
+        sD[pos] = d;
+        sP[pos] = j;
+      }
+      if (mask) lastpos = base + 31 - __clz(mask);
+      len += __popc(mask);
+      const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
+      if (tail < carry) carry = tail;
+    }
+    if (lane == 0) ws.cls[int64_t(row) * t.NC + ci] = ClassRow{carry, lastpos, len};
+  }
+  // tiles per (m, n) and the wave-scale table (GEMM families)
+  if (MODE <= 1) {
+    const int nb = int(g.b_hi - g.b_lo);
+    uint64_t* T = ws.T + int64_t(row) * t.C;
+    double* W = ws.W + int64_t(row) * nb * t.C;
+    for (int c = lane; c < t.C; c += 32) {
+      if (!curve_valid(t, c)) continue;
+      const uint64_t tmn = ceil_div(m, t.tile_m[c]) * ceil_div(n, t.tile_n[c]) * t.split_k[c];
+      T[c] = tmn;
+      if (MODE == 0) {
+        const uint64_t bpw = t.bpw[c];
+        for (int ib = 0; ib < nb; ++ib)
+          W[ib * t.C + c] = wave_scale(t, c, ceil_div(g.B[g.b_lo + ib] * tmn, bpw));
+      }
+    }
+  }
+}
+
+// Scan index of the first member of group g whose distance equals `best`
 // (the group attains best): the first staircase entry with D <= best.
-__device__ __forceinline__ int stair_index(const GroupRow& gr, uint64_t best,
-                                           const uint64_t* __restrict__ sD,
-                                           const int32_t* __restrict__ sP,
-                                           const int32_t* __restrict__ gidx) {
-  if (best == gr.dmin) return gr.last;
-  int s = gr.sstart;
-  while (sD[s] > best) ++s;
-  return gidx[gr.gbase + sP[s]];
+struct RowView {
+  const ClassRow* cls;
+  const uint64_t* sD;
+  const int32_t* sP;
+};
+
+__device__ __forceinline__ int group_index(const TablesDev& t, const RowView& rv, int g,
+                                           uint64_t best) {
+  const int c = t.grp_class[g];
+  const ClassRow cr = rv.cls[c];
+  int pos = cr.lastpos;
+  if (best != cr.dmin) {
+    int s = t.cls_start[c];
+    while (rv.sD[s] > best) ++s;
+    pos = rv.sP[s];
+  }
+  return t.g_idx[t.grp_start[g] + pos];
 }
 
 // Nearest-config argmin for one query k (_kernels.pyx:29-47 semantics).
@@ -121,30 +200,26 @@ __device__ __forceinline__ int stair_index(const GroupRow& gr, uint64_t best,
 // smallest scan index among every member attaining the final best.
 // Returns the ORIGINAL candidate scan index (INT32_MAX when G == 0).
 template <bool G32>
-__device__ __forceinline__ int nearest_sweep(int G, double qk, int start,
-                                             const GroupRow* __restrict__ grp,
-                                             const uint64_t* __restrict__ sD,
-                                             const int32_t* __restrict__ sP,
-                                             const int32_t* __restrict__ gidx) {
+__device__ __forceinline__ int nearest_sweep(const TablesDev& t, const RowView& rv, double qk,
+                                             int start) {
   uint64_t best = ~0ull;
   uint32_t mask = 0;
   int best_i = 0x7FFFFFFF;
   auto visit = [&](int g) -> bool {
-    const double2 v = *reinterpret_cast<const double2*>(&grp[g]);
-    const uint64_t dk = abs_bits(__dsub_rn(v.x, qk));
+    const uint64_t dk = abs_bits(__dsub_rn(t.grp_lk[g], qk));
     if (dk > best) return false;
-    const uint64_t dg = umax64(dk, static_cast<uint64_t>(__double_as_longlong(v.y)));
+    const uint64_t dg = umax64(dk, rv.cls[t.grp_class[g]].dmin);
     if (G32) {
       if (dg < best) { best = dg; mask = 1u << g; }
       else if (dg == best) mask |= 1u << g;
     } else if (dg <= best) {
-      const int idx = stair_index(grp[g], dg, sD, sP, gidx);
+      const int idx = group_index(t, rv, g, dg);
       if (dg < best || idx < best_i) best_i = idx;
       best = dg;
     }
     return true;
   };
-  for (int g = start; g < G; ++g)
+  for (int g = start; g < t.G; ++g)
     if (!visit(g)) break;
   for (int g = start - 1; g >= 0; --g)
     if (!visit(g)) break;
@@ -152,7 +227,7 @@ __device__ __forceinline__ int nearest_sweep(int G, double qk, int start,
     while (mask) {
       const int g = __ffs(mask) - 1;
       mask &= mask - 1;
-      const int idx = stair_index(grp[g], best, sD, sP, gidx);
+      const int idx = group_index(t, rv, g, best);
       best_i = idx < best_i ? idx : best_i;
     }
   }
@@ -166,13 +241,14 @@ __device__ __forceinline__ int nearest_sweep(int G, double qk, int start,
 // < 2^44 so equal logs imply equal coordinates).  Hence
 //   best = max(dmin, min(dk_left, dk_right))   (nearest groups to qk)
 //   winner = the leftmost group attaining best, member = staircase(best).
-__device__ __forceinline__ int2 nearest_one_class(int G, double qk, int start,
-                                                  const double* __restrict__ glk, uint64_t dmin,
-                                                  int lastpos, const uint64_t* __restrict__ sD,
-                                                  const int32_t* __restrict__ sP) {
+// Returns (group, member position).
+__device__ __forceinline__ int2 nearest_one_class(const TablesDev& t, const RowView& rv,
+                                                  uint64_t dmin, int lastpos, double qk,
+                                                  int start) {
+  const double* glk = t.grp_lk;
   auto dk = [&](int g) { return abs_bits(__dsub_rn(glk[g], qk)); };
   const uint64_t dkL = start > 0 ? dk(start - 1) : ~0ull;
-  const uint64_t dkR = start < G ? dk(start) : ~0ull;
+  const uint64_t dkR = start < t.G ? dk(start) : ~0ull;
   const uint64_t mn = dkL < dkR ? dkL : dkR;
   int g, pos;
   if (mn <= dmin) {            // best == dmin: every group with dk <= dmin ties
@@ -191,8 +267,8 @@ __device__ __forceinline__ int2 nearest_one_class(int G, double qk, int start,
       g = start;
     }
     int s = 0;
-    while (sD[s] > mn) ++s;
-    pos = sP[s];
+    while (rv.sD[s] > mn) ++s;
+    pos = rv.sP[s];
   }
   return make_int2(g, pos);
 }
@@ -200,172 +276,85 @@ __device__ __forceinline__ int2 nearest_one_class(int G, double qk, int start,
 template <bool VERIFY, int MODE, int NEAR>
 __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
                                                         const double* __restrict__ base_tab,
-                                                        LaunchOut out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* Dv = reinterpret_cast<uint64_t*>(smem + gl.off_D);
-  uint64_t* sD = reinterpret_cast<uint64_t*>(smem + gl.off_sD);
-  int32_t* sP = reinterpret_cast<int32_t*>(smem + gl.off_sP);
-  GroupRow* grp = reinterpret_cast<GroupRow*>(smem + gl.off_grp);
-  ClassRow* cls = reinterpret_cast<ClassRow*>(smem + gl.off_cls);
-  uint64_t* Tmn = reinterpret_cast<uint64_t*>(smem + gl.off_T);
-  double* W = reinterpret_cast<double*>(smem + gl.off_W);
-  int32_t* gcur = reinterpret_cast<int32_t*>(smem + gl.off_gcur);
-  double* glk = reinterpret_cast<double*>(smem + gl.off_glk);
-  int32_t* gst = reinterpret_cast<int32_t*>(smem + gl.off_gst);
-
-  const int nN = int(g.nN), nK = int(g.nK), rows = int(g.nM * g.nN);
-  const int ib0 = int(g.b_lo) + int(blockIdx.z) * gl.bper;
-  const int ib1 = min(int(g.b_hi), ib0 + gl.bper);
-  if (ib0 >= ib1) return;
-  const int nb = ib1 - ib0;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int64_t plane = g.nM * g.nN * g.nK;
-  const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
-
-  // row-independent tables: curve of every candidate in group order, and
-  // (one-class path) the group lk / start arrays
-  for (int j = tid; j < t.R; j += blockDim.x) gcur[j] = t.g_curve[j];
+                                                        RowWs ws, LaunchOut out) {
+  const int row = blockIdx.x;
+  const int nN = int(g.nN), nK = int(g.nK);
+  const int ib0 = int(blockIdx.z) * gl.bper;  // slice-relative
+  const int ib1 = min(int(g.b_hi - g.b_lo), ib0 + gl.bper);
+  const int nb = ib1 - ib0, nbs_all = int(g.b_hi - g.b_lo);
+  const RowView rv{ws.cls + int64_t(row) * t.NC, ws.sD + int64_t(row) * t.CM,
+                   ws.sP + int64_t(row) * t.CM};
+  uint64_t dmin1 = 0;
+  int lastpos1 = 0;
   if (NEAR == 2) {
-    for (int j = tid; j < t.G; j += blockDim.x) {
-      glk[j] = t.grp_lk[j];
-      gst[j] = t.grp_start[j];
-    }
+    const ClassRow cr = rv.cls[0];
+    dmin1 = cr.dmin;
+    lastpos1 = cr.lastpos;
   }
-
-  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
-    const int im = row / nN, jn = row - im * nN;
-    const uint64_t m = g.M[im], n = g.N[jn];
-    const double qm = g.logM[im], qn = g.logN[jn];
-    __syncthreads();  // previous row's readers are done with shared memory
-
-    // 1. D for every class member (the k-independent part of the distance)
-    for (int j = tid; j < t.CM; j += blockDim.x)
-      Dv[j] = umax64(abs_bits(__dsub_rn(t.cls_lm[j], qm)), abs_bits(__dsub_rn(t.cls_ln[j], qn)));
-    // 2. tiles per (m, n) and the wave-scale table W[ib][c] (GEMM families)
-    if (MODE <= 1) {
-      for (int c = tid; c < t.C; c += blockDim.x) {
-        if (!curve_valid(t, c)) continue;
-        const uint64_t tmn = ceil_div(m, t.tile_m[c]) * ceil_div(n, t.tile_n[c]) * t.split_k[c];
-        Tmn[c] = tmn;
-        if (MODE == 0) {
-          const uint64_t bpw = t.bpw[c];
-          for (int ib = 0; ib < nb; ++ib)
-            W[ib * t.C + c] = wave_scale(t, c, ceil_div(g.B[ib0 + ib] * tmn, bpw));
-        }
-      }
-    }
-    __syncthreads();
-
-    // 3. per class: prefix-minimum staircase of D in member (scan) order
-    for (int ci = warp; ci < t.NC; ci += nwarps) {
-      const int start = t.cls_start[ci], size = t.cls_size[ci];
-      uint64_t carry = ~0ull;
-      int len = 0, lastpos = 0;
-      for (int base = 0; base < size; base += 32) {
-        const int j = base + lane;
-        const uint64_t d = j < size ? Dv[start + j] : ~0ull;
-        uint64_t pm = d;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
-          if (lane >= off && o < pm) pm = o;
-        }
-        uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
-        if (lane == 0) excl = ~0ull;
-        if (carry < excl) excl = carry;
-        const bool rec = (j < size) && (d < excl);
-        const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
-        if (rec) {
-          const int pos = start + len + __popc(mask & ((1u << lane) - 1u));
-          sD[pos] = d;
-          sP[pos] = j;
-        }
-        if (mask) lastpos = base + 31 - __clz(mask);
-        len += __popc(mask);
-        const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
-        if (tail < carry) carry = tail;
-      }
-      if (lane == 0) cls[ci] = ClassRow{carry, start, len, lastpos, 0};
-    }
-    __syncthreads();
-    // 4. per group: lk, class minimum and the scan index attaining it first
-    if (NEAR != 2) {
-      for (int gi = tid; gi < t.G; gi += blockDim.x) {
-        const ClassRow cr = cls[t.grp_class[gi]];
-        const int gb = t.grp_start[gi];
-        grp[gi] = GroupRow{t.grp_lk[gi], cr.dmin, cr.sstart,
-                           cr.len ? t.g_idx[gb + cr.lastpos] : 0x7FFFFFFF, gb, 0};
-      }
-      __syncthreads();
-    }
-    uint64_t dmin1 = 0;
-    int lastpos1 = 0;
+  const int64_t plane = g.nM * g.nN * g.nK;
+  double* const obase = out.lat + int64_t(ib0) * plane + int64_t(row) * nK;
+  const double* Wrow = MODE == 0 ? ws.W + (int64_t(row) * nbs_all + ib0) * t.C : nullptr;
+  const uint64_t* Trow = MODE <= 1 ? ws.T + int64_t(row) * t.C : nullptr;
+  const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
+  for (int j = 0; j < gl.kpt; ++j) {
+    const int ik = k0 + j * int(blockDim.x) + int(threadIdx.x);
+    if (ik >= nK) break;
+    const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
+    const int start = __double2loint(ki.y);
+    int ci;
     if (NEAR == 2) {
-      dmin1 = cls[0].dmin;
-      lastpos1 = cls[0].lastpos;
+      const int2 gp = nearest_one_class(t, rv, dmin1, lastpos1, ki.x, start);
+      ci = t.g_curve[t.grp_start[gp.x] + gp.y];
+    } else {
+      const int best = nearest_sweep<NEAR == 1>(t, rv, ki.x, start);
+      ci = best < t.R ? t.cand_curve[best] : -1;
     }
-
-    // 5. points: thread owns kpt k values (stride blockDim); every batch value
-    double* const obase = out.lat + int64_t(ib0 - g.b_lo) * plane + int64_t(row) * nK;
-    for (int j = 0; j < gl.kpt; ++j) {
-      const int ik = k0 + j * int(blockDim.x) + tid;
-      if (ik >= nK) break;
-      const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
-      const int start = __double2loint(ki.y);
-      int ci;
-      if (NEAR == 2) {
-        // group g, member position p -> curve of that candidate (smem)
-        const int2 gp = nearest_one_class(t.G, ki.x, start, glk, dmin1, lastpos1, sD, sP);
-        ci = gcur[gst[gp.x] + gp.y];
-      } else {
-        const int best = nearest_sweep<NEAR == 1>(t.G, ki.x, start, grp, sD, sP, t.g_idx);
-        ci = best < t.R ? t.cand_curve[best] : -1;
+    double* o = obase + ik;
+    if (ci < 0) {
+      if (out.nan_stats) {
+        atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
+        atomicAdd(out.nan_stats + 1, (unsigned long long)nb);
       }
-      double* o = obase + ik;
-      if (ci < 0) {
-        if (out.nan_stats) {
-          atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
-          atomicAdd(out.nan_stats + 1, (unsigned long long)nb);
-        }
-        for (int ib = 0; ib < nb; ++ib, o += plane) {
-          *o = qnan();
-          if (VERIFY) {
-            const int64_t p = o - out.lat;
-            out.curve[p] = -1;
-            out.blocks[p] = 0;
-            out.waves[p] = 0;
-          }
-        }
-        continue;
-      }
-      const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
-      if (MODE == 0 && !VERIFY) {
-        const double* w = W + ci;
-#pragma unroll 4
-        for (int ib = 0; ib < nb; ++ib, o += plane, w += t.C) *o = __dmul_rn(base, *w);
-        continue;
-      }
-      const uint64_t k = g.K[ik];
       for (int ib = 0; ib < nb; ++ib, o += plane) {
-        double lat;
-        uint64_t blocks, waves;
-        if (MODE <= 1) {
-          blocks = g.B[ib0 + ib] * Tmn[ci];
-          waves = ceil_div(blocks, t.bpw[ci]);
-          lat = __dmul_rn(base, wave_scale(t, ci, waves));
-        } else {
-          const PointResult r = predict_point(t, ci, g.B[ib0 + ib], m, n, k, base);
-          lat = r.lat;
-          blocks = r.blocks;
-          waves = r.waves;
-        }
-        *o = lat;
+        *o = qnan();
         if (VERIFY) {
           const int64_t p = o - out.lat;
-          out.curve[p] = ci;
-          out.blocks[p] = blocks;
-          out.waves[p] = waves;
+          out.curve[p] = -1;
+          out.blocks[p] = 0;
+          out.waves[p] = 0;
         }
+      }
+      continue;
+    }
+    const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
+    if (MODE == 0 && !VERIFY) {
+      const double* w = Wrow + ci;
+#pragma unroll 4
+      for (int ib = 0; ib < nb; ++ib, o += plane, w += t.C) *o = __dmul_rn(base, *w);
+      continue;
+    }
+    const uint64_t k = g.K[ik];
+    const int im = row / nN, jn = row - im * nN;
+    for (int ib = 0; ib < nb; ++ib, o += plane) {
+      const uint64_t b = g.B[g.b_lo + ib0 + ib];
+      double lat;
+      uint64_t blocks, waves;
+      if (MODE <= 1) {
+        blocks = b * Trow[ci];
+        waves = ceil_div(blocks, t.bpw[ci]);
+        lat = __dmul_rn(base, wave_scale(t, ci, waves));
+      } else {
+        const PointResult r = predict_point(t, ci, b, g.M[im], g.N[jn], k, base);
+        lat = r.lat;
+        blocks = r.blocks;
+        waves = r.waves;
+      }
+      *o = lat;
+      if (VERIFY) {
+        const int64_t p = o - out.lat;
+        out.curve[p] = ci;
+        out.blocks[p] = blocks;
+        out.waves[p] = waves;
       }
     }
   }
@@ -479,7 +468,7 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   };
   gl.kpt = 4;
   gl.ktiles = ktiles_for(gl.kpt);
-  while (gl.kpt > 1 && rows * gl.ktiles < target) {
+  while (gl.kpt > 1 && rows * gl.ktiles < 4 * target) {
     gl.kpt >>= 1;
     gl.ktiles = ktiles_for(gl.kpt);
   }
@@ -490,14 +479,12 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   gl.nbs = int((nb + gl.bper - 1) / gl.bper);
   if (all_curves) {
     gl.mode = (t.all_gemm && 8ll * t.C * (gl.bper + 1) <= 96 * 1024) ? 0 : 2;
-    gl.smem = gl.mode == 0 ? ((8ll * t.C + 15) & ~15ll) + 8ll * t.C * gl.bper : 0;
     return gl;
   }
   if (!t.all_gemm) gl.mode = 2;
-  else if (8ll * t.C * gl.bper <= 48 * 1024 && t.C <= 4 * g.nK) gl.mode = 0;
+  else if (rows * nb * t.C <= (int64_t(1) << 27)) gl.mode = 0;  // W table <= 1 GiB
   else gl.mode = 1;
   gl.near = (t.NC == 1 && t.lowest_wins) ? 2 : (t.G <= 32 ? 1 : 0);
-  layout(t, gl);
   return gl;
 }
 
@@ -508,20 +495,12 @@ bool grid_dims_ok(const GridDev& g, const GridLaunch& gl) {
 
 template <bool V, int M>
 cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
-                          const double* base, const LaunchOut& out, cudaStream_t s) {
+                          const double* base, const RowWs& ws, const LaunchOut& out,
+                          cudaStream_t s) {
   auto* fn = gl.near == 2 ? grid_kernel<V, M, 2> : gl.near == 1 ? grid_kernel<V, M, 1>
                                                                  : grid_kernel<V, M, 0>;
-  if (gl.smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gl.smem));
-    if (e != cudaSuccess) return e;
-  }
-  // persistent over rows: enough CTAs to fill every SM ~4 deep, each CTA
-  // loops over rows (per-CTA constants are loaded once)
-  const int64_t rows = g.nM * g.nN;
-  const int64_t per_row = int64_t(gl.ktiles) * gl.nbs;
-  const int64_t want = std::max<int64_t>(1, (148 * 4 * 2 + per_row - 1) / per_row);
-  const dim3 grid(unsigned(std::min<int64_t>(rows, want)), unsigned(gl.ktiles), unsigned(gl.nbs));
-  fn<<<grid, kThreads, gl.smem, s>>>(t, g, gl, base, out);
+  const dim3 grid(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
+  fn<<<grid, kThreads, 0, s>>>(t, g, gl, base, ws, out);
   return cudaGetLastError();
 }
 
@@ -533,8 +512,7 @@ void launch_base_table(const TablesDev& t, const GridDev& g, double* ws, cudaStr
 }  // namespace
 
 int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g) {
-  const int64_t e = int64_t(t.C) * g.nK;
-  return e <= (int64_t(1) << 25) ? e : 0;  // base table only when <= 256 MiB
+  return ws_layout(t, g, plan_grid(t, g, false)).total;
 }
 
 int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, double* ws,
@@ -543,24 +521,31 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
   if (card == 0) return 0;
   const GridLaunch gl = plan_grid(t, g, false);
-  if (gl.smem > 227 * 1024 || !grid_dims_ok(g, gl) || int64_t(t.C) * g.nK > 0x7FFFFFFFll)
+  const WsLayout L = ws_layout(t, g, gl);
+  if (!ws || ws_elems < L.total || !grid_dims_ok(g, gl) || t.C > 65535 ||
+      int64_t(t.C) * g.nK > 0x7FFFFFFFll)
     return int(cudaErrorInvalidValue);
-  const double* base = nullptr;
-  if (ws && ws_elems >= int64_t(t.C) * g.nK && t.C > 0 && t.C <= 65535) {
-    if (stages & kStageBase) launch_base_table(t, g, ws, s);
-    base = ws;
+  const RowWs rws = row_ws(L, ws);
+  const double* base = t.C > 0 ? ws + L.base : nullptr;
+  const int64_t rows = g.nM * g.nN;
+  if (stages & kStageBase) {
+    if (t.C > 0) launch_base_table(t, g, ws + L.base, s);
+    const int nb = int((rows * 32 + 255) / 256);
+    if (gl.mode == 0) row_prep_kernel<0><<<nb, 256, 0, s>>>(t, g, rws);
+    else if (gl.mode == 1) row_prep_kernel<1><<<nb, 256, 0, s>>>(t, g, rws);
+    else row_prep_kernel<2><<<nb, 256, 0, s>>>(t, g, rws);
   }
   const bool v = out.curve != nullptr;
   cudaError_t e = cudaSuccess;
   if (stages & kStageGrid) {
     if (v) {
-      e = gl.mode == 0 ? launch_grid_t<true, 0>(t, g, gl, base, out, s)
-          : gl.mode == 1 ? launch_grid_t<true, 1>(t, g, gl, base, out, s)
-                         : launch_grid_t<true, 2>(t, g, gl, base, out, s);
+      e = gl.mode == 0 ? launch_grid_t<true, 0>(t, g, gl, base, rws, out, s)
+          : gl.mode == 1 ? launch_grid_t<true, 1>(t, g, gl, base, rws, out, s)
+                         : launch_grid_t<true, 2>(t, g, gl, base, rws, out, s);
     } else {
-      e = gl.mode == 0 ? launch_grid_t<false, 0>(t, g, gl, base, out, s)
-          : gl.mode == 1 ? launch_grid_t<false, 1>(t, g, gl, base, out, s)
-                         : launch_grid_t<false, 2>(t, g, gl, base, out, s);
+      e = gl.mode == 0 ? launch_grid_t<false, 0>(t, g, gl, base, rws, out, s)
+          : gl.mode == 1 ? launch_grid_t<false, 1>(t, g, gl, base, rws, out, s)
+                         : launch_grid_t<false, 2>(t, g, gl, base, rws, out, s);
     }
   }
   if (e != cudaSuccess) return int(e);
@@ -577,16 +562,17 @@ int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* ws, dou
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
   if (card == 0 || t.C == 0) return 0;
-  const GridLaunch gl = plan_grid(t, g, true);
+  GridLaunch gl = plan_grid(t, g, true);
   if (!grid_dims_ok(g, gl) || t.C > 65535) return int(cudaErrorInvalidValue);
   launch_base_table(t, g, ws, s);
-  if (gl.smem > 48 * 1024) {
+  const int64_t smem = gl.mode == 0 ? ((8ll * t.C + 15) & ~15ll) + 8ll * t.C * gl.bper : 0;
+  if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(all_curves_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(gl.smem));
+                                         int(smem));
     if (e != cudaSuccess) return int(e);
   }
   const dim3 grid(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
-  all_curves_kernel<<<grid, kThreads, gl.smem, s>>>(t, g, gl, ws, out);
+  all_curves_kernel<<<grid, kThreads, smem, s>>>(t, g, gl, ws, out);
   return int(cudaGetLastError());
 }
 
