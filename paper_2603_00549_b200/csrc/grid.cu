@@ -61,7 +61,27 @@ struct GridLaunch {
   int bper;      // batch values per slab
   int mode;      // 0: GEMM + W table, 1: GEMM per point, 2: general (row-block)
   int near;      // 0: general sweep, 1: sweep + tie mask (G <= 32), 2: one member class
+  // grid_kernel shared-memory layout (byte offsets), computed on the host
+  int off_sD, off_sP, off_cls, off_W, off_gcur, off_gst, off_glk;
+  int64_t smem;
 };
+
+void smem_layout(const TablesDev& t, GridLaunch& gl) {
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = o;
+    o = (o + bytes + 15) & ~int64_t(15);
+    return int(at);
+  };
+  gl.off_sD = take(8ll * t.CM);
+  gl.off_sP = take(4ll * t.CM);
+  gl.off_cls = take(16ll * t.NC);
+  gl.off_W = take(gl.mode == 0 ? 8ll * t.C * gl.bper : 0);
+  gl.off_gcur = take(4ll * t.R);
+  gl.off_gst = take(4ll * t.G);
+  gl.off_glk = take(8ll * t.G);
+  gl.smem = o;
+}
 
 // Per-row state written by row_prep_kernel (workspace, L2-resident).
 struct ClassRow {
@@ -108,57 +128,93 @@ RowWs row_ws(const WsLayout& L, double* ws) {
                ws + L.W};
 }
 
+// Fused per-launch preparation, 64 threads per CTA:
+//   CTAs [0, rows):         one (m, n) row each — warp 0 builds the member-class
+//                           staircases, all threads build Tmn / W over curves
+//   CTAs [rows, rows + C*kc): base table, one (curve, 64-k chunk) each, with the
+//                           curve's samples staged in shared memory
+constexpr int kPrepThreads = 64;
+
 template <int MODE>
-__global__ void __launch_bounds__(256) row_prep_kernel(TablesDev t, GridDev g, RowWs ws) {
-  const int lane = threadIdx.x & 31;
-  const int row = int((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5);
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(TablesDev t, GridDev g, RowWs ws,
+                                                            double* __restrict__ base, int kchunks) {
   const int rows = int(g.nM * g.nN);
-  if (row >= rows) return;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (int(blockIdx.x) >= rows) {
+    // ---- base table: base[c][ik]
+    __shared__ double sd[kMaxSmemSamples], sy[kMaxSmemSamples];
+    const int e = int(blockIdx.x) - rows;
+    const int c = e / kchunks, chunk = e - c * kchunks;
+    const int nK = int(g.nK);
+    const int ik = chunk * kPrepThreads + tid;
+    const int lo = t.s_off[c], hi = t.s_off[c + 1], ns = hi - lo;
+    if (ns <= 0) {
+      if (ik < nK) base[int64_t(c) * nK + ik] = 0.0;
+      return;
+    }
+    const bool staged = ns <= kMaxSmemSamples;
+    if (staged)
+      for (int j = tid; j < ns; j += kPrepThreads) {
+        sd[j] = t.s_dims[lo + j];
+        sy[j] = t.s_thrs[lo + j];
+      }
+    __syncthreads();
+    if (ik >= nK) return;
+    const double nd = __ull2double_rn(g.K[ik]);
+    const double thr = staged ? interp_samples(sd, sy, 0, ns, nd)
+                              : interp_samples(t.s_dims, t.s_thrs, lo, hi, nd);
+    base[int64_t(c) * nK + ik] = base_from_thr(t, c, nd, thr);
+    return;
+  }
+  // ---- row state
+  const int row = blockIdx.x;
   const int nN = int(g.nN);
   const int im = row / nN, jn = row - im * nN;
   const uint64_t m = g.M[im], n = g.N[jn];
-  const double qm = g.logM[im], qn = g.logN[jn];
-  uint64_t* sD = ws.sD + int64_t(row) * t.CM;
-  int32_t* sP = ws.sP + int64_t(row) * t.CM;
-  // prefix-minimum staircase of D per member class, in member (scan) order
-  for (int ci = 0; ci < t.NC; ++ci) {
-    const int start = t.cls_start[ci], size = t.cls_size[ci];
-    uint64_t carry = ~0ull;
-    int len = 0, lastpos = 0;
-    for (int base = 0; base < size; base += 32) {
-      const int j = base + lane;
-      const uint64_t d = j < size ? umax64(abs_bits(__dsub_rn(t.cls_lm[start + j], qm)),
-                                           abs_bits(__dsub_rn(t.cls_ln[start + j], qn)))
-                                  : ~0ull;
-      uint64_t pm = d;
+  if (tid < 32) {
+    const double qm = g.logM[im], qn = g.logN[jn];
+    uint64_t* sD = ws.sD + int64_t(row) * t.CM;
+    int32_t* sP = ws.sP + int64_t(row) * t.CM;
+    // prefix-minimum staircase of D per member class, in member (scan) order
+    for (int ci = 0; ci < t.NC; ++ci) {
+      const int start = t.cls_start[ci], size = t.cls_size[ci];
+      uint64_t carry = ~0ull;
+      int len = 0, lastpos = 0;
+      for (int b0 = 0; b0 < size; b0 += 32) {
+        const int j = b0 + lane;
+        const uint64_t d = j < size ? umax64(abs_bits(__dsub_rn(t.cls_lm[start + j], qm)),
+                                             abs_bits(__dsub_rn(t.cls_ln[start + j], qn)))
+                                    : ~0ull;
+        uint64_t pm = d;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
-        if (lane >= off && o < pm) pm = o;
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
+          if (lane >= off && o < pm) pm = o;
+        }
+        uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
+        if (lane == 0) excl = ~0ull;
+        if (carry < excl) excl = carry;
+        const bool rec = (j < size) && (d < excl);
+        const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
+        if (rec) {
+          const int pos = start + len + __popc(mask & ((1u << lane) - 1u));
+          sD[pos] = d;
+          sP[pos] = j;
+        }
+        if (mask) lastpos = b0 + 31 - __clz(mask);
+        len += __popc(mask);
+        const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
+        if (tail < carry) carry = tail;
       }
-      uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
-      if (lane == 0) excl = ~0ull;
-      if (carry < excl) excl = carry;
-      const bool rec = (j < size) && (d < excl);
-      const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
-      if (rec) {
-        const int pos = start + len + __popc(mask & ((1u << lane) - 1u));
-        sD[pos] = d;
-        sP[pos] = j;
-      }
-      if (mask) lastpos = base + 31 - __clz(mask);
-      len += __popc(mask);
-      const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
-      if (tail < carry) carry = tail;
+      if (lane == 0) ws.cls[int64_t(row) * t.NC + ci] = ClassRow{carry, lastpos, len};
     }
-    if (lane == 0) ws.cls[int64_t(row) * t.NC + ci] = ClassRow{carry, lastpos, len};
   }
   // tiles per (m, n) and the wave-scale table (GEMM families)
   if (MODE <= 1) {
     const int nb = int(g.b_hi - g.b_lo);
     uint64_t* T = ws.T + int64_t(row) * t.C;
     double* W = ws.W + int64_t(row) * nb * t.C;
-    for (int c = lane; c < t.C; c += 32) {
+    for (int c = tid; c < t.C; c += kPrepThreads) {
       if (!curve_valid(t, c)) continue;
       const uint64_t tmn = ceil_div(m, t.tile_m[c]) * ceil_div(n, t.tile_n[c]) * t.split_k[c];
       T[c] = tmn;
@@ -200,13 +256,14 @@ __device__ __forceinline__ int group_index(const TablesDev& t, const RowView& rv
 // smallest scan index among every member attaining the final best.
 // Returns the ORIGINAL candidate scan index (INT32_MAX when G == 0).
 template <bool G32>
-__device__ __forceinline__ int nearest_sweep(const TablesDev& t, const RowView& rv, double qk,
+__device__ __forceinline__ int nearest_sweep(const TablesDev& t, const RowView& rv,
+                                             const double* __restrict__ glk, double qk,
                                              int start) {
   uint64_t best = ~0ull;
   uint32_t mask = 0;
   int best_i = 0x7FFFFFFF;
   auto visit = [&](int g) -> bool {
-    const uint64_t dk = abs_bits(__dsub_rn(t.grp_lk[g], qk));
+    const uint64_t dk = abs_bits(__dsub_rn(glk[g], qk));
     if (dk > best) return false;
     const uint64_t dg = umax64(dk, rv.cls[t.grp_class[g]].dmin);
     if (G32) {
@@ -242,13 +299,12 @@ __device__ __forceinline__ int nearest_sweep(const TablesDev& t, const RowView& 
 //   best = max(dmin, min(dk_left, dk_right))   (nearest groups to qk)
 //   winner = the leftmost group attaining best, member = staircase(best).
 // Returns (group, member position).
-__device__ __forceinline__ int2 nearest_one_class(const TablesDev& t, const RowView& rv,
-                                                  uint64_t dmin, int lastpos, double qk,
-                                                  int start) {
-  const double* glk = t.grp_lk;
+__device__ __forceinline__ int2 nearest_one_class(int G, const double* __restrict__ glk,
+                                                  const RowView& rv, uint64_t dmin, int lastpos,
+                                                  double qk, int start) {
   auto dk = [&](int g) { return abs_bits(__dsub_rn(glk[g], qk)); };
   const uint64_t dkL = start > 0 ? dk(start - 1) : ~0ull;
-  const uint64_t dkR = start < t.G ? dk(start) : ~0ull;
+  const uint64_t dkR = start < G ? dk(start) : ~0ull;
   const uint64_t mn = dkL < dkR ? dkL : dkR;
   int g, pos;
   if (mn <= dmin) {            // best == dmin: every group with dk <= dmin ties
@@ -277,36 +333,63 @@ template <bool VERIFY, int MODE, int NEAR>
 __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
                                                         const double* __restrict__ base_tab,
                                                         RowWs ws, LaunchOut out) {
+  extern __shared__ __align__(16) uint8_t smem[];
   const int row = blockIdx.x;
   const int nN = int(g.nN), nK = int(g.nK);
   const int ib0 = int(blockIdx.z) * gl.bper;  // slice-relative
   const int ib1 = min(int(g.b_hi - g.b_lo), ib0 + gl.bper);
-  const int nb = ib1 - ib0, nbs_all = int(g.b_hi - g.b_lo);
-  const RowView rv{ws.cls + int64_t(row) * t.NC, ws.sD + int64_t(row) * t.CM,
-                   ws.sP + int64_t(row) * t.CM};
+  const int nb = ib1 - ib0, nb_all = int(g.b_hi - g.b_lo);
+  const int tid = threadIdx.x;
+
+  // stage the row state + candidate tables in shared memory (one barrier)
+  uint64_t* sD = reinterpret_cast<uint64_t*>(smem + gl.off_sD);
+  int32_t* sP = reinterpret_cast<int32_t*>(smem + gl.off_sP);
+  ClassRow* scls = reinterpret_cast<ClassRow*>(smem + gl.off_cls);
+  double* W = reinterpret_cast<double*>(smem + gl.off_W);
+  int32_t* gcur = reinterpret_cast<int32_t*>(smem + gl.off_gcur);
+  int32_t* gst = reinterpret_cast<int32_t*>(smem + gl.off_gst);
+  double* glk = reinterpret_cast<double*>(smem + gl.off_glk);
+  {
+    const uint64_t* rsD = ws.sD + int64_t(row) * t.CM;
+    const int32_t* rsP = ws.sP + int64_t(row) * t.CM;
+    for (int j = tid; j < t.CM; j += blockDim.x) {
+      sD[j] = rsD[j];
+      sP[j] = rsP[j];
+    }
+    for (int j = tid; j < t.NC; j += blockDim.x) scls[j] = ws.cls[int64_t(row) * t.NC + j];
+    if (MODE == 0) {
+      const double* Wrow = ws.W + (int64_t(row) * nb_all + ib0) * t.C;
+      for (int j = tid; j < nb * t.C; j += blockDim.x) W[j] = Wrow[j];
+    }
+    for (int j = tid; j < t.R; j += blockDim.x) gcur[j] = t.g_curve[j];
+    for (int j = tid; j < t.G; j += blockDim.x) {
+      gst[j] = t.grp_start[j];
+      glk[j] = t.grp_lk[j];
+    }
+  }
+  __syncthreads();
+  const RowView rv{scls, sD, sP};
   uint64_t dmin1 = 0;
   int lastpos1 = 0;
   if (NEAR == 2) {
-    const ClassRow cr = rv.cls[0];
-    dmin1 = cr.dmin;
-    lastpos1 = cr.lastpos;
+    dmin1 = scls[0].dmin;
+    lastpos1 = scls[0].lastpos;
   }
   const int64_t plane = g.nM * g.nN * g.nK;
   double* const obase = out.lat + int64_t(ib0) * plane + int64_t(row) * nK;
-  const double* Wrow = MODE == 0 ? ws.W + (int64_t(row) * nbs_all + ib0) * t.C : nullptr;
   const uint64_t* Trow = MODE <= 1 ? ws.T + int64_t(row) * t.C : nullptr;
   const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
   for (int j = 0; j < gl.kpt; ++j) {
-    const int ik = k0 + j * int(blockDim.x) + int(threadIdx.x);
+    const int ik = k0 + j * int(blockDim.x) + tid;
     if (ik >= nK) break;
     const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
     const int start = __double2loint(ki.y);
     int ci;
     if (NEAR == 2) {
-      const int2 gp = nearest_one_class(t, rv, dmin1, lastpos1, ki.x, start);
-      ci = t.g_curve[t.grp_start[gp.x] + gp.y];
+      const int2 gp = nearest_one_class(t.G, glk, rv, dmin1, lastpos1, ki.x, start);
+      ci = gcur[gst[gp.x] + gp.y];
     } else {
-      const int best = nearest_sweep<NEAR == 1>(t, rv, ki.x, start);
+      const int best = nearest_sweep<NEAR == 1>(t, rv, glk, ki.x, start);
       ci = best < t.R ? t.cand_curve[best] : -1;
     }
     double* o = obase + ik;
@@ -328,7 +411,7 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
     }
     const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
     if (MODE == 0 && !VERIFY) {
-      const double* w = Wrow + ci;
+      const double* w = W + ci;
 #pragma unroll 4
       for (int ib = 0; ib < nb; ++ib, o += plane, w += t.C) *o = __dmul_rn(base, *w);
       continue;
@@ -468,7 +551,7 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   };
   gl.kpt = 4;
   gl.ktiles = ktiles_for(gl.kpt);
-  while (gl.kpt > 1 && rows * gl.ktiles < 4 * target) {
+  while (gl.kpt > 1 && rows * gl.ktiles < target) {
     gl.kpt >>= 1;
     gl.ktiles = ktiles_for(gl.kpt);
   }
@@ -485,6 +568,11 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   else if (rows * nb * t.C <= (int64_t(1) << 27)) gl.mode = 0;  // W table <= 1 GiB
   else gl.mode = 1;
   gl.near = (t.NC == 1 && t.lowest_wins) ? 2 : (t.G <= 32 ? 1 : 0);
+  smem_layout(t, gl);
+  if (gl.mode == 0 && gl.smem > 160 * 1024) {  // W slice too large for smem
+    gl.mode = 1;
+    smem_layout(t, gl);
+  }
   return gl;
 }
 
@@ -499,8 +587,12 @@ cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch
                           cudaStream_t s) {
   auto* fn = gl.near == 2 ? grid_kernel<V, M, 2> : gl.near == 1 ? grid_kernel<V, M, 1>
                                                                  : grid_kernel<V, M, 0>;
+  if (gl.smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gl.smem));
+    if (e != cudaSuccess) return e;
+  }
   const dim3 grid(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
-  fn<<<grid, kThreads, 0, s>>>(t, g, gl, base, ws, out);
+  fn<<<grid, kThreads, gl.smem, s>>>(t, g, gl, base, ws, out);
   return cudaGetLastError();
 }
 
@@ -522,18 +614,21 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   if (card == 0) return 0;
   const GridLaunch gl = plan_grid(t, g, false);
   const WsLayout L = ws_layout(t, g, gl);
-  if (!ws || ws_elems < L.total || !grid_dims_ok(g, gl) || t.C > 65535 ||
+  if ((L.total > 0 && (!ws || ws_elems < L.total)) || !grid_dims_ok(g, gl) || gl.smem > 227 * 1024 ||
       int64_t(t.C) * g.nK > 0x7FFFFFFFll)
     return int(cudaErrorInvalidValue);
-  const RowWs rws = row_ws(L, ws);
+  double* wsp = ws ? ws : nullptr;
+  const RowWs rws = row_ws(L, wsp);
   const double* base = t.C > 0 ? ws + L.base : nullptr;
   const int64_t rows = g.nM * g.nN;
   if (stages & kStageBase) {
-    if (t.C > 0) launch_base_table(t, g, ws + L.base, s);
-    const int nb = int((rows * 32 + 255) / 256);
-    if (gl.mode == 0) row_prep_kernel<0><<<nb, 256, 0, s>>>(t, g, rws);
-    else if (gl.mode == 1) row_prep_kernel<1><<<nb, 256, 0, s>>>(t, g, rws);
-    else row_prep_kernel<2><<<nb, 256, 0, s>>>(t, g, rws);
+    const int kchunks = int((g.nK + kPrepThreads - 1) / kPrepThreads);
+    const int64_t nblk = rows + (t.C > 0 ? int64_t(t.C) * kchunks : 0);
+    if (nblk > 0x7FFFFFFFll) return int(cudaErrorInvalidValue);
+    double* bt = t.C > 0 ? wsp + L.base : nullptr;
+    if (gl.mode == 0) prep_kernel<0><<<unsigned(nblk), kPrepThreads, 0, s>>>(t, g, rws, bt, kchunks);
+    else if (gl.mode == 1) prep_kernel<1><<<unsigned(nblk), kPrepThreads, 0, s>>>(t, g, rws, bt, kchunks);
+    else prep_kernel<2><<<unsigned(nblk), kPrepThreads, 0, s>>>(t, g, rws, bt, kchunks);
   }
   const bool v = out.curve != nullptr;
   cudaError_t e = cudaSuccess;
