@@ -36,6 +36,21 @@ __device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) {
   return num / b;
 }
 
+// ceil((a) / d) for the curve's divisor j (0 tile_m, 1 tile_n, 2 blocks per
+// wave) through the host-computed u32 magic when a + d - 1 fits in 32 bits;
+// identical integer result to ceil_div.
+__device__ __forceinline__ uint64_t ceil_div_c(const TablesDev& t, int c, int j, uint64_t a,
+                                               uint64_t d) {
+  const uint64_t num = a + d - 1;
+  const uint32_t s = t.dv_s[3 * c + j];
+  if ((s >> 16) && num <= 0xFFFFFFFFull) {
+    const uint32_t n32 = uint32_t(num);
+    const uint32_t q = __umulhi(t.dv_m[3 * c + j], n32);
+    return uint64_t((q + ((n32 - q) >> (s & 0xFF))) >> ((s >> 8) & 0xFF));
+  }
+  return num / d;
+}
+
 // compute._interpolate_detail / _kernels._interp over samples [lo, hi):
 // clamp outside the sampled range, exact at samples, linear between
 // neighbours: t = (k - k1) / (k3 - k1); thr = t1 + t * (t3 - t1)  (no FMA).
@@ -75,8 +90,8 @@ __device__ __forceinline__ double base_of(const TablesDev& t, int c, uint64_t k)
 __device__ __forceinline__ uint64_t blocks_of(const TablesDev& t, int c, uint64_t b, uint64_t m,
                                               uint64_t n, uint64_t k) {
   const uint64_t tm = t.tile_m[c];
-  if (t.rowblock[c]) return ceil_div(b * k, tm);
-  return b * ceil_div(m, tm) * ceil_div(n, t.tile_n[c]) * t.split_k[c];
+  if (t.rowblock[c]) return ceil_div_c(t, c, 0, b * k, tm);
+  return b * ceil_div_c(t, c, 0, m, tm) * ceil_div_c(t, c, 1, n, t.tile_n[c]) * t.split_k[c];
 }
 
 // waves / ref_waves  (compute.py:137, _kernels.pyx:132)
@@ -96,7 +111,7 @@ __device__ __forceinline__ PointResult predict_point(const TablesDev& t, int c, 
                                                      double base) {
   PointResult r;
   r.blocks = blocks_of(t, c, b, m, n, k);
-  r.waves = ceil_div(r.blocks, t.bpw[c]);
+  r.waves = ceil_div_c(t, c, 2, r.blocks, t.bpw[c]);
   r.lat = __dmul_rn(base, wave_scale(t, c, r.waves));
   return r;
 }

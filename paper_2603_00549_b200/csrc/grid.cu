@@ -216,12 +216,13 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(TablesDev t, GridDev
     double* W = ws.W + int64_t(row) * nb * t.C;
     for (int c = tid; c < t.C; c += kPrepThreads) {
       if (!curve_valid(t, c)) continue;
-      const uint64_t tmn = ceil_div(m, t.tile_m[c]) * ceil_div(n, t.tile_n[c]) * t.split_k[c];
+      const uint64_t tmn = ceil_div_c(t, c, 0, m, t.tile_m[c]) *
+                           ceil_div_c(t, c, 1, n, t.tile_n[c]) * t.split_k[c];
       T[c] = tmn;
-      if (MODE == 0) {
+      if (MODE == 0) {  // curve-major: W[c][ib]
         const uint64_t bpw = t.bpw[c];
         for (int ib = 0; ib < nb; ++ib)
-          W[ib * t.C + c] = wave_scale(t, c, ceil_div(g.B[g.b_lo + ib] * tmn, bpw));
+          W[c * nb + ib] = wave_scale(t, c, ceil_div_c(t, c, 2, g.B[g.b_lo + ib] * tmn, bpw));
       }
     }
   }
@@ -329,7 +330,7 @@ __device__ __forceinline__ int2 nearest_one_class(int G, const double* __restric
   return make_int2(g, pos);
 }
 
-template <bool VERIFY, int MODE, int NEAR>
+template <bool VERIFY, int MODE, int NEAR, int NB>
 __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
                                                         const double* __restrict__ base_tab,
                                                         RowWs ws, LaunchOut out) {
@@ -357,9 +358,12 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
       sP[j] = rsP[j];
     }
     for (int j = tid; j < t.NC; j += blockDim.x) scls[j] = ws.cls[int64_t(row) * t.NC + j];
-    if (MODE == 0) {
-      const double* Wrow = ws.W + (int64_t(row) * nb_all + ib0) * t.C;
-      for (int j = tid; j < nb * t.C; j += blockDim.x) W[j] = Wrow[j];
+    if (MODE == 0) {  // this slab's columns of the row's curve-major W[c][ib]
+      const double* Wrow = ws.W + int64_t(row) * nb_all * t.C;
+      for (int j = tid; j < nb * t.C; j += blockDim.x) {
+        const int c = j / nb, ib = j - c * nb;
+        W[j] = Wrow[c * nb_all + ib0 + ib];
+      }
     }
     for (int j = tid; j < t.R; j += blockDim.x) gcur[j] = t.g_curve[j];
     for (int j = tid; j < t.G; j += blockDim.x) {
@@ -411,9 +415,13 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
     }
     const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
     if (MODE == 0 && !VERIFY) {
-      const double* w = W + ci;
-#pragma unroll 4
-      for (int ib = 0; ib < nb; ++ib, o += plane, w += t.C) *o = __dmul_rn(base, *w);
+      const double* w = W + ci * nb;
+      if (NB > 0) {
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib) o[ib * plane] = __dmul_rn(base, w[ib]);
+      } else {
+        for (int ib = 0; ib < nb; ++ib, o += plane) *o = __dmul_rn(base, w[ib]);
+      }
       continue;
     }
     const uint64_t k = g.K[ik];
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
       uint64_t blocks, waves;
       if (MODE <= 1) {
         blocks = b * Trow[ci];
-        waves = ceil_div(blocks, t.bpw[ci]);
+        waves = ceil_div_c(t, ci, 2, blocks, t.bpw[ci]);
         lat = __dmul_rn(base, wave_scale(t, ci, waves));
       } else {
         const PointResult r = predict_point(t, ci, b, g.M[im], g.N[jn], k, base);
@@ -494,14 +502,15 @@ __global__ void __launch_bounds__(kThreads) all_curves_kernel(TablesDev t, GridD
   const bool table = gl.mode == 0;
   if (table) {
     for (int c = tid; c < t.C; c += blockDim.x)
-      Tmn[c] = curve_valid(t, c)
-                   ? ceil_div(m, t.tile_m[c]) * ceil_div(n, t.tile_n[c]) * t.split_k[c]
-                   : 0;
+      Tmn[c] = curve_valid(t, c) ? ceil_div_c(t, c, 0, m, t.tile_m[c]) *
+                                       ceil_div_c(t, c, 1, n, t.tile_n[c]) * t.split_k[c]
+                                 : 0;
     __syncthreads();
     for (int e = tid; e < nb * t.C; e += blockDim.x) {
       const int ib = e / t.C;
       const int c = e - ib * t.C;
-      if (curve_valid(t, c)) W[e] = wave_scale(t, c, ceil_div(g.B[ib0 + ib] * Tmn[c], t.bpw[c]));
+      if (curve_valid(t, c))
+        W[e] = wave_scale(t, c, ceil_div_c(t, c, 2, g.B[ib0 + ib] * Tmn[c], t.bpw[c]));
     }
     __syncthreads();
   }
@@ -585,8 +594,10 @@ template <bool V, int M>
 cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
                           const double* base, const RowWs& ws, const LaunchOut& out,
                           cudaStream_t s) {
-  auto* fn = gl.near == 2 ? grid_kernel<V, M, 2> : gl.near == 1 ? grid_kernel<V, M, 1>
-                                                                 : grid_kernel<V, M, 0>;
+  const bool nb4 = M == 0 && !V && gl.bper == 4 && (g.b_hi - g.b_lo) % 4 == 0;
+  auto* fn = gl.near == 2 ? (nb4 ? grid_kernel<V, M, 2, 4> : grid_kernel<V, M, 2, 0>)
+             : gl.near == 1 ? grid_kernel<V, M, 1, 0>
+                            : grid_kernel<V, M, 0, 0>;
   if (gl.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gl.smem));
     if (e != cudaSuccess) return e;

@@ -37,6 +37,10 @@ struct TablesDev {
   const uint64_t* tile_n = nullptr;
   const uint64_t* split_k = nullptr;
   const uint64_t* bpw = nullptr;     // blocks per wave (sm_count * blocks_per_sm)
+  // u32 division magic for (tile_m, tile_n, bpw) of each curve [3*C]:
+  // dv_m = multiplier, dv_s = sh1 | sh2 << 8 | valid << 16 (Granlund-Montgomery)
+  const uint32_t* dv_m = nullptr;
+  const uint32_t* dv_s = nullptr;
   const uint8_t* rowblock = nullptr;
   const int32_t* s_off = nullptr;    // [C+1] sample offsets
   const double* s_dims = nullptr;

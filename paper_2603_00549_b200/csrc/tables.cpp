@@ -170,6 +170,22 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
     ex_rec[i] = int32_t(ex[i][5]);
   }
 
+  // u32 division magic (Granlund & Montgomery, PLDI'94, fig. 4.1): for every
+  // 32-bit n, n / d == (t + ((n - t) >> sh1)) >> sh2 with t = umulhi(m, n)
+  std::vector<uint32_t> dv_m(3 * C, 0), dv_s(3 * C, 0);
+  for (int64_t c = 0; c < C; ++c) {
+    const uint64_t divs[3] = {v->tile_m[c], v->tile_n[c], v->blocks_per_wave[c]};
+    for (int j = 0; j < 3; ++j) {
+      const uint64_t d = divs[j];
+      if (d < 1 || d > 0xFFFFFFFFull) continue;  // not valid: generic u64 division
+      int l = 0;
+      while ((uint64_t(1) << l) < d) ++l;
+      const uint64_t m = ((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1;
+      const uint32_t sh1 = l < 1 ? l : 1, sh2 = l > 1 ? l - 1 : 0;
+      dv_m[3 * c + j] = uint32_t(m);
+      dv_s[3 * c + j] = sh1 | (sh2 << 8) | (1u << 16);
+    }
+  }
   std::vector<int32_t> s_off(C + 1);
   for (int64_t c = 0; c <= C; ++c) s_off[c] = int32_t(v->sample_offsets[c]);
   std::vector<uint8_t> rowblock(C);
@@ -196,6 +212,8 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.tile_n = blob.add(v->tile_n, C);
   t.split_k = blob.add(v->split_k, C);
   t.bpw = blob.add(v->blocks_per_wave, C);
+  t.dv_m = blob.add(dv_m);
+  t.dv_s = blob.add(dv_s);
   t.rowblock = blob.add(rowblock);
   t.s_off = blob.add(s_off);
   t.s_dims = blob.add(v->sample_dims, S);
@@ -229,6 +247,7 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.ref_thr = shift(o.ref_thr, base); t.ref_waves = shift(o.ref_waves, base);
   t.tile_m = shift(o.tile_m, base); t.tile_n = shift(o.tile_n, base);
   t.split_k = shift(o.split_k, base); t.bpw = shift(o.bpw, base);
+  t.dv_m = shift(o.dv_m, base); t.dv_s = shift(o.dv_s, base);
   t.rowblock = shift(o.rowblock, base); t.s_off = shift(o.s_off, base);
   t.s_dims = shift(o.s_dims, base); t.s_thrs = shift(o.s_thrs, base);
   t.g_lm = shift(o.g_lm, base); t.g_ln = shift(o.g_ln, base);
