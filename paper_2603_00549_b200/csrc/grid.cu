@@ -4,14 +4,18 @@
 //
 // Per launch (all device-side, CUDA-graph capturable):
 //   base_table_kernel  base(c, k) = ref_dur*(k/ref_dim)*(ref_thr/thr(c,k)) for
-//                      every curve and k value (per-curve samples in smem)
-//   row_prep_kernel    one warp per (m, n) row: D_j = max(|lm_j-qm|, |ln_j-qn|)
-//                      for every class member and its prefix-minimum staircase
-//                      (warp scan + ballot), Tmn[c] = ceil(m/tm)*ceil(n/tn)*sk
-//                      and the wave-scale table W[ib][c] = waves / ref_waves
-//   grid_kernel        one thread per (row, k): nearest config (outward k-group
-//                      sweep over the row's staircases), then one DMUL and one
-//                      coalesced 8-byte store per batch value
+//                      every curve and k value (per-curve samples in smem);
+//                      releases the dependent grid kernel immediately
+//                      (programmatic dependent launch)
+//   grid_kernel        one CTA per ((m, n) row, k tile, batch slab).  Setup
+//                      overlaps the base-table kernel: warp 0 builds the
+//                      member-class staircases of D_j = max(|lm_j-qm|,|ln_j-qn|)
+//                      (warp scan + ballot) while the other warps build
+//                      Tmn[c] = ceil(m/tm)*ceil(n/tn)*sk and the wave-scale
+//                      table W[c][ib] in shared memory; after
+//                      griddepcontrol.wait each thread owns k values: nearest
+//                      config by the outward k-group sweep, then one DMUL and
+//                      one coalesced 8-byte store per batch value
 //   fixup_kernel       exact-record hits (take priority over nearest)
 #include <algorithm>
 
@@ -22,6 +26,9 @@ namespace {
 
 using namespace dev;
 
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // ----------------------------------------------------------- base table
 // base[c][ik] for every curve c and k value; one CTA per (curve, k chunk)
 // with the curve's samples staged in shared memory.
@@ -29,6 +36,7 @@ constexpr int kMaxSmemSamples = 256;
 
 __global__ void __launch_bounds__(256) base_table_kernel(TablesDev t, const uint64_t* __restrict__ K,
                                                          int nK, double* __restrict__ base) {
+  pdl_release();  // the grid kernel may start its (independent) row setup now
   __shared__ double sd[kMaxSmemSamples], sy[kMaxSmemSamples];
   const int c = blockIdx.y;
   const int lo = t.s_off[c], hi = t.s_off[c + 1], ns = hi - lo;
@@ -62,8 +70,14 @@ struct GridLaunch {
   int mode;      // 0: GEMM + W table, 1: GEMM per point, 2: general (row-block)
   int near;      // 0: general sweep, 1: sweep + tie mask (G <= 32), 2: one member class
   // grid_kernel shared-memory layout (byte offsets), computed on the host
-  int off_sD, off_sP, off_cls, off_W, off_gcur, off_gst, off_glk;
+  int off_sD, off_sP, off_cls, off_T, off_W, off_gcur, off_gst, off_glk;
   int64_t smem;
+};
+
+struct ClassRow {
+  uint64_t dmin;    // min over the class members of D (ordered bits)
+  int32_t lastpos;  // member position attaining dmin first
+  int32_t len;      // staircase length
 };
 
 void smem_layout(const TablesDev& t, GridLaunch& gl) {
@@ -76,6 +90,7 @@ void smem_layout(const TablesDev& t, GridLaunch& gl) {
   gl.off_sD = take(8ll * t.CM);
   gl.off_sP = take(4ll * t.CM);
   gl.off_cls = take(16ll * t.NC);
+  gl.off_T = take(gl.mode <= 1 ? 8ll * t.C : 0);
   gl.off_W = take(gl.mode == 0 ? 8ll * t.C * gl.bper : 0);
   gl.off_gcur = take(4ll * t.R);
   gl.off_gst = take(4ll * t.G);
@@ -83,158 +98,14 @@ void smem_layout(const TablesDev& t, GridLaunch& gl) {
   gl.smem = o;
 }
 
-// Per-row state written by row_prep_kernel (workspace, L2-resident).
-struct ClassRow {
-  uint64_t dmin;    // min over the class members of D (ordered bits)
-  int32_t lastpos;  // member position attaining dmin first
-  int32_t len;      // staircase length
-};
-
-struct RowWs {
-  ClassRow* cls;   // [rows][NC]
-  uint64_t* sD;    // [rows][CM] staircase D (class segments at cls_start)
-  int32_t* sP;     // [rows][CM] staircase member positions
-  uint64_t* T;     // [rows][C]  tiles per (m, n)     (modes 0, 1)
-  double* W;       // [rows][nb][C] wave scale         (mode 0)
-};
-
-// Workspace layout (doubles): base table, then the row state.
-struct WsLayout {
-  int64_t base, cls, sD, sP, T, W, total;
-};
-
-WsLayout ws_layout(const TablesDev& t, const GridDev& g, const GridLaunch& gl) {
-  WsLayout L;
-  const int64_t rows = g.nM * g.nN, nb = g.b_hi - g.b_lo;
-  int64_t o = 0;
-  auto take = [&](int64_t doubles) {
-    const int64_t at = o;
-    o += (doubles + 31) & ~int64_t(31);  // 256-byte aligned sections
-    return at;
-  };
-  L.base = take(int64_t(t.C) * g.nK);
-  L.cls = take(rows * t.NC * 2);
-  L.sD = take(rows * t.CM);
-  L.sP = take((rows * t.CM + 1) / 2);
-  L.T = take(gl.mode <= 1 ? rows * t.C : 0);
-  L.W = take(gl.mode == 0 ? rows * nb * t.C : 0);
-  L.total = o;
-  return L;
-}
-
-RowWs row_ws(const WsLayout& L, double* ws) {
-  return RowWs{reinterpret_cast<ClassRow*>(ws + L.cls), reinterpret_cast<uint64_t*>(ws + L.sD),
-               reinterpret_cast<int32_t*>(ws + L.sP), reinterpret_cast<uint64_t*>(ws + L.T),
-               ws + L.W};
-}
-
-// Fused per-launch preparation, 64 threads per CTA:
-//   CTAs [0, rows):         one (m, n) row each — warp 0 builds the member-class
-//                           staircases, all threads build Tmn / W over curves
-//   CTAs [rows, rows + C*kc): base table, one (curve, 64-k chunk) each, with the
-//                           curve's samples staged in shared memory
-constexpr int kPrepThreads = 64;
-
-template <int MODE>
-__global__ void __launch_bounds__(kPrepThreads) prep_kernel(TablesDev t, GridDev g, RowWs ws,
-                                                            double* __restrict__ base, int kchunks) {
-  const int rows = int(g.nM * g.nN);
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (int(blockIdx.x) >= rows) {
-    // ---- base table: base[c][ik]
-    __shared__ double sd[kMaxSmemSamples], sy[kMaxSmemSamples];
-    const int e = int(blockIdx.x) - rows;
-    const int c = e / kchunks, chunk = e - c * kchunks;
-    const int nK = int(g.nK);
-    const int ik = chunk * kPrepThreads + tid;
-    const int lo = t.s_off[c], hi = t.s_off[c + 1], ns = hi - lo;
-    if (ns <= 0) {
-      if (ik < nK) base[int64_t(c) * nK + ik] = 0.0;
-      return;
-    }
-    const bool staged = ns <= kMaxSmemSamples;
-    if (staged)
-      for (int j = tid; j < ns; j += kPrepThreads) {
-        sd[j] = t.s_dims[lo + j];
-        sy[j] = t.s_thrs[lo + j];
-      }
-    __syncthreads();
-    if (ik >= nK) return;
-    const double nd = __ull2double_rn(g.K[ik]);
-    const double thr = staged ? interp_samples(sd, sy, 0, ns, nd)
-                              : interp_samples(t.s_dims, t.s_thrs, lo, hi, nd);
-    base[int64_t(c) * nK + ik] = base_from_thr(t, c, nd, thr);
-    return;
-  }
-  // ---- row state
-  const int row = blockIdx.x;
-  const int nN = int(g.nN);
-  const int im = row / nN, jn = row - im * nN;
-  const uint64_t m = g.M[im], n = g.N[jn];
-  if (tid < 32) {
-    const double qm = g.logM[im], qn = g.logN[jn];
-    uint64_t* sD = ws.sD + int64_t(row) * t.CM;
-    int32_t* sP = ws.sP + int64_t(row) * t.CM;
-    // prefix-minimum staircase of D per member class, in member (scan) order
-    for (int ci = 0; ci < t.NC; ++ci) {
-      const int start = t.cls_start[ci], size = t.cls_size[ci];
-      uint64_t carry = ~0ull;
-      int len = 0, lastpos = 0;
-      for (int b0 = 0; b0 < size; b0 += 32) {
-        const int j = b0 + lane;
-        const uint64_t d = j < size ? umax64(abs_bits(__dsub_rn(t.cls_lm[start + j], qm)),
-                                             abs_bits(__dsub_rn(t.cls_ln[start + j], qn)))
-                                    : ~0ull;
-        uint64_t pm = d;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
-          if (lane >= off && o < pm) pm = o;
-        }
-        uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
-        if (lane == 0) excl = ~0ull;
-        if (carry < excl) excl = carry;
-        const bool rec = (j < size) && (d < excl);
-        const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
-        if (rec) {
-          const int pos = start + len + __popc(mask & ((1u << lane) - 1u));
-          sD[pos] = d;
-          sP[pos] = j;
-        }
-        if (mask) lastpos = b0 + 31 - __clz(mask);
-        len += __popc(mask);
-        const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
-        if (tail < carry) carry = tail;
-      }
-      if (lane == 0) ws.cls[int64_t(row) * t.NC + ci] = ClassRow{carry, lastpos, len};
-    }
-  }
-  // tiles per (m, n) and the wave-scale table (GEMM families)
-  if (MODE <= 1) {
-    const int nb = int(g.b_hi - g.b_lo);
-    uint64_t* T = ws.T + int64_t(row) * t.C;
-    double* W = ws.W + int64_t(row) * nb * t.C;
-    for (int c = tid; c < t.C; c += kPrepThreads) {
-      if (!curve_valid(t, c)) continue;
-      const uint64_t tmn = ceil_div_c(t, c, 0, m, t.tile_m[c]) *
-                           ceil_div_c(t, c, 1, n, t.tile_n[c]) * t.split_k[c];
-      T[c] = tmn;
-      if (MODE == 0) {  // curve-major: W[c][ib]
-        const uint64_t bpw = t.bpw[c];
-        for (int ib = 0; ib < nb; ++ib)
-          W[c * nb + ib] = wave_scale(t, c, ceil_div_c(t, c, 2, g.B[g.b_lo + ib] * tmn, bpw));
-      }
-    }
-  }
-}
-
-// Scan index of the first member of group g whose distance equals `best`
-// (the group attains best): the first staircase entry with D <= best.
 struct RowView {
   const ClassRow* cls;
   const uint64_t* sD;
   const int32_t* sP;
 };
+
+// Scan index of the first member of group g whose distance equals `best`
+// (the group attains best): the first staircase entry with D <= best.
 
 __device__ __forceinline__ int group_index(const TablesDev& t, const RowView& rv, int g,
                                            uint64_t best) {
@@ -333,40 +204,81 @@ __device__ __forceinline__ int2 nearest_one_class(int G, const double* __restric
 template <bool VERIFY, int MODE, int NEAR, int NB>
 __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
                                                         const double* __restrict__ base_tab,
-                                                        RowWs ws, LaunchOut out) {
+                                                        LaunchOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int row = blockIdx.x;
-  const int nN = int(g.nN), nK = int(g.nK);
-  const int ib0 = int(blockIdx.z) * gl.bper;  // slice-relative
-  const int ib1 = min(int(g.b_hi - g.b_lo), ib0 + gl.bper);
-  const int nb = ib1 - ib0, nb_all = int(g.b_hi - g.b_lo);
-  const int tid = threadIdx.x;
-
-  // stage the row state + candidate tables in shared memory (one barrier)
   uint64_t* sD = reinterpret_cast<uint64_t*>(smem + gl.off_sD);
   int32_t* sP = reinterpret_cast<int32_t*>(smem + gl.off_sP);
   ClassRow* scls = reinterpret_cast<ClassRow*>(smem + gl.off_cls);
+  uint64_t* T = reinterpret_cast<uint64_t*>(smem + gl.off_T);
   double* W = reinterpret_cast<double*>(smem + gl.off_W);
   int32_t* gcur = reinterpret_cast<int32_t*>(smem + gl.off_gcur);
   int32_t* gst = reinterpret_cast<int32_t*>(smem + gl.off_gst);
   double* glk = reinterpret_cast<double*>(smem + gl.off_glk);
-  {
-    const uint64_t* rsD = ws.sD + int64_t(row) * t.CM;
-    const int32_t* rsP = ws.sP + int64_t(row) * t.CM;
-    for (int j = tid; j < t.CM; j += blockDim.x) {
-      sD[j] = rsD[j];
-      sP[j] = rsP[j];
+
+  const int row = blockIdx.x;
+  const int nN = int(g.nN), nK = int(g.nK);
+  const int im = row / nN, jn = row - im * nN;
+  const int ib0 = int(blockIdx.z) * gl.bper;  // slice-relative
+  const int nb = min(int(g.b_hi - g.b_lo), ib0 + gl.bper) - ib0;
+  const int tid = threadIdx.x;
+  const uint64_t m = g.M[im], n = g.N[jn];
+
+  // ---- row setup (independent of the base table: overlaps its kernel)
+  if (tid < 32) {
+    // member-class staircases: prefix minimum of D in member (scan) order
+    const int lane = tid;
+    const double qm = g.logM[im], qn = g.logN[jn];
+    for (int ci = 0; ci < t.NC; ++ci) {
+      const int start = t.cls_start[ci], size = t.cls_size[ci];
+      uint64_t carry = ~0ull;
+      int len = 0, lastpos = 0;
+      for (int b0 = 0; b0 < size; b0 += 32) {
+        const int j = b0 + lane;
+        const uint64_t d = j < size ? umax64(abs_bits(__dsub_rn(t.cls_lm[start + j], qm)),
+                                             abs_bits(__dsub_rn(t.cls_ln[start + j], qn)))
+                                    : ~0ull;
+        uint64_t pm = d;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
+          if (lane >= off && o < pm) pm = o;
+        }
+        uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
+        if (lane == 0) excl = ~0ull;
+        if (carry < excl) excl = carry;
+        const bool rec = (j < size) && (d < excl);
+        const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
+        if (rec) {
+          const int pos = start + len + __popc(mask & ((1u << lane) - 1u));
+          sD[pos] = d;
+          sP[pos] = j;
+        }
+        if (mask) lastpos = b0 + 31 - __clz(mask);
+        len += __popc(mask);
+        const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
+        if (tail < carry) carry = tail;
+      }
+      if (lane == 0) scls[ci] = ClassRow{carry, lastpos, len};
     }
-    for (int j = tid; j < t.NC; j += blockDim.x) scls[j] = ws.cls[int64_t(row) * t.NC + j];
-    if (MODE == 0) {  // this slab's columns of the row's curve-major W[c][ib]
-      const double* Wrow = ws.W + int64_t(row) * nb_all * t.C;
-      for (int j = tid; j < nb * t.C; j += blockDim.x) {
-        const int c = j / nb, ib = j - c * nb;
-        W[j] = Wrow[c * nb_all + ib0 + ib];
+  } else {
+    // tiles per (m, n) and the curve-major wave-scale table W[c][ib]
+    const int nth = blockDim.x - 32, me = tid - 32;
+    if (MODE <= 1) {
+      for (int c = me; c < t.C; c += nth) {
+        if (!curve_valid(t, c)) continue;
+        const uint64_t tmn = ceil_div_c(t, c, 0, m, t.tile_m[c]) *
+                             ceil_div_c(t, c, 1, n, t.tile_n[c]) * t.split_k[c];
+        T[c] = tmn;
+        if (MODE == 0) {
+          const uint64_t bpw = t.bpw[c];
+          for (int ib = 0; ib < nb; ++ib)
+            W[c * nb + ib] =
+                wave_scale(t, c, ceil_div_c(t, c, 2, g.B[g.b_lo + ib0 + ib] * tmn, bpw));
+        }
       }
     }
-    for (int j = tid; j < t.R; j += blockDim.x) gcur[j] = t.g_curve[j];
-    for (int j = tid; j < t.G; j += blockDim.x) {
+    for (int j = me; j < t.R; j += nth) gcur[j] = t.g_curve[j];
+    for (int j = me; j < t.G; j += nth) {
       gst[j] = t.grp_start[j];
       glk[j] = t.grp_lk[j];
     }
@@ -379,9 +291,11 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
     dmin1 = scls[0].dmin;
     lastpos1 = scls[0].lastpos;
   }
+  pdl_wait();  // base table complete and visible
+
+  // ---- points: thread owns kpt k values (stride blockDim); every batch value
   const int64_t plane = g.nM * g.nN * g.nK;
   double* const obase = out.lat + int64_t(ib0) * plane + int64_t(row) * nK;
-  const uint64_t* Trow = MODE <= 1 ? ws.T + int64_t(row) * t.C : nullptr;
   const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
   for (int j = 0; j < gl.kpt; ++j) {
     const int ik = k0 + j * int(blockDim.x) + tid;
@@ -425,17 +339,16 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
       continue;
     }
     const uint64_t k = g.K[ik];
-    const int im = row / nN, jn = row - im * nN;
     for (int ib = 0; ib < nb; ++ib, o += plane) {
       const uint64_t b = g.B[g.b_lo + ib0 + ib];
       double lat;
       uint64_t blocks, waves;
       if (MODE <= 1) {
-        blocks = b * Trow[ci];
+        blocks = b * T[ci];
         waves = ceil_div_c(t, ci, 2, blocks, t.bpw[ci]);
         lat = __dmul_rn(base, wave_scale(t, ci, waves));
       } else {
-        const PointResult r = predict_point(t, ci, b, g.M[im], g.N[jn], k, base);
+        const PointResult r = predict_point(t, ci, b, m, n, k, base);
         lat = r.lat;
         blocks = r.blocks;
         waves = r.waves;
@@ -573,9 +486,7 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
     gl.mode = (t.all_gemm && 8ll * t.C * (gl.bper + 1) <= 96 * 1024) ? 0 : 2;
     return gl;
   }
-  if (!t.all_gemm) gl.mode = 2;
-  else if (rows * nb * t.C <= (int64_t(1) << 27)) gl.mode = 0;  // W table <= 1 GiB
-  else gl.mode = 1;
+  gl.mode = t.all_gemm ? 0 : 2;
   gl.near = (t.NC == 1 && t.lowest_wins) ? 2 : (t.G <= 32 ? 1 : 0);
   smem_layout(t, gl);
   if (gl.mode == 0 && gl.smem > 160 * 1024) {  // W slice too large for smem
@@ -592,8 +503,7 @@ bool grid_dims_ok(const GridDev& g, const GridLaunch& gl) {
 
 template <bool V, int M>
 cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
-                          const double* base, const RowWs& ws, const LaunchOut& out,
-                          cudaStream_t s) {
+                          const double* base, const LaunchOut& out, cudaStream_t s) {
   const bool nb4 = M == 0 && !V && gl.bper == 4 && (g.b_hi - g.b_lo) % 4 == 0;
   auto* fn = gl.near == 2 ? (nb4 ? grid_kernel<V, M, 2, 4> : grid_kernel<V, M, 2, 0>)
              : gl.near == 1 ? grid_kernel<V, M, 1, 0>
@@ -602,9 +512,19 @@ cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gl.smem));
     if (e != cudaSuccess) return e;
   }
-  const dim3 grid(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
-  fn<<<grid, kThreads, gl.smem, s>>>(t, g, gl, base, ws, out);
-  return cudaGetLastError();
+  // programmatic dependent launch: the row setup overlaps the base-table
+  // kernel; griddepcontrol.wait guards the first base-table read
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = size_t(gl.smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, t, g, gl, base, out);
 }
 
 void launch_base_table(const TablesDev& t, const GridDev& g, double* ws, cudaStream_t s) {
@@ -615,7 +535,7 @@ void launch_base_table(const TablesDev& t, const GridDev& g, double* ws, cudaStr
 }  // namespace
 
 int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g) {
-  return ws_layout(t, g, plan_grid(t, g, false)).total;
+  return int64_t(t.C) * g.nK;
 }
 
 int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, double* ws,
@@ -624,34 +544,23 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
   if (card == 0) return 0;
   const GridLaunch gl = plan_grid(t, g, false);
-  const WsLayout L = ws_layout(t, g, gl);
-  if ((L.total > 0 && (!ws || ws_elems < L.total)) || !grid_dims_ok(g, gl) || gl.smem > 227 * 1024 ||
-      int64_t(t.C) * g.nK > 0x7FFFFFFFll)
+  const int64_t need = int64_t(t.C) * g.nK;
+  if ((need > 0 && (!ws || ws_elems < need)) || !grid_dims_ok(g, gl) || gl.smem > 227 * 1024 ||
+      t.C > 65535 || need > 0x7FFFFFFFll)
     return int(cudaErrorInvalidValue);
-  double* wsp = ws ? ws : nullptr;
-  const RowWs rws = row_ws(L, wsp);
-  const double* base = t.C > 0 ? ws + L.base : nullptr;
-  const int64_t rows = g.nM * g.nN;
-  if (stages & kStageBase) {
-    const int kchunks = int((g.nK + kPrepThreads - 1) / kPrepThreads);
-    const int64_t nblk = rows + (t.C > 0 ? int64_t(t.C) * kchunks : 0);
-    if (nblk > 0x7FFFFFFFll) return int(cudaErrorInvalidValue);
-    double* bt = t.C > 0 ? wsp + L.base : nullptr;
-    if (gl.mode == 0) prep_kernel<0><<<unsigned(nblk), kPrepThreads, 0, s>>>(t, g, rws, bt, kchunks);
-    else if (gl.mode == 1) prep_kernel<1><<<unsigned(nblk), kPrepThreads, 0, s>>>(t, g, rws, bt, kchunks);
-    else prep_kernel<2><<<unsigned(nblk), kPrepThreads, 0, s>>>(t, g, rws, bt, kchunks);
-  }
+  const double* base = t.C > 0 ? ws : nullptr;
+  if ((stages & kStageBase) && t.C > 0) launch_base_table(t, g, ws, s);
   const bool v = out.curve != nullptr;
   cudaError_t e = cudaSuccess;
   if (stages & kStageGrid) {
     if (v) {
-      e = gl.mode == 0 ? launch_grid_t<true, 0>(t, g, gl, base, rws, out, s)
-          : gl.mode == 1 ? launch_grid_t<true, 1>(t, g, gl, base, rws, out, s)
-                         : launch_grid_t<true, 2>(t, g, gl, base, rws, out, s);
+      e = gl.mode == 0 ? launch_grid_t<true, 0>(t, g, gl, base, out, s)
+          : gl.mode == 1 ? launch_grid_t<true, 1>(t, g, gl, base, out, s)
+                         : launch_grid_t<true, 2>(t, g, gl, base, out, s);
     } else {
-      e = gl.mode == 0 ? launch_grid_t<false, 0>(t, g, gl, base, rws, out, s)
-          : gl.mode == 1 ? launch_grid_t<false, 1>(t, g, gl, base, rws, out, s)
-                         : launch_grid_t<false, 2>(t, g, gl, base, rws, out, s);
+      e = gl.mode == 0 ? launch_grid_t<false, 0>(t, g, gl, base, out, s)
+          : gl.mode == 1 ? launch_grid_t<false, 1>(t, g, gl, base, out, s)
+                         : launch_grid_t<false, 2>(t, g, gl, base, out, s);
     }
   }
   if (e != cudaSuccess) return int(e);
