@@ -201,8 +201,10 @@ __device__ __forceinline__ int2 nearest_one_class(int G, const double* __restric
   return make_int2(g, pos);
 }
 
+constexpr int kGridThreads = 128;
+
 template <bool VERIFY, int MODE, int NEAR, int NB>
-__global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
+__global__ void __launch_bounds__(kGridThreads, 10) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
                                                         const double* __restrict__ base_tab,
                                                         LaunchOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -277,7 +279,6 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
         }
       }
     }
-    for (int j = me; j < t.R; j += nth) gcur[j] = t.g_curve[j];
     for (int j = me; j < t.G; j += nth) {
       gst[j] = t.grp_start[j];
       glk[j] = t.grp_lk[j];
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(TablesDev t, GridDev g, 
     int ci;
     if (NEAR == 2) {
       const int2 gp = nearest_one_class(t.G, glk, rv, dmin1, lastpos1, ki.x, start);
-      ci = gcur[gst[gp.x] + gp.y];
+      ci = t.g_curve[gst[gp.x] + gp.y];
     } else {
       const int best = nearest_sweep<NEAR == 1>(t, rv, glk, ki.x, start);
       ci = best < t.R ? t.cand_curve[best] : -1;
@@ -468,10 +469,11 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   const int64_t rows = g.nM * g.nN;
   const int64_t nb = g.b_hi - g.b_lo;
   const int64_t target = 148 * 8;
+  const int threads = all_curves ? kThreads : kGridThreads;
   auto ktiles_for = [&](int kpt) {
-    return int((g.nK + int64_t(kpt) * kThreads - 1) / (int64_t(kpt) * kThreads));
+    return int((g.nK + int64_t(kpt) * threads - 1) / (int64_t(kpt) * threads));
   };
-  gl.kpt = 4;
+  gl.kpt = all_curves ? 4 : 8;
   gl.ktiles = ktiles_for(gl.kpt);
   while (gl.kpt > 1 && rows * gl.ktiles < target) {
     gl.kpt >>= 1;
@@ -516,7 +518,7 @@ cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch
   // kernel; griddepcontrol.wait guards the first base-table read
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kGridThreads);
   cfg.dynamicSmemBytes = size_t(gl.smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
