@@ -204,7 +204,7 @@ __device__ __forceinline__ int2 nearest_one_class(int G, const double* __restric
 constexpr int kGridThreads = 128;
 
 template <bool VERIFY, int MODE, int NEAR, int NB>
-__global__ void __launch_bounds__(kGridThreads, 10) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
+__global__ void __launch_bounds__(kGridThreads, 8) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
                                                         const double* __restrict__ base_tab,
                                                         LaunchOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(kGridThreads, 10) grid_kernel(TablesDev t, Gri
         }
       }
     }
+    for (int j = me; j < t.R; j += nth) gcur[j] = t.g_curve[j];
     for (int j = me; j < t.G; j += nth) {
       gst[j] = t.grp_start[j];
       glk[j] = t.grp_lk[j];
@@ -298,6 +299,56 @@ __global__ void __launch_bounds__(kGridThreads, 10) grid_kernel(TablesDev t, Gri
   const int64_t plane = g.nM * g.nN * g.nK;
   double* const obase = out.lat + int64_t(ib0) * plane + int64_t(row) * nK;
   const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
+  if (NEAR == 2 && MODE == 0 && !VERIFY && NB > 0) {
+    // hot path, software-pipelined in groups of U k values: all kinfo loads,
+    // then all nearest searches, then all base-table loads in flight
+    // together, then the stores (memory-level parallelism for a kernel whose
+    // per-point chain is kinfo -> curve -> base -> store)
+    constexpr int U = 4;
+    const int step = int(blockDim.x);
+    for (int j0 = 0; j0 < gl.kpt; j0 += U) {
+      double2 ki[U];
+      int ik[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ik[u] = k0 + (j0 + u) * step + tid;
+        ki[u] = ik[u] < nK ? *reinterpret_cast<const double2*>(&g.kinfo[ik[u]])
+                           : make_double2(0.0, 0.0);
+      }
+      int ci[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ik[u] < nK && j0 + u < gl.kpt) {
+          const int2 gp = nearest_one_class(t.G, glk, rv, dmin1, lastpos1, ki[u].x,
+                                            __double2loint(ki[u].y));
+          ci[u] = gcur[gst[gp.x] + gp.y];
+        } else {
+          ci[u] = -2;  // out of range
+        }
+      }
+      double bv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) bv[u] = ci[u] >= 0 ? base_tab[ci[u] * nK + ik[u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ci[u] == -2) continue;
+        double* o = obase + ik[u];
+        if (ci[u] < 0) {
+          if (out.nan_stats) {
+            atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
+            atomicAdd(out.nan_stats + 1, (unsigned long long)NB);
+          }
+#pragma unroll
+          for (int ib = 0; ib < NB; ++ib) o[ib * plane] = qnan();
+          continue;
+        }
+        const double* w = W + ci[u] * NB;
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib) o[ib * plane] = __dmul_rn(bv[u], w[ib]);
+      }
+    }
+    return;
+  }
   for (int j = 0; j < gl.kpt; ++j) {
     const int ik = k0 + j * int(blockDim.x) + tid;
     if (ik >= nK) break;
@@ -306,7 +357,7 @@ __global__ void __launch_bounds__(kGridThreads, 10) grid_kernel(TablesDev t, Gri
     int ci;
     if (NEAR == 2) {
       const int2 gp = nearest_one_class(t.G, glk, rv, dmin1, lastpos1, ki.x, start);
-      ci = t.g_curve[gst[gp.x] + gp.y];
+      ci = gcur[gst[gp.x] + gp.y];
     } else {
       const int best = nearest_sweep<NEAR == 1>(t, rv, glk, ki.x, start);
       ci = best < t.R ? t.cand_curve[best] : -1;
