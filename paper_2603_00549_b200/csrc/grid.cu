@@ -62,15 +62,27 @@ __global__ void __launch_bounds__(256) base_table_kernel(TablesDev t, const uint
 }
 
 // ------------------------------------------------------------ grid kernel
+// Warp-specialised, persistent: each CTA has kProducerWarps producer warps
+// and kConsumerWarps consumer warps and walks (row, batch-slab) tiles with a
+// stride of gridDim.x.  Producers build the next tile's row state into one of
+// two shared-memory buffers while consumers compute the current tile's points
+// from the other; the hand-off uses named barriers (FULL/EMPTY per buffer).
+constexpr int kProducerWarps = 2;   // warp 0: staircases, warp 1: Tmn / W
+constexpr int kConsumerWarps = 4;
+constexpr int kConsumers = 32 * kConsumerWarps;
+constexpr int kWsThreads = 32 * (kProducerWarps + kConsumerWarps);
+
 struct GridLaunch {
-  int kpt;       // k values per thread
-  int ktiles;    // k tiles per row  (gridDim.y)
-  int nbs;       // batch slabs      (gridDim.z)
+  int tiles;     // rows * nbs
+  int kpt;       // k values per consumer thread
+  int nbs;       // batch slabs
   int bper;      // batch values per slab
   int mode;      // 0: GEMM + W table, 1: GEMM per point, 2: general (row-block)
   int near;      // 0: general sweep, 1: sweep + tie mask (G <= 32), 2: one member class
-  // grid_kernel shared-memory layout (byte offsets), computed on the host
-  int off_sD, off_sP, off_cls, off_T, off_W, off_gcur, off_gst, off_glk;
+  int ctas;      // persistent CTAs
+  // shared memory: constant part, then two row-state buffers
+  int off_gcur, off_gst, off_glk, off_buf, buf_bytes;
+  int b_sD, b_sP, b_cls, b_T, b_W;  // offsets inside a buffer
   int64_t smem;
 };
 
@@ -87,16 +99,33 @@ void smem_layout(const TablesDev& t, GridLaunch& gl) {
     o = (o + bytes + 15) & ~int64_t(15);
     return int(at);
   };
-  gl.off_sD = take(8ll * t.CM);
-  gl.off_sP = take(4ll * t.CM);
-  gl.off_cls = take(16ll * t.NC);
-  gl.off_T = take(gl.mode <= 1 ? 8ll * t.C : 0);
-  gl.off_W = take(gl.mode == 0 ? 8ll * t.C * gl.bper : 0);
   gl.off_gcur = take(4ll * t.R);
   gl.off_gst = take(4ll * t.G);
   gl.off_glk = take(8ll * t.G);
-  gl.smem = o;
+  gl.off_buf = int(o);
+  int64_t bo = 0;
+  auto btake = [&](int64_t bytes) {
+    const int64_t at = bo;
+    bo = (bo + bytes + 15) & ~int64_t(15);
+    return int(at);
+  };
+  gl.b_sD = btake(8ll * t.CM);
+  gl.b_sP = btake(4ll * t.CM);
+  gl.b_cls = btake(16ll * t.NC);
+  gl.b_T = btake(gl.mode <= 1 ? 8ll * t.C : 0);
+  gl.b_W = btake(gl.mode == 0 ? 8ll * t.C * gl.bper : 0);
+  gl.buf_bytes = int(bo);
+  gl.smem = o + 2 * bo;
 }
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+constexpr int kBarFull = 1;   // ids 1, 2
+constexpr int kBarEmpty = 3;  // ids 3, 4
 
 struct RowView {
   const ClassRow* cls;
@@ -201,34 +230,17 @@ __device__ __forceinline__ int2 nearest_one_class(int G, const double* __restric
   return make_int2(g, pos);
 }
 
-constexpr int kGridThreads = 128;
-
-template <bool VERIFY, int MODE, int NEAR, int NB>
-__global__ void __launch_bounds__(kGridThreads, 8) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
-                                                        const double* __restrict__ base_tab,
-                                                        LaunchOut out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* sD = reinterpret_cast<uint64_t*>(smem + gl.off_sD);
-  int32_t* sP = reinterpret_cast<int32_t*>(smem + gl.off_sP);
-  ClassRow* scls = reinterpret_cast<ClassRow*>(smem + gl.off_cls);
-  uint64_t* T = reinterpret_cast<uint64_t*>(smem + gl.off_T);
-  double* W = reinterpret_cast<double*>(smem + gl.off_W);
-  int32_t* gcur = reinterpret_cast<int32_t*>(smem + gl.off_gcur);
-  int32_t* gst = reinterpret_cast<int32_t*>(smem + gl.off_gst);
-  double* glk = reinterpret_cast<double*>(smem + gl.off_glk);
-
-  const int row = blockIdx.x;
-  const int nN = int(g.nN), nK = int(g.nK);
+// Row state of one (row, slab) tile, produced into buffer `buf`.
+__device__ __forceinline__ void produce_tile(const TablesDev& t, const GridDev& g,
+                                             const GridLaunch& gl, int warp, int lane, int row,
+                                             int slab, uint8_t* buf) {
+  uint64_t* sD = reinterpret_cast<uint64_t*>(buf + gl.b_sD);
+  int32_t* sP = reinterpret_cast<int32_t*>(buf + gl.b_sP);
+  ClassRow* scls = reinterpret_cast<ClassRow*>(buf + gl.b_cls);
+  const int nN = int(g.nN);
   const int im = row / nN, jn = row - im * nN;
-  const int ib0 = int(blockIdx.z) * gl.bper;  // slice-relative
-  const int nb = min(int(g.b_hi - g.b_lo), ib0 + gl.bper) - ib0;
-  const int tid = threadIdx.x;
-  const uint64_t m = g.M[im], n = g.N[jn];
-
-  // ---- row setup (independent of the base table: overlaps its kernel)
-  if (tid < 32) {
+  if (warp == 0) {
     // member-class staircases: prefix minimum of D in member (scan) order
-    const int lane = tid;
     const double qm = g.logM[im], qn = g.logN[jn];
     for (int ci = 0; ci < t.NC; ++ci) {
       const int start = t.cls_start[ci], size = t.cls_size[ci];
@@ -262,68 +274,74 @@ __global__ void __launch_bounds__(kGridThreads, 8) grid_kernel(TablesDev t, Grid
       }
       if (lane == 0) scls[ci] = ClassRow{carry, lastpos, len};
     }
-  } else {
+  } else if (gl.mode <= 1) {
     // tiles per (m, n) and the curve-major wave-scale table W[c][ib]
-    const int nth = blockDim.x - 32, me = tid - 32;
-    if (MODE <= 1) {
-      for (int c = me; c < t.C; c += nth) {
-        if (!curve_valid(t, c)) continue;
-        const uint64_t tmn = ceil_div_c(t, c, 0, m, t.tile_m[c]) *
-                             ceil_div_c(t, c, 1, n, t.tile_n[c]) * t.split_k[c];
-        T[c] = tmn;
-        if (MODE == 0) {
-          const uint64_t bpw = t.bpw[c];
-          for (int ib = 0; ib < nb; ++ib)
-            W[c * nb + ib] =
-                wave_scale(t, c, ceil_div_c(t, c, 2, g.B[g.b_lo + ib0 + ib] * tmn, bpw));
-        }
+    uint64_t* T = reinterpret_cast<uint64_t*>(buf + gl.b_T);
+    double* W = reinterpret_cast<double*>(buf + gl.b_W);
+    const uint64_t m = g.M[im], n = g.N[jn];
+    const int ib0 = slab * gl.bper;
+    const int nb = min(int(g.b_hi - g.b_lo), ib0 + gl.bper) - ib0;
+    for (int c = lane + 32 * (warp - 1); c < t.C; c += 32 * (kProducerWarps - 1)) {
+      if (!curve_valid(t, c)) continue;
+      const uint64_t tmn = ceil_div_c(t, c, 0, m, t.tile_m[c]) *
+                           ceil_div_c(t, c, 1, n, t.tile_n[c]) * t.split_k[c];
+      T[c] = tmn;
+      if (gl.mode == 0) {
+        const uint64_t bpw = t.bpw[c];
+        for (int ib = 0; ib < nb; ++ib)
+          W[c * nb + ib] =
+              wave_scale(t, c, ceil_div_c(t, c, 2, g.B[g.b_lo + ib0 + ib] * tmn, bpw));
       }
     }
-    for (int j = me; j < t.R; j += nth) gcur[j] = t.g_curve[j];
-    for (int j = me; j < t.G; j += nth) {
-      gst[j] = t.grp_start[j];
-      glk[j] = t.grp_lk[j];
-    }
   }
-  __syncthreads();
+}
+
+template <bool VERIFY, int MODE, int NEAR, int NB>
+__device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& g,
+                                             const GridLaunch& gl, const double* base_tab,
+                                             const LaunchOut& out, int ctid, int row, int slab,
+                                             const uint8_t* buf, const int32_t* gcur,
+                                             const int32_t* gst, const double* glk) {
+  const uint64_t* sD = reinterpret_cast<const uint64_t*>(buf + gl.b_sD);
+  const int32_t* sP = reinterpret_cast<const int32_t*>(buf + gl.b_sP);
+  const ClassRow* scls = reinterpret_cast<const ClassRow*>(buf + gl.b_cls);
+  const uint64_t* T = reinterpret_cast<const uint64_t*>(buf + gl.b_T);
+  const double* W = reinterpret_cast<const double*>(buf + gl.b_W);
   const RowView rv{scls, sD, sP};
+  const int nN = int(g.nN), nK = int(g.nK);
+  const int ib0 = slab * gl.bper;
+  const int nb = min(int(g.b_hi - g.b_lo), ib0 + gl.bper) - ib0;
   uint64_t dmin1 = 0;
   int lastpos1 = 0;
   if (NEAR == 2) {
     dmin1 = scls[0].dmin;
     lastpos1 = scls[0].lastpos;
   }
-  pdl_wait();  // base table complete and visible
-
-  // ---- points: thread owns kpt k values (stride blockDim); every batch value
   const int64_t plane = g.nM * g.nN * g.nK;
   double* const obase = out.lat + int64_t(ib0) * plane + int64_t(row) * nK;
-  const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
   if (NEAR == 2 && MODE == 0 && !VERIFY && NB > 0) {
     // hot path, software-pipelined in groups of U k values: all kinfo loads,
     // then all nearest searches, then all base-table loads in flight
-    // together, then the stores (memory-level parallelism for a kernel whose
-    // per-point chain is kinfo -> curve -> base -> store)
+    // together, then the stores
     constexpr int U = 4;
-    const int step = int(blockDim.x);
-    for (int j0 = 0; j0 < gl.kpt; j0 += U) {
+    for (int k0 = 0; k0 < nK; k0 += U * kConsumers) {
       double2 ki[U];
       int ik[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        ik[u] = k0 + (j0 + u) * step + tid;
+        ik[u] = k0 + u * kConsumers + ctid;
         ki[u] = ik[u] < nK ? *reinterpret_cast<const double2*>(&g.kinfo[ik[u]])
                            : make_double2(0.0, 0.0);
       }
       int ci[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (ik[u] < nK && j0 + u < gl.kpt) {
+        if (ik[u] < nK) {
           const int2 gp = nearest_one_class(t.G, glk, rv, dmin1, lastpos1, ki[u].x,
                                             __double2loint(ki[u].y));
           ci[u] = gcur[gst[gp.x] + gp.y];
         } else {
-          ci[u] = -2;  // out of range
+          ci[u] = -2;  // beyond the k axis
         }
       }
       double bv[U];
@@ -349,9 +367,8 @@ __global__ void __launch_bounds__(kGridThreads, 8) grid_kernel(TablesDev t, Grid
     }
     return;
   }
-  for (int j = 0; j < gl.kpt; ++j) {
-    const int ik = k0 + j * int(blockDim.x) + tid;
-    if (ik >= nK) break;
+  const int im = row / nN, jn = row - im * nN;
+  for (int ik = ctid; ik < nK; ik += kConsumers) {
     const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
     const int start = __double2loint(ki.y);
     int ci;
@@ -382,12 +399,7 @@ __global__ void __launch_bounds__(kGridThreads, 8) grid_kernel(TablesDev t, Grid
     const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
     if (MODE == 0 && !VERIFY) {
       const double* w = W + ci * nb;
-      if (NB > 0) {
-#pragma unroll
-        for (int ib = 0; ib < NB; ++ib) o[ib * plane] = __dmul_rn(base, w[ib]);
-      } else {
-        for (int ib = 0; ib < nb; ++ib, o += plane) *o = __dmul_rn(base, w[ib]);
-      }
+      for (int ib = 0; ib < nb; ++ib, o += plane) *o = __dmul_rn(base, w[ib]);
       continue;
     }
     const uint64_t k = g.K[ik];
@@ -400,7 +412,7 @@ __global__ void __launch_bounds__(kGridThreads, 8) grid_kernel(TablesDev t, Grid
         waves = ceil_div_c(t, ci, 2, blocks, t.bpw[ci]);
         lat = __dmul_rn(base, wave_scale(t, ci, waves));
       } else {
-        const PointResult r = predict_point(t, ci, b, m, n, k, base);
+        const PointResult r = predict_point(t, ci, b, g.M[im], g.N[jn], k, base);
         lat = r.lat;
         blocks = r.blocks;
         waves = r.waves;
@@ -412,6 +424,48 @@ __global__ void __launch_bounds__(kGridThreads, 8) grid_kernel(TablesDev t, Grid
         out.blocks[p] = blocks;
         out.waves[p] = waves;
       }
+    }
+  }
+}
+
+template <bool VERIFY, int MODE, int NEAR, int NB>
+__global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g, GridLaunch gl,
+                                                          const double* __restrict__ base_tab,
+                                                          LaunchOut out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int32_t* gcur = reinterpret_cast<int32_t*>(smem + gl.off_gcur);
+  int32_t* gst = reinterpret_cast<int32_t*>(smem + gl.off_gst);
+  double* glk = reinterpret_cast<double*>(smem + gl.off_glk);
+  uint8_t* bufs = smem + gl.off_buf;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // tile-independent candidate tables
+  for (int j = tid; j < t.R; j += blockDim.x) gcur[j] = t.g_curve[j];
+  for (int j = tid; j < t.G; j += blockDim.x) {
+    gst[j] = t.grp_start[j];
+    glk[j] = t.grp_lk[j];
+  }
+  __syncthreads();
+  if (warp < kProducerWarps) {
+    int it = 0;
+    for (int tile = blockIdx.x; tile < gl.tiles; tile += gridDim.x, ++it) {
+      const int b = it & 1;
+      if (it >= 2) named_sync(kBarEmpty + b, kWsThreads);
+      produce_tile(t, g, gl, warp, lane, tile / gl.nbs, tile % gl.nbs, bufs + b * gl.buf_bytes);
+      named_arrive(kBarFull + b, kWsThreads);
+    }
+    // complete the consumers' last EMPTY arrivals (every barrier instance full)
+    for (int j = max(0, it - 2); j < it; ++j) named_sync(kBarEmpty + (j & 1), kWsThreads);
+  } else {
+    pdl_wait();  // base table complete and visible
+    const int ctid = tid - 32 * kProducerWarps;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < gl.tiles; tile += gridDim.x, ++it) {
+      const int b = it & 1;
+      named_sync(kBarFull + b, kWsThreads);
+      consume_tile<VERIFY, MODE, NEAR, NB>(t, g, gl, base_tab, out, ctid, tile / gl.nbs,
+                                           tile % gl.nbs, bufs + b * gl.buf_bytes, gcur, gst,
+                                           glk);
+      named_arrive(kBarEmpty + b, kWsThreads);
     }
   }
 }
@@ -519,39 +573,48 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   GridLaunch gl{};
   const int64_t rows = g.nM * g.nN;
   const int64_t nb = g.b_hi - g.b_lo;
-  const int64_t target = 148 * 8;
-  const int threads = all_curves ? kThreads : kGridThreads;
-  auto ktiles_for = [&](int kpt) {
-    return int((g.nK + int64_t(kpt) * threads - 1) / (int64_t(kpt) * threads));
-  };
-  gl.kpt = all_curves ? 4 : 8;
-  gl.ktiles = ktiles_for(gl.kpt);
-  while (gl.kpt > 1 && rows * gl.ktiles < target) {
-    gl.kpt >>= 1;
-    gl.ktiles = ktiles_for(gl.kpt);
-  }
-  const int64_t ctas = rows * gl.ktiles;
-  int64_t nbs = 1;
-  if (ctas < target && nb > 1) nbs = std::min<int64_t>(nb, (target + ctas - 1) / ctas);
-  gl.bper = int((nb + nbs - 1) / nbs);
-  gl.nbs = int((nb + gl.bper - 1) / gl.bper);
-  if (all_curves) {
+  if (all_curves) {  // all_curves_kernel: (row, k tile, slab) CTAs of kThreads
+    const int64_t target = 148 * 8;
+    auto ktiles_for = [&](int kpt) {
+      return int((g.nK + int64_t(kpt) * kThreads - 1) / (int64_t(kpt) * kThreads));
+    };
+    gl.kpt = 4;
+    int ktiles = ktiles_for(gl.kpt);
+    while (gl.kpt > 1 && rows * ktiles < target) {
+      gl.kpt >>= 1;
+      ktiles = ktiles_for(gl.kpt);
+    }
+    gl.tiles = ktiles;  // reused as k tiles
+    const int64_t ctas = rows * ktiles;
+    int64_t nbs = 1;
+    if (ctas < target && nb > 1) nbs = std::min<int64_t>(nb, (target + ctas - 1) / ctas);
+    gl.bper = int((nb + nbs - 1) / nbs);
+    gl.nbs = int((nb + gl.bper - 1) / gl.bper);
     gl.mode = (t.all_gemm && 8ll * t.C * (gl.bper + 1) <= 96 * 1024) ? 0 : 2;
     return gl;
   }
+  // warp-specialised grid kernel: (row, batch slab) tiles
+  const int64_t target_tiles = 148 * 8;
+  int64_t nbs = 1;
+  if (rows < target_tiles && nb > 1) nbs = std::min<int64_t>(nb, (target_tiles + rows - 1) / rows);
+  gl.bper = int((nb + nbs - 1) / nbs);
+  gl.nbs = int((nb + gl.bper - 1) / gl.bper);
+  gl.tiles = int(rows * gl.nbs);
+  gl.kpt = int((g.nK + kConsumers - 1) / kConsumers);
   gl.mode = t.all_gemm ? 0 : 2;
   gl.near = (t.NC == 1 && t.lowest_wins) ? 2 : (t.G <= 32 ? 1 : 0);
   smem_layout(t, gl);
-  if (gl.mode == 0 && gl.smem > 160 * 1024) {  // W slice too large for smem
+  if (gl.mode == 0 && gl.smem > 160 * 1024) {  // W slices too large for smem
     gl.mode = 1;
     smem_layout(t, gl);
   }
+  gl.ctas = int(std::min<int64_t>(gl.tiles, 148 * 4));
   return gl;
 }
 
 bool grid_dims_ok(const GridDev& g, const GridLaunch& gl) {
-  return g.nM * g.nN <= 0x7FFFFFFFll && gl.ktiles <= 65535 && gl.nbs <= 65535 &&
-         g.nK <= 0x3FFFFFFFll && g.nB <= 0x7FFFFFFFll;
+  return g.nM * g.nN * gl.nbs <= 0x7FFFFFFFll && gl.nbs <= 65535 && g.nK <= 0x3FFFFFFFll &&
+         g.nB <= 0x7FFFFFFFll;
 }
 
 template <bool V, int M>
@@ -565,11 +628,12 @@ cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gl.smem));
     if (e != cudaSuccess) return e;
   }
-  // programmatic dependent launch: the row setup overlaps the base-table
-  // kernel; griddepcontrol.wait guards the first base-table read
+  if (gl.tiles == 0) return cudaSuccess;
+  // programmatic dependent launch: tile setup overlaps the base-table kernel;
+  // griddepcontrol.wait guards the first base-table read
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
-  cfg.blockDim = dim3(kGridThreads);
+  cfg.gridDim = dim3(unsigned(gl.ctas));
+  cfg.blockDim = dim3(kWsThreads);
   cfg.dynamicSmemBytes = size_t(gl.smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -631,7 +695,7 @@ int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* ws, dou
   const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
   if (card == 0 || t.C == 0) return 0;
   GridLaunch gl = plan_grid(t, g, true);
-  if (!grid_dims_ok(g, gl) || t.C > 65535) return int(cudaErrorInvalidValue);
+  if (!grid_dims_ok(g, gl) || t.C > 65535 || gl.tiles > 65535) return int(cudaErrorInvalidValue);
   launch_base_table(t, g, ws, s);
   const int64_t smem = gl.mode == 0 ? ((8ll * t.C + 15) & ~15ll) + 8ll * t.C * gl.bper : 0;
   if (smem > 48 * 1024) {
@@ -639,7 +703,7 @@ int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* ws, dou
                                          int(smem));
     if (e != cudaSuccess) return int(e);
   }
-  const dim3 grid(unsigned(g.nM * g.nN), unsigned(gl.ktiles), unsigned(gl.nbs));
+  const dim3 grid(unsigned(g.nM * g.nN), unsigned(gl.tiles), unsigned(gl.nbs));
   all_curves_kernel<<<grid, kThreads, smem, s>>>(t, g, gl, ws, out);
   return int(cudaGetLastError());
 }
