@@ -97,7 +97,8 @@ __device__ __forceinline__ uint64_t blocks_of(const TablesDev& t, int c, uint64_
 // waves / ref_waves  (compute.py:137, _kernels.pyx:132)
 __device__ __forceinline__ double wave_scale(const TablesDev& t, int c, uint64_t waves) {
   const double w = __ull2double_rn(waves), rw = t.ref_waves[c];
-  return rw == 1.0 ? w : __ddiv_rn(w, rw);  // x / 1.0 == x exactly (IEEE)
+  if (__builtin_expect(rw == 1.0, 1)) return w;  // x / 1.0 == x exactly (IEEE)
+  return __ddiv_rn(w, rw);
 }
 
 struct PointResult {

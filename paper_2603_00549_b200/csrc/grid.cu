@@ -99,7 +99,7 @@ void smem_layout(const TablesDev& t, GridLaunch& gl) {
     o = (o + bytes + 15) & ~int64_t(15);
     return int(at);
   };
-  gl.off_gcur = take(4ll * t.R);
+  gl.off_gcur = take(8ll * t.R);
   gl.off_gst = take(4ll * t.G);
   gl.off_glk = take(8ll * t.G);
   gl.off_buf = int(o);
@@ -112,8 +112,8 @@ void smem_layout(const TablesDev& t, GridLaunch& gl) {
   gl.b_sD = btake(8ll * t.CM);
   gl.b_sP = btake(4ll * t.CM);
   gl.b_cls = btake(16ll * t.NC);
-  gl.b_T = btake(gl.mode <= 1 ? 8ll * t.C : 0);
-  gl.b_W = btake(gl.mode == 0 ? 8ll * t.C * gl.bper : 0);
+  gl.b_T = btake(gl.mode <= 1 ? 8ll * t.NW : 0);
+  gl.b_W = btake(gl.mode == 0 ? 8ll * t.NW * gl.bper : 0);
   gl.buf_bytes = int(bo);
   gl.smem = o + 2 * bo;
 }
@@ -281,15 +281,15 @@ __device__ __forceinline__ void produce_tile(const TablesDev& t, const GridDev& 
     const uint64_t m = g.M[im], n = g.N[jn];
     const int ib0 = slab * gl.bper;
     const int nb = min(int(g.b_hi - g.b_lo), ib0 + gl.bper) - ib0;
-    for (int c = lane + 32 * (warp - 1); c < t.C; c += 32 * (kProducerWarps - 1)) {
-      if (!curve_valid(t, c)) continue;
+    for (int wc = lane + 32 * (warp - 1); wc < t.NW; wc += 32 * (kProducerWarps - 1)) {
+      const int c = t.wc_rep[wc];  // every curve of the class has these parameters
       const uint64_t tmn = ceil_div_c(t, c, 0, m, t.tile_m[c]) *
                            ceil_div_c(t, c, 1, n, t.tile_n[c]) * t.split_k[c];
-      T[c] = tmn;
+      T[wc] = tmn;
       if (gl.mode == 0) {
         const uint64_t bpw = t.bpw[c];
         for (int ib = 0; ib < nb; ++ib)
-          W[c * nb + ib] =
+          W[wc * nb + ib] =
               wave_scale(t, c, ceil_div_c(t, c, 2, g.B[g.b_lo + ib0 + ib] * tmn, bpw));
       }
     }
@@ -300,7 +300,7 @@ template <bool VERIFY, int MODE, int NEAR, int NB>
 __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& g,
                                              const GridLaunch& gl, const double* base_tab,
                                              const LaunchOut& out, int ctid, int row, int slab,
-                                             const uint8_t* buf, const int32_t* gcur,
+                                             const uint8_t* buf, const int2* gcur,
                                              const int32_t* gst, const double* glk) {
   const uint64_t* sD = reinterpret_cast<const uint64_t*>(buf + gl.b_sD);
   const int32_t* sP = reinterpret_cast<const int32_t*>(buf + gl.b_sP);
@@ -333,15 +333,18 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
         ki[u] = ik[u] < nK ? *reinterpret_cast<const double2*>(&g.kinfo[ik[u]])
                            : make_double2(0.0, 0.0);
       }
-      int ci[U];
+      int ci[U], wc[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (ik[u] < nK) {
           const int2 gp = nearest_one_class(t.G, glk, rv, dmin1, lastpos1, ki[u].x,
                                             __double2loint(ki[u].y));
-          ci[u] = gcur[gst[gp.x] + gp.y];
+          const int2 cw = gcur[gst[gp.x] + gp.y];
+          ci[u] = cw.x;
+          wc[u] = cw.y;
         } else {
           ci[u] = -2;  // beyond the k axis
+          wc[u] = 0;
         }
       }
       double bv[U];
@@ -360,7 +363,7 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
           for (int ib = 0; ib < NB; ++ib) o[ib * plane] = qnan();
           continue;
         }
-        const double* w = W + ci[u] * NB;
+        const double* w = W + wc[u] * NB;
 #pragma unroll
         for (int ib = 0; ib < NB; ++ib) o[ib * plane] = __dmul_rn(bv[u], w[ib]);
       }
@@ -374,7 +377,7 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
     int ci;
     if (NEAR == 2) {
       const int2 gp = nearest_one_class(t.G, glk, rv, dmin1, lastpos1, ki.x, start);
-      ci = gcur[gst[gp.x] + gp.y];
+      ci = gcur[gst[gp.x] + gp.y].x;
     } else {
       const int best = nearest_sweep<NEAR == 1>(t, rv, glk, ki.x, start);
       ci = best < t.R ? t.cand_curve[best] : -1;
@@ -397,8 +400,9 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
       continue;
     }
     const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
+    const int wci = t.wc_of[ci];
     if (MODE == 0 && !VERIFY) {
-      const double* w = W + ci * nb;
+      const double* w = W + wci * nb;
       for (int ib = 0; ib < nb; ++ib, o += plane) *o = __dmul_rn(base, w[ib]);
       continue;
     }
@@ -408,7 +412,7 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
       double lat;
       uint64_t blocks, waves;
       if (MODE <= 1) {
-        blocks = b * T[ci];
+        blocks = b * T[wci];
         waves = ceil_div_c(t, ci, 2, blocks, t.bpw[ci]);
         lat = __dmul_rn(base, wave_scale(t, ci, waves));
       } else {
@@ -433,13 +437,16 @@ __global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g
                                                           const double* __restrict__ base_tab,
                                                           LaunchOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
-  int32_t* gcur = reinterpret_cast<int32_t*>(smem + gl.off_gcur);
+  int2* gcur = reinterpret_cast<int2*>(smem + gl.off_gcur);
   int32_t* gst = reinterpret_cast<int32_t*>(smem + gl.off_gst);
   double* glk = reinterpret_cast<double*>(smem + gl.off_glk);
   uint8_t* bufs = smem + gl.off_buf;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // tile-independent candidate tables
-  for (int j = tid; j < t.R; j += blockDim.x) gcur[j] = t.g_curve[j];
+  // tile-independent candidate tables: (curve, wave class) per group position
+  for (int j = tid; j < t.R; j += blockDim.x) {
+    const int c = t.g_curve[j];
+    gcur[j] = make_int2(c, c >= 0 ? t.wc_of[c] : -1);
+  }
   for (int j = tid; j < t.G; j += blockDim.x) {
     gst[j] = t.grp_start[j];
     glk[j] = t.grp_lk[j];

@@ -41,6 +41,11 @@ struct TablesDev {
   // dv_m = multiplier, dv_s = sh1 | sh2 << 8 | valid << 16 (Granlund-Montgomery)
   const uint32_t* dv_m = nullptr;
   const uint32_t* dv_s = nullptr;
+  // wave classes: curves with identical (rowblock, tile_m, tile_n, split_k,
+  // blocks_per_wave, ref_waves) share every blocks / waves / wave-scale value
+  int32_t NW = 0;
+  const int32_t* wc_of = nullptr;   // [C] class of each curve (-1: no samples)
+  const int32_t* wc_rep = nullptr;  // [NW] representative curve of each class
   const uint8_t* rowblock = nullptr;
   const int32_t* s_off = nullptr;    // [C+1] sample offsets
   const double* s_dims = nullptr;

@@ -186,6 +186,24 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
       dv_s[3 * c + j] = sh1 | (sh2 << 8) | (1u << 16);
     }
   }
+  // wave classes
+  std::vector<int32_t> wc_of(C, -1), wc_rep;
+  {
+    std::map<std::array<uint64_t, 6>, int32_t> seen;
+    for (int64_t c = 0; c < C; ++c) {
+      if (v->sample_offsets[c + 1] <= v->sample_offsets[c]) continue;
+      uint64_t rw;
+      std::memcpy(&rw, &v->ref_waves[c], 8);
+      const std::array<uint64_t, 6> key = {uint64_t(v->family_rowblock[c] ? 1 : 0), v->tile_m[c],
+                                           v->tile_n[c], v->split_k[c], v->blocks_per_wave[c], rw};
+      auto it = seen.find(key);
+      if (it == seen.end()) {
+        it = seen.emplace(key, int32_t(wc_rep.size())).first;
+        wc_rep.push_back(int32_t(c));
+      }
+      wc_of[c] = it->second;
+    }
+  }
   std::vector<int32_t> s_off(C + 1);
   for (int64_t c = 0; c <= C; ++c) s_off[c] = int32_t(v->sample_offsets[c]);
   std::vector<uint8_t> rowblock(C);
@@ -214,6 +232,9 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.bpw = blob.add(v->blocks_per_wave, C);
   t.dv_m = blob.add(dv_m);
   t.dv_s = blob.add(dv_s);
+  t.NW = int32_t(wc_rep.size());
+  t.wc_of = blob.add(wc_of);
+  t.wc_rep = blob.add(wc_rep);
   t.rowblock = blob.add(rowblock);
   t.s_off = blob.add(s_off);
   t.s_dims = blob.add(v->sample_dims, S);
@@ -248,6 +269,7 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.tile_m = shift(o.tile_m, base); t.tile_n = shift(o.tile_n, base);
   t.split_k = shift(o.split_k, base); t.bpw = shift(o.bpw, base);
   t.dv_m = shift(o.dv_m, base); t.dv_s = shift(o.dv_s, base);
+  t.wc_of = shift(o.wc_of, base); t.wc_rep = shift(o.wc_rep, base);
   t.rowblock = shift(o.rowblock, base); t.s_off = shift(o.s_off, base);
   t.s_dims = shift(o.s_dims, base); t.s_thrs = shift(o.s_thrs, base);
   t.g_lm = shift(o.g_lm, base); t.g_ln = shift(o.g_ln, base);
