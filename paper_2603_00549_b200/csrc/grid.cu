@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) base_table_kernel(TablesDev t, const uint
 // two shared-memory buffers while consumers compute the current tile's points
 // from the other; the hand-off uses named barriers (FULL/EMPTY per buffer).
 constexpr int kProducerWarps = 2;   // warp 0: staircases, warp 1: Tmn / W
-constexpr int kConsumerWarps = 4;
+constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kWsThreads = 32 * (kProducerWarps + kConsumerWarps);
 
@@ -615,7 +615,7 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
     gl.mode = 1;
     smem_layout(t, gl);
   }
-  gl.ctas = int(std::min<int64_t>(gl.tiles, 148 * 4));
+  gl.ctas = int(std::min<int64_t>(gl.tiles, 148 * 3));
   return gl;
 }
 
