@@ -82,7 +82,8 @@ struct GridLaunch {
   int ctas;      // persistent CTAs
   // shared memory: constant part, then two row-state buffers
   int off_gcur, off_gst, off_glk, off_buf, buf_bytes;
-  int b_sD, b_sP, b_cls, b_T, b_W;  // offsets inside a buffer
+  int b_sD, b_sP, b_cls, b_T, b_W, b_fix, b_nfix;  // offsets inside a buffer
+  int fix_cap;   // in-kernel exact-hit fix-ups per row (0: separate fixup_kernel)
   int64_t smem;
 };
 
@@ -114,6 +115,8 @@ void smem_layout(const TablesDev& t, GridLaunch& gl) {
   gl.b_cls = btake(16ll * t.NC);
   gl.b_T = btake(gl.mode <= 1 ? 8ll * t.NW : 0);
   gl.b_W = btake(gl.mode == 0 ? 8ll * t.NW * gl.bper : 0);
+  gl.b_fix = btake(16ll * gl.fix_cap);
+  gl.b_nfix = btake(16);
   gl.buf_bytes = int(bo);
   gl.smem = o + 2 * bo;
 }
@@ -239,6 +242,12 @@ __device__ __forceinline__ void produce_tile(const TablesDev& t, const GridDev& 
   ClassRow* scls = reinterpret_cast<ClassRow*>(buf + gl.b_cls);
   const int nN = int(g.nN);
   const int im = row / nN, jn = row - im * nN;
+  if (gl.fix_cap > 0) {  // exact-hit fix-ups of this row (usually none)
+    const int f0 = g.fixr_off[row], nf = g.fixr_off[row + 1] - f0;
+    FixEntry* fx = reinterpret_cast<FixEntry*>(buf + gl.b_fix);
+    for (int j = lane + 32 * warp; j < nf; j += 32 * kProducerWarps) fx[j] = g.fixr[f0 + j];
+    if (warp == 0 && lane == 0) *reinterpret_cast<int*>(buf + gl.b_nfix) = nf;
+  }
   if (warp == 0) {
     // member-class staircases: prefix minimum of D in member (scan) order
     const double qm = g.logM[im], qn = g.logN[jn];
@@ -319,7 +328,9 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
   }
   const int64_t plane = g.nM * g.nN * g.nK;
   double* const obase = out.lat + int64_t(ib0) * plane + int64_t(row) * nK;
-  if (NEAR == 2 && MODE == 0 && !VERIFY && NB > 0) {
+  const int nfix = gl.fix_cap > 0 ? *reinterpret_cast<const int*>(buf + gl.b_nfix) : 0;
+  const FixEntry* fx = reinterpret_cast<const FixEntry*>(buf + gl.b_fix);
+  if (NEAR == 2 && MODE == 0 && !VERIFY && NB > 0 && nfix == 0) {
     // hot path, software-pipelined in groups of U k values: all kinfo loads,
     // then all nearest searches, then all base-table loads in flight
     // together, then the stores
@@ -370,7 +381,10 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
     }
     return;
   }
+  // general path: every mode / verification, and rows with exact-hit
+  // fix-ups (the recorded kernel overrides the nearest one, _kernels.pyx:107-110)
   const int im = row / nN, jn = row - im * nN;
+  const uint64_t m = g.M[im], n = g.N[jn];
   for (int ik = ctid; ik < nK; ik += kConsumers) {
     const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
     const int start = __double2loint(ki.y);
@@ -382,49 +396,50 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
       const int best = nearest_sweep<NEAR == 1>(t, rv, glk, ki.x, start);
       ci = best < t.R ? t.cand_curve[best] : -1;
     }
-    double* o = obase + ik;
-    if (ci < 0) {
-      if (out.nan_stats) {
-        atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
-        atomicAdd(out.nan_stats + 1, (unsigned long long)nb);
-      }
-      for (int ib = 0; ib < nb; ++ib, o += plane) {
-        *o = qnan();
-        if (VERIFY) {
-          const int64_t p = o - out.lat;
-          out.curve[p] = -1;
-          out.blocks[p] = 0;
-          out.waves[p] = 0;
-        }
-      }
-      continue;
-    }
-    const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
-    const int wci = t.wc_of[ci];
-    if (MODE == 0 && !VERIFY) {
-      const double* w = W + wci * nb;
-      for (int ib = 0; ib < nb; ++ib, o += plane) *o = __dmul_rn(base, w[ib]);
-      continue;
-    }
     const uint64_t k = g.K[ik];
+    const double base =
+        ci < 0 ? 0.0 : base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, k);
+    const int wci = ci < 0 ? -1 : t.wc_of[ci];
+    double* o = obase + ik;
     for (int ib = 0; ib < nb; ++ib, o += plane) {
-      const uint64_t b = g.B[g.b_lo + ib0 + ib];
+      int c = ci;
+      double bs = base;
+      bool exact = false;
+      for (int f = 0; f < nfix; ++f)  // rows with fix-ups only
+        if (fx[f].ik == ik && fx[f].ib == ib0 + ib) {
+          c = fx[f].curve;
+          exact = true;
+        }
       double lat;
-      uint64_t blocks, waves;
-      if (MODE <= 1) {
+      uint64_t blocks = 0, waves = 0;
+      const uint64_t b = g.B[g.b_lo + ib0 + ib];
+      if (c < 0) {
+        lat = qnan();
+      } else if (exact) {
+        const PointResult r = predict_point(t, c, b, m, n, k, base_of(t, c, k));
+        lat = r.lat;
+        blocks = r.blocks;
+        waves = r.waves;
+      } else if (MODE == 0 && !VERIFY) {
+        lat = __dmul_rn(bs, W[wci * nb + ib]);
+      } else if (MODE <= 1) {
         blocks = b * T[wci];
-        waves = ceil_div_c(t, ci, 2, blocks, t.bpw[ci]);
-        lat = __dmul_rn(base, wave_scale(t, ci, waves));
+        waves = ceil_div_c(t, c, 2, blocks, t.bpw[c]);
+        lat = __dmul_rn(bs, wave_scale(t, c, waves));
       } else {
-        const PointResult r = predict_point(t, ci, b, g.M[im], g.N[jn], k, base);
+        const PointResult r = predict_point(t, c, b, m, n, k, bs);
         lat = r.lat;
         blocks = r.blocks;
         waves = r.waves;
       }
       *o = lat;
+      if (c < 0 && out.nan_stats) {
+        atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
+        atomicAdd(out.nan_stats + 1, 1ull);
+      }
       if (VERIFY) {
         const int64_t p = o - out.lat;
-        out.curve[p] = ci;
+        out.curve[p] = c;
         out.blocks[p] = blocks;
         out.waves[p] = waves;
       }
@@ -610,6 +625,7 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   gl.kpt = int((g.nK + kConsumers - 1) / kConsumers);
   gl.mode = t.all_gemm ? 0 : 2;
   gl.near = (t.NC == 1 && t.lowest_wins) ? 2 : (t.G <= 32 ? 1 : 0);
+  gl.fix_cap = (g.n_fix > 0 && g.max_fix_row <= 512) ? g.max_fix_row : 0;
   smem_layout(t, gl);
   if (gl.mode == 0 && gl.smem > 160 * 1024) {  // W slices too large for smem
     gl.mode = 1;
@@ -688,7 +704,7 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
     }
   }
   if (e != cudaSuccess) return int(e);
-  if (g.n_fix > 0 && (stages & kStageFixup)) {
+  if (g.n_fix > 0 && gl.fix_cap == 0 && (stages & kStageFixup)) {
     const int nb = int((g.n_fix + 127) / 128);
     if (v) fixup_kernel<true><<<nb, 128, 0, s>>>(t, g, out);
     else fixup_kernel<false><<<nb, 128, 0, s>>>(t, g, out);

@@ -84,6 +84,14 @@ struct alignas(16) KInfo {
   int32_t pad;
 };
 
+// Exact-hit fix-up of one grid point, bucketed by (m, n) row.
+struct alignas(16) FixEntry {
+  int32_t ik;     // k index
+  int32_t ib;     // batch index, slice-relative
+  int32_t curve;  // recorded kernel's curve (-1: no curve -> NaN)
+  int32_t pad;
+};
+
 // Per-launch grid description (device pointers into one per-call upload).
 struct GridDev {
   int64_t nB = 0, nM = 0, nN = 0, nK = 0;  // full axis lengths
@@ -102,6 +110,11 @@ struct GridDev {
   const int64_t* fix_pos = nullptr;
   const uint64_t* fix_coord = nullptr;  // 4 per fix-up
   const int32_t* fix_curve = nullptr;
+  // the same fix-ups bucketed by (m, n) row for the in-kernel path:
+  // entries {ik, ib (slice-relative), curve, 0}, rows+1 offsets
+  const int32_t* fixr_off = nullptr;
+  const FixEntry* fixr = nullptr;
+  int32_t max_fix_row = 0;
 };
 
 // Host-side image of the staged tables (one contiguous byte blob whose

@@ -344,10 +344,31 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   std::vector<int64_t> fix_pos;
   std::vector<uint64_t> fix_coord;
   std::vector<int32_t> fix_curve;
+  const int64_t rows = nM * nN, inner = nM * nN * nK;
+  std::vector<int32_t> fixr_off(rows + 1, 0);
+  std::vector<FixEntry> fixr;
   for (auto& [pos, val] : fix) {
     fix_pos.push_back(pos);
     for (int j = 0; j < 4; ++j) fix_coord.push_back(val.first[j]);
     fix_curve.push_back(val.second);
+    const int64_t ib = pos / inner, rem = pos - ib * inner;
+    fixr_off[rem / nK + 1] += 1;
+  }
+  int32_t max_fix_row = 0;
+  for (int64_t r = 0; r < rows; ++r) {
+    max_fix_row = std::max(max_fix_row, fixr_off[r + 1]);
+    fixr_off[r + 1] += fixr_off[r];
+  }
+  fixr.resize(fix_pos.size());
+  {
+    std::vector<int32_t> fill(fixr_off.begin(), fixr_off.end() - 1);
+    size_t i = 0;
+    for (auto& [pos, val] : fix) {
+      const int64_t ib = pos / inner, rem = pos - ib * inner;
+      const int64_t row = rem / nK, ik = rem - row * nK;
+      fixr[fill[row]++] = FixEntry{int32_t(ik), int32_t(ib), val.second, 0};
+      ++i;
+    }
   }
 
   Blob blob;
@@ -366,6 +387,9 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   g.fix_pos = blob.add(fix_pos);
   g.fix_coord = blob.add(fix_coord);
   g.fix_curve = blob.add(fix_curve);
+  g.fixr_off = blob.add(fixr_off);
+  g.fixr = blob.add(fixr);
+  g.max_fix_row = max_fix_row;
   out->blob.swap(blob.bytes());
   return "";
 }
@@ -377,6 +401,7 @@ GridDev rebase(const GridDev& o, const void* base) {
   g.logK = shift(o.logK, base); g.kinfo = shift(o.kinfo, base);
   g.fix_pos = shift(o.fix_pos, base);
   g.fix_coord = shift(o.fix_coord, base); g.fix_curve = shift(o.fix_curve, base);
+  g.fixr_off = shift(o.fixr_off, base); g.fixr = shift(o.fixr, base);
   return g;
 }
 
