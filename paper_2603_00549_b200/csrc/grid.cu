@@ -234,23 +234,44 @@ __device__ __forceinline__ int2 nearest_one_class(int G, const double* __restric
 }
 
 // Row state of one (row, slab) tile, produced into buffer `buf`.
+// Row scalars a producer needs, loaded one tile ahead (latency off the
+// producer's critical path).
+struct RowPre {
+  double qm, qn;
+  uint64_t m, n;
+  int f0, nf;
+};
+
+__device__ __forceinline__ RowPre load_row(const GridDev& g, const GridLaunch& gl, int row) {
+  const int nN = int(g.nN);
+  const int im = row / nN, jn = row - im * nN;
+  RowPre r;
+  r.qm = g.logM[im];
+  r.qn = g.logN[jn];
+  r.m = g.M[im];
+  r.n = g.N[jn];
+  r.f0 = r.nf = 0;
+  if (gl.fix_cap > 0) {
+    r.f0 = g.fixr_off[row];
+    r.nf = g.fixr_off[row + 1] - r.f0;
+  }
+  return r;
+}
+
 __device__ __forceinline__ void produce_tile(const TablesDev& t, const GridDev& g,
-                                             const GridLaunch& gl, int warp, int lane, int row,
-                                             int slab, uint8_t* buf) {
+                                             const GridLaunch& gl, int warp, int lane,
+                                             const RowPre& rp, int slab, uint8_t* buf) {
   uint64_t* sD = reinterpret_cast<uint64_t*>(buf + gl.b_sD);
   int32_t* sP = reinterpret_cast<int32_t*>(buf + gl.b_sP);
   ClassRow* scls = reinterpret_cast<ClassRow*>(buf + gl.b_cls);
-  const int nN = int(g.nN);
-  const int im = row / nN, jn = row - im * nN;
   if (gl.fix_cap > 0) {  // exact-hit fix-ups of this row (usually none)
-    const int f0 = g.fixr_off[row], nf = g.fixr_off[row + 1] - f0;
     FixEntry* fx = reinterpret_cast<FixEntry*>(buf + gl.b_fix);
-    for (int j = lane + 32 * warp; j < nf; j += 32 * kProducerWarps) fx[j] = g.fixr[f0 + j];
-    if (warp == 0 && lane == 0) *reinterpret_cast<int*>(buf + gl.b_nfix) = nf;
+    for (int j = lane + 32 * warp; j < rp.nf; j += 32 * kProducerWarps) fx[j] = g.fixr[rp.f0 + j];
+    if (warp == 0 && lane == 0) *reinterpret_cast<int*>(buf + gl.b_nfix) = rp.nf;
   }
   if (warp == 0) {
     // member-class staircases: prefix minimum of D in member (scan) order
-    const double qm = g.logM[im], qn = g.logN[jn];
+    const double qm = rp.qm, qn = rp.qn;
     for (int ci = 0; ci < t.NC; ++ci) {
       const int start = t.cls_start[ci], size = t.cls_size[ci];
       uint64_t carry = ~0ull;
@@ -287,7 +308,7 @@ __device__ __forceinline__ void produce_tile(const TablesDev& t, const GridDev& 
     // tiles per (m, n) and the curve-major wave-scale table W[c][ib]
     uint64_t* T = reinterpret_cast<uint64_t*>(buf + gl.b_T);
     double* W = reinterpret_cast<double*>(buf + gl.b_W);
-    const uint64_t m = g.M[im], n = g.N[jn];
+    const uint64_t m = rp.m, n = rp.n;
     const int ib0 = slab * gl.bper;
     const int nb = min(int(g.b_hi - g.b_lo), ib0 + gl.bper) - ib0;
     for (int wc = lane + 32 * (warp - 1); wc < t.NW; wc += 32 * (kProducerWarps - 1)) {
@@ -469,11 +490,16 @@ __global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g
   __syncthreads();
   if (warp < kProducerWarps) {
     int it = 0;
-    for (int tile = blockIdx.x; tile < gl.tiles; tile += gridDim.x, ++it) {
+    int tile = blockIdx.x;
+    RowPre cur = tile < gl.tiles ? load_row(g, gl, tile / gl.nbs) : RowPre{};
+    for (; tile < gl.tiles; tile += gridDim.x, ++it) {
+      const int nt = tile + gridDim.x;
+      const RowPre nxt = nt < gl.tiles ? load_row(g, gl, nt / gl.nbs) : cur;  // prefetch
       const int b = it & 1;
       if (it >= 2) named_sync(kBarEmpty + b, kWsThreads);
-      produce_tile(t, g, gl, warp, lane, tile / gl.nbs, tile % gl.nbs, bufs + b * gl.buf_bytes);
+      produce_tile(t, g, gl, warp, lane, cur, tile % gl.nbs, bufs + b * gl.buf_bytes);
       named_arrive(kBarFull + b, kWsThreads);
+      cur = nxt;
     }
     // complete the consumers' last EMPTY arrivals (every barrier instance full)
     for (int j = max(0, it - 2); j < it; ++j) named_sync(kBarEmpty + (j & 1), kWsThreads);
