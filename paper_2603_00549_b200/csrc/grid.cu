@@ -34,11 +34,23 @@ __device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.lau
 // with the curve's samples staged in shared memory.
 constexpr int kMaxSmemSamples = 256;
 
-__global__ void __launch_bounds__(256) base_table_kernel(TablesDev t, const uint64_t* __restrict__ K,
-                                                         int nK, double* __restrict__ base) {
+__global__ void __launch_bounds__(256) base_table_kernel(TablesDev t, GridDev g,
+                                                         const uint64_t* __restrict__ K, int nK,
+                                                         double* __restrict__ base,
+                                                         double* __restrict__ fixval) {
   pdl_release();  // the grid kernel may start its (independent) row setup now
   __shared__ double sd[kMaxSmemSamples], sy[kMaxSmemSamples];
   const int c = blockIdx.y;
+  if (c == t.C) {  // exact-record hits: their final latency, applied after the grid kernel
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < g.n_fix;
+         i += int64_t(gridDim.x) * blockDim.x) {
+      const uint64_t* c4 = g.fix_coord + 4 * i;
+      const int ci = g.fix_curve[i];
+      fixval[i] = ci < 0 ? qnan()
+                         : predict_point(t, ci, c4[0], c4[1], c4[2], c4[3], base_of(t, ci, c4[3])).lat;
+    }
+    return;
+  }
   const int lo = t.s_off[c], hi = t.s_off[c + 1], ns = hi - lo;
   if (ns <= 0) {
     for (int ik = blockIdx.x * blockDim.x + threadIdx.x; ik < nK; ik += gridDim.x * blockDim.x)
@@ -82,8 +94,7 @@ struct GridLaunch {
   int ctas;      // persistent CTAs
   // shared memory: constant part, then two row-state buffers
   int off_gcur, off_gst, off_glk, off_buf, buf_bytes;
-  int b_sD, b_sP, b_cls, b_T, b_W, b_fix, b_nfix;  // offsets inside a buffer
-  int fix_cap;   // in-kernel exact-hit fix-ups per row (0: separate fixup_kernel)
+  int b_sD, b_sP, b_cls, b_T, b_W;  // offsets inside a buffer
   int64_t smem;
 };
 
@@ -115,8 +126,6 @@ void smem_layout(const TablesDev& t, GridLaunch& gl) {
   gl.b_cls = btake(16ll * t.NC);
   gl.b_T = btake(gl.mode <= 1 ? 8ll * t.NW : 0);
   gl.b_W = btake(gl.mode == 0 ? 8ll * t.NW * gl.bper : 0);
-  gl.b_fix = btake(16ll * gl.fix_cap);
-  gl.b_nfix = btake(16);
   gl.buf_bytes = int(bo);
   gl.smem = o + 2 * bo;
 }
@@ -239,23 +248,12 @@ __device__ __forceinline__ int2 nearest_one_class(int G, const double* __restric
 struct RowPre {
   double qm, qn;
   uint64_t m, n;
-  int f0, nf;
 };
 
-__device__ __forceinline__ RowPre load_row(const GridDev& g, const GridLaunch& gl, int row) {
+__device__ __forceinline__ RowPre load_row(const GridDev& g, int row) {
   const int nN = int(g.nN);
   const int im = row / nN, jn = row - im * nN;
-  RowPre r;
-  r.qm = g.logM[im];
-  r.qn = g.logN[jn];
-  r.m = g.M[im];
-  r.n = g.N[jn];
-  r.f0 = r.nf = 0;
-  if (gl.fix_cap > 0) {
-    r.f0 = g.fixr_off[row];
-    r.nf = g.fixr_off[row + 1] - r.f0;
-  }
-  return r;
+  return RowPre{g.logM[im], g.logN[jn], g.M[im], g.N[jn]};
 }
 
 __device__ __forceinline__ void produce_tile(const TablesDev& t, const GridDev& g,
@@ -264,11 +262,6 @@ __device__ __forceinline__ void produce_tile(const TablesDev& t, const GridDev& 
   uint64_t* sD = reinterpret_cast<uint64_t*>(buf + gl.b_sD);
   int32_t* sP = reinterpret_cast<int32_t*>(buf + gl.b_sP);
   ClassRow* scls = reinterpret_cast<ClassRow*>(buf + gl.b_cls);
-  if (gl.fix_cap > 0) {  // exact-hit fix-ups of this row (usually none)
-    FixEntry* fx = reinterpret_cast<FixEntry*>(buf + gl.b_fix);
-    for (int j = lane + 32 * warp; j < rp.nf; j += 32 * kProducerWarps) fx[j] = g.fixr[rp.f0 + j];
-    if (warp == 0 && lane == 0) *reinterpret_cast<int*>(buf + gl.b_nfix) = rp.nf;
-  }
   if (warp == 0) {
     // member-class staircases: prefix minimum of D in member (scan) order
     const double qm = rp.qm, qn = rp.qn;
@@ -349,9 +342,7 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
   }
   const int64_t plane = g.nM * g.nN * g.nK;
   double* const obase = out.lat + int64_t(ib0) * plane + int64_t(row) * nK;
-  const int nfix = gl.fix_cap > 0 ? *reinterpret_cast<const int*>(buf + gl.b_nfix) : 0;
-  const FixEntry* fx = reinterpret_cast<const FixEntry*>(buf + gl.b_fix);
-  if (NEAR == 2 && MODE == 0 && !VERIFY && NB > 0 && nfix == 0) {
+  if (NEAR == 2 && MODE == 0 && !VERIFY && NB > 0) {
     // hot path, software-pipelined in groups of U k values: all kinfo loads,
     // then all nearest searches, then all base-table loads in flight
     // together, then the stores
@@ -402,10 +393,7 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
     }
     return;
   }
-  // general path: every mode / verification, and rows with exact-hit
-  // fix-ups (the recorded kernel overrides the nearest one, _kernels.pyx:107-110)
   const int im = row / nN, jn = row - im * nN;
-  const uint64_t m = g.M[im], n = g.N[jn];
   for (int ik = ctid; ik < nK; ik += kConsumers) {
     const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
     const int start = __double2loint(ki.y);
@@ -417,50 +405,49 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
       const int best = nearest_sweep<NEAR == 1>(t, rv, glk, ki.x, start);
       ci = best < t.R ? t.cand_curve[best] : -1;
     }
-    const uint64_t k = g.K[ik];
-    const double base =
-        ci < 0 ? 0.0 : base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, k);
-    const int wci = ci < 0 ? -1 : t.wc_of[ci];
     double* o = obase + ik;
-    for (int ib = 0; ib < nb; ++ib, o += plane) {
-      int c = ci;
-      double bs = base;
-      bool exact = false;
-      for (int f = 0; f < nfix; ++f)  // rows with fix-ups only
-        if (fx[f].ik == ik && fx[f].ib == ib0 + ib) {
-          c = fx[f].curve;
-          exact = true;
+    if (ci < 0) {
+      if (out.nan_stats) {
+        atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
+        atomicAdd(out.nan_stats + 1, (unsigned long long)nb);
+      }
+      for (int ib = 0; ib < nb; ++ib, o += plane) {
+        *o = qnan();
+        if (VERIFY) {
+          const int64_t p = o - out.lat;
+          out.curve[p] = -1;
+          out.blocks[p] = 0;
+          out.waves[p] = 0;
         }
-      double lat;
-      uint64_t blocks = 0, waves = 0;
+      }
+      continue;
+    }
+    const double base = base_tab ? base_tab[ci * nK + ik] : base_of(t, ci, g.K[ik]);
+    const int wci = t.wc_of[ci];
+    if (MODE == 0 && !VERIFY) {
+      const double* w = W + wci * nb;
+      for (int ib = 0; ib < nb; ++ib, o += plane) *o = __dmul_rn(base, w[ib]);
+      continue;
+    }
+    const uint64_t k = g.K[ik];
+    for (int ib = 0; ib < nb; ++ib, o += plane) {
       const uint64_t b = g.B[g.b_lo + ib0 + ib];
-      if (c < 0) {
-        lat = qnan();
-      } else if (exact) {
-        const PointResult r = predict_point(t, c, b, m, n, k, base_of(t, c, k));
-        lat = r.lat;
-        blocks = r.blocks;
-        waves = r.waves;
-      } else if (MODE == 0 && !VERIFY) {
-        lat = __dmul_rn(bs, W[wci * nb + ib]);
-      } else if (MODE <= 1) {
+      double lat;
+      uint64_t blocks, waves;
+      if (MODE <= 1) {
         blocks = b * T[wci];
-        waves = ceil_div_c(t, c, 2, blocks, t.bpw[c]);
-        lat = __dmul_rn(bs, wave_scale(t, c, waves));
+        waves = ceil_div_c(t, ci, 2, blocks, t.bpw[ci]);
+        lat = __dmul_rn(base, wave_scale(t, ci, waves));
       } else {
-        const PointResult r = predict_point(t, c, b, m, n, k, bs);
+        const PointResult r = predict_point(t, ci, b, g.M[im], g.N[jn], k, base);
         lat = r.lat;
         blocks = r.blocks;
         waves = r.waves;
       }
       *o = lat;
-      if (c < 0 && out.nan_stats) {
-        atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
-        atomicAdd(out.nan_stats + 1, 1ull);
-      }
       if (VERIFY) {
         const int64_t p = o - out.lat;
-        out.curve[p] = c;
+        out.curve[p] = ci;
         out.blocks[p] = blocks;
         out.waves[p] = waves;
       }
@@ -491,10 +478,10 @@ __global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g
   if (warp < kProducerWarps) {
     int it = 0;
     int tile = blockIdx.x;
-    RowPre cur = tile < gl.tiles ? load_row(g, gl, tile / gl.nbs) : RowPre{};
+    RowPre cur = tile < gl.tiles ? load_row(g, tile / gl.nbs) : RowPre{};
     for (; tile < gl.tiles; tile += gridDim.x, ++it) {
       const int nt = tile + gridDim.x;
-      const RowPre nxt = nt < gl.tiles ? load_row(g, gl, nt / gl.nbs) : cur;  // prefetch
+      const RowPre nxt = nt < gl.tiles ? load_row(g, nt / gl.nbs) : cur;  // prefetch
       const int b = it & 1;
       if (it >= 2) named_sync(kBarEmpty + b, kWsThreads);
       produce_tile(t, g, gl, warp, lane, cur, tile % gl.nbs, bufs + b * gl.buf_bytes);
@@ -519,8 +506,10 @@ __global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g
 }
 
 // Exact-record hits take priority over the nearest result (_kernels.pyx:107-110).
+// `fixval` (nullable) holds their latencies, precomputed by the base-table
+// kernel off the critical path.
 template <bool VERIFY>
-__global__ void fixup_kernel(TablesDev t, GridDev g, LaunchOut out) {
+__global__ void fixup_kernel(TablesDev t, GridDev g, LaunchOut out, const double* fixval) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= g.n_fix) return;
   const int64_t p = g.fix_pos[i];
@@ -543,6 +532,10 @@ __global__ void fixup_kernel(TablesDev t, GridDev g, LaunchOut out) {
   if (ci < 0) {
     out.lat[p] = qnan();
     if (VERIFY) { out.curve[p] = -1; out.blocks[p] = 0; out.waves[p] = 0; }
+    return;
+  }
+  if (!VERIFY && fixval) {
+    out.lat[p] = fixval[i];
     return;
   }
   const PointResult r = predict_point(t, ci, c4[0], c4[1], c4[2], c4[3], base_of(t, ci, c4[3]));
@@ -651,7 +644,6 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   gl.kpt = int((g.nK + kConsumers - 1) / kConsumers);
   gl.mode = t.all_gemm ? 0 : 2;
   gl.near = (t.NC == 1 && t.lowest_wins) ? 2 : (t.G <= 32 ? 1 : 0);
-  gl.fix_cap = (g.n_fix > 0 && g.max_fix_row <= 512) ? g.max_fix_row : 0;
   smem_layout(t, gl);
   if (gl.mode == 0 && gl.smem > 160 * 1024) {  // W slices too large for smem
     gl.mode = 1;
@@ -693,15 +685,17 @@ cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch
   return cudaLaunchKernelEx(&cfg, fn, t, g, gl, base, out);
 }
 
-void launch_base_table(const TablesDev& t, const GridDev& g, double* ws, cudaStream_t s) {
+void launch_base_table(const TablesDev& t, const GridDev& g, double* ws, double* fixval,
+                       cudaStream_t s) {
   const int chunks = int(std::min<int64_t>((g.nK + 255) / 256, 64));
-  base_table_kernel<<<dim3(chunks, t.C), 256, 0, s>>>(t, g.K, int(g.nK), ws);
+  const int ys = t.C + (fixval && g.n_fix > 0 ? 1 : 0);
+  base_table_kernel<<<dim3(chunks, ys), 256, 0, s>>>(t, g, g.K, int(g.nK), ws, fixval);
 }
 
 }  // namespace
 
 int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g) {
-  return int64_t(t.C) * g.nK;
+  return int64_t(t.C) * g.nK + g.n_fix;  // base table, then exact-hit values
 }
 
 int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, double* ws,
@@ -710,12 +704,15 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
   if (card == 0) return 0;
   const GridLaunch gl = plan_grid(t, g, false);
-  const int64_t need = int64_t(t.C) * g.nK;
+  const int64_t nbase = int64_t(t.C) * g.nK, need = nbase + g.n_fix;
   if ((need > 0 && (!ws || ws_elems < need)) || !grid_dims_ok(g, gl) || gl.smem > 227 * 1024 ||
-      t.C > 65535 || need > 0x7FFFFFFFll)
+      t.C >= 65535 || nbase > 0x7FFFFFFFll)
     return int(cudaErrorInvalidValue);
   const double* base = t.C > 0 ? ws : nullptr;
-  if ((stages & kStageBase) && t.C > 0) launch_base_table(t, g, ws, s);
+  // exact-hit values are precomputed with the base table whenever it runs in
+  // the same launch sequence (stage masks that skip it recompute in fixup_kernel)
+  double* fixval = (g.n_fix > 0 && (stages & kStageBase)) ? ws + nbase : nullptr;
+  if ((stages & kStageBase) && (t.C > 0 || fixval)) launch_base_table(t, g, ws, fixval, s);
   const bool v = out.curve != nullptr;
   cudaError_t e = cudaSuccess;
   if (stages & kStageGrid) {
@@ -730,10 +727,10 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
     }
   }
   if (e != cudaSuccess) return int(e);
-  if (g.n_fix > 0 && gl.fix_cap == 0 && (stages & kStageFixup)) {
+  if (g.n_fix > 0 && (stages & kStageFixup)) {
     const int nb = int((g.n_fix + 127) / 128);
-    if (v) fixup_kernel<true><<<nb, 128, 0, s>>>(t, g, out);
-    else fixup_kernel<false><<<nb, 128, 0, s>>>(t, g, out);
+    if (v) fixup_kernel<true><<<nb, 128, 0, s>>>(t, g, out, nullptr);
+    else fixup_kernel<false><<<nb, 128, 0, s>>>(t, g, out, fixval);
   }
   return int(cudaGetLastError());
 }
@@ -745,7 +742,7 @@ int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* ws, dou
   if (card == 0 || t.C == 0) return 0;
   GridLaunch gl = plan_grid(t, g, true);
   if (!grid_dims_ok(g, gl) || t.C > 65535 || gl.tiles > 65535) return int(cudaErrorInvalidValue);
-  launch_base_table(t, g, ws, s);
+  launch_base_table(t, g, ws, nullptr, s);
   const int64_t smem = gl.mode == 0 ? ((8ll * t.C + 15) & ~15ll) + 8ll * t.C * gl.bper : 0;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(all_curves_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
