@@ -142,6 +142,10 @@ int pm2l_grid_plan_launch(pm2l_grid_plan* p, double* out_lat, int32_t* out_curve
 /* info[0] slice cardinality, [1] exact fix-ups, [2] workspace bytes,
  * [3] bytes staged host->device at creation. */
 int pm2l_grid_plan_info(const pm2l_grid_plan* p, int64_t* info);
+/* Which grid kernel a launch with these outputs would run (diagnostics and
+ * tests): 0 general k-group sweep, 1 sweep + tie mask, 2 one-class closed
+ * form, 3 one-class lookup path; negative on error. */
+int pm2l_grid_plan_kernel(const pm2l_grid_plan* p, const double* out_lat, int verify);
 int pm2l_grid_plan_destroy(pm2l_grid_plan* p);
 /* first NaN index of lat[0..n) -> atomicMin into *first (DEVICE u64). */
 int pm2l_nan_scan(const double* lat, int64_t n, uint64_t* first, void* stream);

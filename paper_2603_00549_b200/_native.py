@@ -16,7 +16,9 @@ import numpy as np
 
 from .errors import BackendUnavailable, DeviceError, ValidationError
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpm2l_b200.so")
+# PM2L_LIB_PATH: diagnostic builds only (tools/row_timing.py)
+_LIB_PATH = os.environ.get("PM2L_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libpm2l_b200.so")
 
 PM2L_OK, PM2L_ERR_INVALID, PM2L_ERR_CUDA, PM2L_ERR_NOMEM, PM2L_ERR_NODEVICE = 0, -1, -2, -3, -4
 
@@ -52,6 +54,7 @@ SIGNATURES = {
                                      C.POINTER(_p)]),
     "pm2l_grid_plan_launch": (_i32, [_p, _p, _p, _p, _p, _p, _i32, _p]),
     "pm2l_grid_plan_info": (_i32, [_p, C.POINTER(_i64)]),
+    "pm2l_grid_plan_kernel": (_i32, [_p, _p, _i32]),
     "pm2l_grid_plan_destroy": (_i32, [_p]),
     "pm2l_nan_scan": (_i32, [_p, _i64, _p, _p]),
     "pm2l_grid_predict_all_curves": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64,
@@ -228,6 +231,13 @@ class GridPlan:
         check(self._lib.pm2l_grid_plan_launch(
             self.handle, ptr(out_lat), ptr(curve), ptr(blocks), ptr(waves), ptr(nan_stats),
             stages, stream_handle(stream)), "pm2l_grid_plan_launch")
+
+    def kernel_path(self, out_lat, verify: bool = False) -> int:
+        """0 sweep, 1 sweep + tie mask, 2 one-class closed form, 3 lookup."""
+        rc = self._lib.pm2l_grid_plan_kernel(self.handle, ptr(out_lat), int(verify))
+        if rc < 0:
+            check(rc, "pm2l_grid_plan_kernel")
+        return rc
 
     def close(self):
         if self.handle:

@@ -6,9 +6,11 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <thread>
 #include <vector>
 
 #include "../../include/pm2l.h"
@@ -312,6 +314,19 @@ int pm2l_grid_plan_info(const pm2l_grid_plan* p, int64_t* info) {
   return PM2L_OK;
 }
 
+int pm2l_grid_plan_kernel(const pm2l_grid_plan* p, const double* out_lat, int verify) {
+  if (!p) return fail(PM2L_ERR_INVALID, "null plan");
+  int32_t dummy = 0;
+  LaunchOut o{const_cast<double*>(out_lat), verify ? &dummy : nullptr};
+  return grid_kernel_path(p->tables->dev, p->grid, o);
+}
+
+#ifdef PM2L_TIMING
+int pm2l_debug_row_timing(unsigned long long* host, int n) {
+  return pm2l::row_timing_copy(host, n);
+}
+#endif
+
 int pm2l_grid_plan_destroy(pm2l_grid_plan* p) {
   if (!p) return PM2L_OK;
   {
@@ -414,13 +429,123 @@ uint64_t fnv(uint64_t h, const void* p, size_t n) {
   return h;
 }
 
+// Persistent host worker threads for the pinned-staging -> caller-buffer
+// copies of the drop-in's result (a single memcpy thread reaches a fraction
+// of the host's memory bandwidth; the caller's numpy buffer is pageable).
+class CopyPool {
+ public:
+  explicit CopyPool(int workers) {
+    for (int i = 0; i < workers; ++i) threads_.emplace_back([this, i] { run(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& th : threads_) th.join();
+  }
+  int parts() const { return int(threads_.size()) + 1; }
+  // memcpy(dst, src, n) split over the workers and the calling thread
+  void copy(void* dst, const void* src, size_t n) {
+    const int P = parts();
+    const size_t piece = ((n + P - 1) / P + 4095) & ~size_t(4095);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = static_cast<uint8_t*>(dst);
+      src_ = static_cast<const uint8_t*>(src);
+      n_ = n;
+      piece_ = piece;
+      pending_ = int(threads_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    part(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void part(int p) {
+    const size_t lo = std::min(n_, size_t(p) * piece_), hi = std::min(n_, lo + piece_);
+    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+  }
+  void run(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      part(i + 1);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  bool stop_ = false;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  uint8_t* dst_ = nullptr;
+  const uint8_t* src_ = nullptr;
+  size_t n_ = 0, piece_ = 0;
+};
+
+constexpr int kStageBufs = 3;
+constexpr size_t kStageChunk = size_t(4) << 20;  // bytes per D2H chunk
+
+struct SliceDevice {
+  DeviceBuf out;                    // device result
+  PinnedBuf stage[kStageBufs];      // pinned D2H staging ring
+  cudaEvent_t ready[kStageBufs] = {};
+  cudaStream_t stream = nullptr;
+};
+
 struct SliceCache {
   std::mutex mu;
   std::unordered_map<uint64_t, pm2l_tables*> tables;  // (content hash ^ device) -> staged
-  std::unordered_map<int, DeviceBuf> out;             // per device output buffers
-  std::unordered_map<int, cudaStream_t> stream;
+  std::unordered_map<int, SliceDevice> dev;
+  std::unique_ptr<CopyPool> pool;
 };
 SliceCache g_slice;
+
+// Device result -> pageable caller buffer: chunked D2H into a ring of pinned
+// buffers on `s`, each chunk copied out by the host pool while the next
+// chunks are in flight over PCIe.
+int drain_to_host(SliceDevice& sd, const double* d_out, double* out, size_t bytes) {
+  if (!g_slice.pool) {
+    const unsigned hc = std::thread::hardware_concurrency();
+    g_slice.pool.reset(new CopyPool(int(std::min(7u, hc > 1 ? hc - 1 : 0u))));
+  }
+  for (int i = 0; i < kStageBufs; ++i) {
+    PM2L_CUDA(sd.stage[i].reserve(kStageChunk));
+    if (!sd.ready[i]) PM2L_CUDA(cudaEventCreateWithFlags(&sd.ready[i], cudaEventDisableTiming));
+  }
+  const size_t n = (bytes + kStageChunk - 1) / kStageChunk;
+  auto issue = [&](size_t c) -> int {
+    const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    const int b = int(c % kStageBufs);
+    PM2L_CUDA(cudaMemcpyAsync(sd.stage[b].ptr, reinterpret_cast<const uint8_t*>(d_out) + off, len,
+                              cudaMemcpyDeviceToHost, sd.stream));
+    PM2L_CUDA(cudaEventRecord(sd.ready[b], sd.stream));
+    return PM2L_OK;
+  };
+  for (size_t c = 0; c < std::min<size_t>(n, kStageBufs); ++c)
+    if (int rc = issue(c)) return rc;
+  for (size_t c = 0; c < n; ++c) {
+    const int b = int(c % kStageBufs);
+    PM2L_CUDA(cudaEventSynchronize(sd.ready[b]));
+    const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    g_slice.pool->copy(reinterpret_cast<uint8_t*>(out) + off, sd.stage[b].ptr, len);
+    if (c + kStageBufs < n)
+      if (int rc = issue(c + kStageBufs)) return rc;
+  }
+  return PM2L_OK;
+}
 
 }  // namespace
 
@@ -478,19 +603,19 @@ int pm2l_predict_grid_slice(
       return rc;
     }
   }
-  cudaStream_t& s = g_slice.stream[device];
+  SliceDevice& sd = g_slice.dev[device];
+  cudaStream_t& s = sd.stream;
   if (!s) PM2L_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   const int64_t count = (b_hi - b_lo) * n_m * n_n * n_k;
   if (count < 0) return fail(PM2L_ERR_INVALID, "batch slice out of range");
   if (count == 0) return PM2L_OK;
   if (!out) return fail(PM2L_ERR_INVALID, "null out");
-  DeviceBuf& ob = g_slice.out[device];
-  PM2L_CUDA(ob.reserve(size_t(count) * sizeof(double)));
-  double* d_out = static_cast<double*>(ob.ptr);
+  PM2L_CUDA(sd.out.reserve(size_t(count) * sizeof(double)));
+  double* d_out = static_cast<double*>(sd.out.ptr);
   if (int rc = pm2l_grid_predict(t, batch_vals, n_batch, m_vals, n_m, n_vals, n_n, k_vals, n_k,
                                  b_lo, b_hi, d_out, nullptr, nullptr, nullptr, s))
     return rc;
-  PM2L_CUDA(cudaMemcpyAsync(out, d_out, size_t(count) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (int rc = drain_to_host(sd, d_out, out, size_t(count) * sizeof(double))) return rc;
   PM2L_CUDA(cudaStreamSynchronize(s));
   return PM2L_OK;
 }

@@ -18,6 +18,7 @@
 //                      one coalesced 8-byte store per batch value
 //   fixup_kernel       exact-record hits (take priority over nearest)
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -505,6 +506,429 @@ __global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g
   }
 }
 
+// ------------------------------------------------- one-class lookup path
+// The one-class argmin (nearest_one_class) splits into a k-only part and a
+// row-only part:
+//   case A  (mn(k) <= dmin): group = leftmost group with dk(g, k) <= dmin,
+//                            member = lastpos
+//   case B  (mn(k) >  dmin): group = gB(k), member = staircase(mn(k))
+// mn, gB and rank(k) (position of k in the descending order of mn inside its
+// k chunk) are k-only and come from the host (GridDev::kfast / mn_sorted).
+// Per (row, k chunk) one warp turns the row's staircase into cut points
+//   cut[s]  = #{ranks with mn >= sD[s]}  (s < len-1);  cut[len-1] = #{mn > dmin}
+//   kap[g]  = first k index at which group g lies left of log2 k AND is
+//             farther than dmin from it (monotone in k: a binary search;
+//             non-decreasing in g)
+// and expands them into two byte maps over the chunk
+//   rmap[rank] = staircase step of mn (case B) or 0xFF (case A)
+//   gmap[ik]   = #{g : kap[g] <= ik} = the case-A group
+// so resolving one k is three shared-memory lookups.  Every comparison is
+// the one nearest_one_class makes, on the same bits: the argmin is identical.
+//
+// Warp-autonomous: each warp builds its tile's state and then writes the
+// tile's points; many independent tiles are in flight per SM and no barrier
+// couples warps.
+constexpr int kRowWarps = 8;
+
+#ifdef PM2L_TIMING
+// diagnostic build only (tools/row_timing.py): per-tile phase timestamps
+__device__ unsigned long long g_row_dbg[16384 * 8];
+#define ROW_MARK(tile, i)                                                         \
+  do {                                                                            \
+    if (lane == 0 && (tile) < 16384) {                                            \
+      unsigned long long t_;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                      \
+      g_row_dbg[(tile) * 8 + (i)] = t_;                                           \
+    }                                                                             \
+  } while (0)
+#else
+#define ROW_MARK(tile, i) do {} while (0)
+#endif
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+// TMA bulk copy global -> shared (bytes: multiple of 16, both ends 16-aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__host__ __device__ constexpr uint32_t r16(int64_t b) { return uint32_t((b + 15) & ~int64_t(15)); }
+
+struct RowLaunch {
+  int tiles, nbs, nkc, kc;   // tiles = rows * nbs * nkc; k chunk length (even)
+  int seg;                   // byte-map bytes per lane (multiple of 16)
+  int ctas;
+  int off_bar, off_gcur, off_glk, off_clm, off_cln, off_wcp, off_kf, off_ms, off_kq, off_warp;
+  int w_sD, w_sP, w_cut, w_W, w_rmap, w_gmap, warp_bytes;
+  int64_t smem;
+};
+
+void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_k, RowLaunch& rl) {
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = o;
+    o = (o + bytes + 15) & ~int64_t(15);
+    return int(at);
+  };
+  rl.off_bar = take(16);
+  rl.off_gcur = take(8ll * t.R);
+  rl.off_glk = take(8ll * t.G);
+  rl.off_clm = take(8ll * t.CM);
+  rl.off_cln = take(8ll * t.CM);
+  rl.off_wcp = take(int64_t(sizeof(WcParam)) * t.NW);
+  rl.off_kf = take(stage_k ? 4ll * g.nK : 0);
+  rl.off_ms = take(stage_k ? 8ll * g.nK : 0);
+  rl.off_kq = take(stage_k ? 8ll * g.nK : 0);
+  rl.off_warp = int(o);
+  int64_t w = 0;
+  auto wtake = [&](int64_t bytes) {
+    const int64_t at = w;
+    w = (w + bytes + 15) & ~int64_t(15);
+    return int(at);
+  };
+  rl.seg = ((rl.kc + 511) / 512) * 16;
+  rl.w_sD = wtake(8ll * t.CM);
+  rl.w_sP = wtake(4ll * t.CM);
+  rl.w_cut = wtake(4ll * (t.CM + t.G + 1));
+  rl.w_W = wtake(8ll * t.NW * nb);
+  rl.w_rmap = wtake(32ll * rl.seg);
+  rl.w_gmap = wtake(32ll * rl.seg);
+  rl.warp_bytes = int(w);
+  rl.smem = o + kRowWarps * w;
+}
+
+// Two byte maps over [0, 32*seg), built in one interleaved pass:
+//   map_j[r] = #{s < ncut_j : cut_j[s] <= r}, and 0xFF from r = ff_j on
+//   (ff_j < 0: never).
+// Difference array (shared-memory byte increments at each cut) + prefix sum:
+// SIMD within each word (x*0x01010101 sums the bytes below each byte), a
+// running carry across the lane's segment, and a warp scan across lanes.
+// Counts stay < 256 (ncut <= 255).
+template <int SEGW>  // u32 words per lane
+__device__ __forceinline__ void build_count_maps(uint8_t* map0, const int32_t* cut0, int ncut0,
+                                                 int ff0, uint8_t* map1, const int32_t* cut1,
+                                                 int ncut1, int lane) {
+  uint32_t* mw0 = reinterpret_cast<uint32_t*>(map0) + lane * SEGW;
+  uint32_t* mw1 = reinterpret_cast<uint32_t*>(map1) + lane * SEGW;
+#pragma unroll
+  for (int q = 0; q < SEGW; q += 4) {
+    *reinterpret_cast<uint4*>(mw0 + q) = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(mw1 + q) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  __syncwarp();
+  constexpr int kLim = 32 * SEGW * 4;
+  for (int s = lane; s < max(ncut0, ncut1); s += 32) {
+    if (s < ncut0) {
+      const int e = cut0[s];
+      if (e < kLim) atomicAdd(reinterpret_cast<uint32_t*>(map0) + (e >> 2), 1u << (8 * (e & 3)));
+    }
+    if (s < ncut1) {
+      const int e = cut1[s];
+      if (e < kLim) atomicAdd(reinterpret_cast<uint32_t*>(map1) + (e >> 2), 1u << (8 * (e & 3)));
+    }
+  }
+  __syncwarp();
+  uint32_t w0[SEGW], w1[SEGW];
+#pragma unroll
+  for (int q = 0; q < SEGW; q += 4) {
+    const uint4 a = *reinterpret_cast<const uint4*>(mw0 + q);
+    const uint4 b = *reinterpret_cast<const uint4*>(mw1 + q);
+    w0[q] = a.x; w0[q + 1] = a.y; w0[q + 2] = a.z; w0[q + 3] = a.w;
+    w1[q] = b.x; w1[q + 1] = b.y; w1[q + 2] = b.z; w1[q + 3] = b.w;
+  }
+  uint32_t run0 = 0, run1 = 0;
+#pragma unroll
+  for (int q = 0; q < SEGW; ++q) {
+    const uint32_t p0 = w0[q] * 0x01010101u, p1 = w1[q] * 0x01010101u;
+    w0[q] = p0 + run0 * 0x01010101u;
+    w1[q] = p1 + run1 * 0x01010101u;
+    run0 += p0 >> 24;
+    run1 += p1 >> 24;
+  }
+  uint32_t e0 = run0, e1 = run1;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t o0 = __shfl_up_sync(0xFFFFFFFFu, e0, off);
+    const uint32_t o1 = __shfl_up_sync(0xFFFFFFFFu, e1, off);
+    if (lane >= off) { e0 += o0; e1 += o1; }
+  }
+  e0 -= run0;
+  e1 -= run1;
+  const int r0 = lane * SEGW * 4;
+#pragma unroll
+  for (int q = 0; q < SEGW; ++q) {
+    w0[q] += e0 * 0x01010101u;
+    w1[q] += e1 * 0x01010101u;
+    if (ff0 >= 0) {
+      const int sh = ff0 - r0 - 4 * q;
+      w0[q] |= sh <= 0 ? 0xFFFFFFFFu : sh >= 4 ? 0u : (0xFFFFFFFFu << (8 * sh));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < SEGW; q += 4) {
+    *reinterpret_cast<uint4*>(mw0 + q) = make_uint4(w0[q], w0[q + 1], w0[q + 2], w0[q + 3]);
+    *reinterpret_cast<uint4*>(mw1 + q) = make_uint4(w1[q], w1[q + 1], w1[q + 2], w1[q + 3]);
+  }
+}
+
+__device__ __forceinline__ uint64_t ceil_div_w(const WcParam& p, int j, uint64_t a, uint64_t d) {
+  const uint64_t num = a + d - 1;
+  const uint32_t s = p.ds[j];
+  if ((s >> 16) && num <= 0xFFFFFFFFull) {
+    const uint32_t n32 = uint32_t(num);
+    const uint32_t q = __umulhi(p.dm[j], n32);
+    return uint64_t((q + ((n32 - q) >> (s & 0xFF))) >> ((s >> 8) & 0xFF));
+  }
+  return num / d;
+}
+
+template <int NB, bool STAGE, int SEGW>
+__global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t, GridDev g,
+                                                                    RowLaunch rl,
+                                                                    const double* __restrict__ base_tab,
+                                                                    LaunchOut out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int2* gcur = reinterpret_cast<int2*>(smem + rl.off_gcur);
+  double* glk = reinterpret_cast<double*>(smem + rl.off_glk);
+  double* clm = reinterpret_cast<double*>(smem + rl.off_clm);
+  double* cln = reinterpret_cast<double*>(smem + rl.off_cln);
+  WcParam* wcp = reinterpret_cast<WcParam*>(smem + rl.off_wcp);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + rl.off_bar);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  ROW_MARK(blockIdx.x * kRowWarps + warp, 0);
+  const uint32_t* kfs = g.kfast;
+  const uint64_t* ms = g.mn_sorted;
+  const double* kq = g.logK;
+  if (STAGE) {
+    kfs = reinterpret_cast<const uint32_t*>(smem + rl.off_kf);
+    ms = reinterpret_cast<const uint64_t*>(smem + rl.off_ms);
+    kq = reinterpret_cast<const double*>(smem + rl.off_kq);
+  }
+  // prologue: every CTA-constant table arrives by TMA bulk copies on one
+  // mbarrier (one round trip, no register staging)
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t nk = uint32_t(g.nK);
+    uint32_t total = r16(8ll * t.R) + r16(8ll * t.G) + 2 * r16(8ll * t.CM) +
+                     r16(int64_t(sizeof(WcParam)) * t.NW);
+    if (STAGE) total += r16(4ll * nk) + 2 * r16(8ll * nk);
+    mbar_expect_tx(bar, total);
+    bulk_g2s(gcur, t.g_cw, r16(8ll * t.R), bar);
+    bulk_g2s(glk, t.grp_lk, r16(8ll * t.G), bar);
+    bulk_g2s(clm, t.cls_lm, r16(8ll * t.CM), bar);
+    bulk_g2s(cln, t.cls_ln, r16(8ll * t.CM), bar);
+    bulk_g2s(wcp, t.wcp, r16(int64_t(sizeof(WcParam)) * t.NW), bar);
+    if (STAGE) {
+      bulk_g2s(smem + rl.off_kf, g.kfast, r16(4ll * nk), bar);
+      bulk_g2s(smem + rl.off_ms, g.mn_sorted, r16(8ll * nk), bar);
+      bulk_g2s(smem + rl.off_kq, g.logK, r16(8ll * nk), bar);
+    }
+  }
+  __syncthreads();  // mbarrier initialised before anyone waits on it
+  mbar_wait(bar, 0);
+  uint8_t* wb = smem + rl.off_warp + warp * rl.warp_bytes;
+  uint64_t* sD = reinterpret_cast<uint64_t*>(wb + rl.w_sD);
+  int32_t* sP = reinterpret_cast<int32_t*>(wb + rl.w_sP);
+  int32_t* cut = reinterpret_cast<int32_t*>(wb + rl.w_cut);
+  double* W = reinterpret_cast<double*>(wb + rl.w_W);
+  uint8_t* rmap = wb + rl.w_rmap;
+  uint8_t* gmap = wb + rl.w_gmap;
+  const int nN = int(g.nN), nK = int(g.nK), G = t.G, CM = t.CM, NW = t.NW;
+  const int64_t plane = g.nM * g.nN * g.nK;
+  bool waited = false;
+  for (int tile = blockIdx.x * kRowWarps + warp; tile < rl.tiles;
+       tile += gridDim.x * kRowWarps) {
+    const int kcx = tile % rl.nkc, rs = tile / rl.nkc;
+    const int slab = rs % rl.nbs, row = rs / rl.nbs;
+    const int im = row / nN, jn = row - im * nN;
+    const int k0 = kcx * rl.kc, kc = min(rl.kc, nK - k0);
+    const double qm = g.logM[im], qn = g.logN[jn];
+    const uint64_t m = g.M[im], n = g.N[jn];
+    ROW_MARK(tile, 1);
+    // ---- staircase: prefix minimum of D_j = max(|lm_j-qm|, |ln_j-qn|)
+    uint64_t dmin = ~0ull;
+    int len = 0, lastpos = 0;
+    for (int b0 = 0; b0 < CM; b0 += 32) {
+      const int j = b0 + lane;
+      const uint64_t d = j < CM ? umax64(abs_bits(__dsub_rn(clm[j], qm)), abs_bits(__dsub_rn(cln[j], qn)))
+                                : ~0ull;
+      uint64_t pm = d;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
+        if (lane >= off && o < pm) pm = o;
+      }
+      uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
+      if (lane == 0) excl = ~0ull;
+      if (dmin < excl) excl = dmin;
+      const bool rec = j < CM && d < excl;
+      const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
+      if (rec) {
+        const int pos = len + __popc(mask & ((1u << lane) - 1u));
+        sD[pos] = d;
+        sP[pos] = j;
+      }
+      if (mask) lastpos = b0 + 31 - __clz(mask);
+      len += __popc(mask);
+      const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
+      if (tail < dmin) dmin = tail;
+    }
+    ROW_MARK(tile, 2);
+    // ---- wave-scale table W[wave class][ib] of this (m, n) and batch slab
+    {
+      uint64_t bb[NB];
+#pragma unroll
+      for (int ib = 0; ib < NB; ++ib) bb[ib] = g.B[g.b_lo + slab * NB + ib];
+      for (int wc = lane; wc < NW; wc += 32) {
+        const WcParam p = wcp[wc];
+        const uint64_t tmn = ceil_div_w(p, 0, m, p.tm) * ceil_div_w(p, 1, n, p.tn) * p.sk;
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib) {
+          const double w = __ull2double_rn(ceil_div_w(p, 2, bb[ib] * tmn, p.bpw));
+          W[wc * NB + ib] = p.rw == 1.0 ? w : __ddiv_rn(w, p.rw);
+        }
+      }
+    }
+    __syncwarp();
+    ROW_MARK(tile, 3);
+    // ---- cut points: binary searches inside the k chunk
+    //   cut[s] (s < len-1): #{ranks with mn >= sD[s]}; cut[len-1]: #{mn > dmin}
+    //   cut[len + g]: first k index where group g is left of log2 k and
+    //                 farther than dmin from it
+    // fixed-trip branch-free binary searches, both kinds in one loop
+    // (lanes never diverge): i < len: rank cuts; i >= len: group cuts
+    //   rank cut: #{ranks r: mn(r) >= sD[i]} (i == len-1: > dmin); mn descends
+    //   group cut: #{k: NOT (group left of log2 k and farther than dmin)}
+    int top = 1;
+    while (top * 2 <= kc) top *= 2;
+    for (int i = lane; i < len + G; i += 32) {
+      const bool rk = i < len, strict = i == len - 1;
+      const int gg = rk ? 0 : i - len;
+      const uint64_t x = sD[rk ? i : 0];
+      const double lk = glk[gg];
+      int lo = 0;
+      for (int step = top; step; step >>= 1) {
+        const int r = k0 + min(lo + step, kc) - 1;
+        const uint64_t v = ms[r];
+        const bool far = int(kfs[r] >> 24) > gg && abs_bits(__dsub_rn(lk, kq[r])) > dmin;
+        const bool adv = rk ? (v > x || (!strict && v == x)) : !far;
+        lo += (lo + step <= kc && adv) ? step : 0;
+      }
+      cut[i] = lo;
+    }
+    __syncwarp();
+    ROW_MARK(tile, 4);
+    build_count_maps<SEGW>(rmap, cut, len - 1, cut[len - 1], gmap, cut + len, G, lane);
+    __syncwarp();
+    ROW_MARK(tile, 5);
+    if (!waited) {
+      pdl_wait();  // base table complete and visible
+      waited = true;
+    }
+    ROW_MARK(tile, 6);
+    // ---- points: two adjacent k per lane (16-byte stores), U pairs in flight
+    double* const obase = out.lat + int64_t(slab * NB) * plane + int64_t(row) * nK + k0;
+    const double* const bbase = base_tab + k0;
+    const int nP = kc >> 1;
+    auto lookup = [&](uint32_t kf, int ikl) -> int2 {
+      const uint32_t sb = rmap[kf & 0xFFFFu];
+      const bool a = sb == 0xFFu;
+      const int gg = a ? int(gmap[ikl]) : int((kf >> 16) & 0xFFu);
+      const int pos = a ? lastpos : sP[sb];
+      return gcur[gg * CM + pos];  // one class: group g's members at g * CM
+    };
+    constexpr int U = 4;
+    for (int q0 = 0; q0 < nP; q0 += 32 * U) {  // warp-uniform trip count (__all_sync)
+      const int p0 = q0 + lane;
+      int2 v[U][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = min(p0 + 32 * u, nP - 1);
+        const uint2 kf = *reinterpret_cast<const uint2*>(kfs + k0 + 2 * p);
+        v[u][0] = lookup(kf.x, 2 * p);
+        v[u][1] = lookup(kf.y, 2 * p + 1);
+      }
+      bool all_ok = true;
+#pragma unroll
+      for (int u = 0; u < U; ++u) all_ok = all_ok && v[u][0].x >= 0 && v[u][1].x >= 0;
+      if (__all_sync(0xFFFFFFFFu, all_ok)) {
+        double bv[U][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int p = min(p0 + 32 * u, nP - 1);
+          bv[u][0] = bbase[v[u][0].x * nK + 2 * p];
+          bv[u][1] = bbase[v[u][1].x * nK + 2 * p + 1];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int p = p0 + 32 * u;
+          if (p >= nP) break;
+          double* o = obase + 2 * p;
+          const double* w0 = W + v[u][0].y * NB;
+          const double* w1 = W + v[u][1].y * NB;
+#pragma unroll
+          for (int ib = 0; ib < NB; ib += (NB >= 2 ? 2 : 1)) {
+            double a0, a1, b0, b1;
+            if (NB >= 2) {
+              const double2 x = *reinterpret_cast<const double2*>(w0 + ib);
+              const double2 y = *reinterpret_cast<const double2*>(w1 + ib);
+              a0 = x.x; a1 = x.y; b0 = y.x; b1 = y.y;
+            } else {
+              a0 = w0[ib]; b0 = w1[ib]; a1 = b1 = 0.0;
+            }
+            *reinterpret_cast<double2*>(o + ib * plane) =
+                make_double2(__dmul_rn(bv[u][0], a0), __dmul_rn(bv[u][1], b0));
+            if (NB >= 2)
+              *reinterpret_cast<double2*>(o + (ib + 1) * plane) =
+                  make_double2(__dmul_rn(bv[u][0], a1), __dmul_rn(bv[u][1], b1));
+          }
+        }
+      } else {
+        // some k resolves to a record without a curve: NaN + statistics
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int p = p0 + 32 * u;
+          if (p >= nP) break;
+          double* o = obase + 2 * p;
+          const bool ok0 = v[u][0].x >= 0, ok1 = v[u][1].x >= 0;
+          const double b0 = ok0 ? bbase[v[u][0].x * nK + 2 * p] : 0.0;
+          const double b1 = ok1 ? bbase[v[u][1].x * nK + 2 * p + 1] : 0.0;
+          if (!(ok0 && ok1) && out.nan_stats) {
+            atomicMin(out.nan_stats, (unsigned long long)(o - out.lat + (ok0 ? 1 : 0)));
+            atomicAdd(out.nan_stats + 1, (unsigned long long)(NB * (2 - ok0 - ok1)));
+          }
+          const double* w0 = W + (ok0 ? v[u][0].y : 0) * NB;
+          const double* w1 = W + (ok1 ? v[u][1].y : 0) * NB;
+#pragma unroll
+          for (int ib = 0; ib < NB; ++ib)
+            *reinterpret_cast<double2*>(o + ib * plane) =
+                make_double2(ok0 ? __dmul_rn(b0, w0[ib]) : qnan(), ok1 ? __dmul_rn(b1, w1[ib]) : qnan());
+        }
+      }
+    }
+    __syncwarp();  // the warp's state buffers are rewritten by the next tile
+    ROW_MARK(tile, 7);
+  }
+  if (!waited) pdl_wait();
+}
+
 // Exact-record hits take priority over the nearest result (_kernels.pyx:107-110).
 // `fixval` (nullable) holds their latencies, precomputed by the base-table
 // kernel off the critical path.
@@ -653,6 +1077,73 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   return gl;
 }
 
+// The one-class lookup kernel applies to latency-only launches of GEMM grids
+// whose tables form one member class, with an even k axis (16-byte pair
+// stores into a 16-byte aligned output) and u8-sized staircases; rl.tiles
+// == 0 otherwise.
+RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
+                    const LaunchOut& out, int* nb_out) {
+  RowLaunch rl{};
+  const int64_t nb = g.b_hi - g.b_lo;
+  if (out.curve || gl.near != 2 || !t.all_gemm || !g.kfast || g.nK % 2 != 0 || nb <= 0 ||
+      (reinterpret_cast<uintptr_t>(out.lat) & 15) != 0 || t.CM > 254 || t.CM < 1 ||
+      g.nM * g.nN > 0x7FFFFFFFll)
+    return rl;
+  int NB = 8;
+  while (nb % NB) NB >>= 1;
+  rl.nbs = int(nb / NB);
+  rl.kc = int(std::min<int64_t>(g.nK, kKChunk));
+  rl.nkc = int((g.nK + rl.kc - 1) / rl.kc);
+  const bool stage_k = g.nK <= kKChunk;
+  const int64_t tiles = g.nM * g.nN * rl.nbs * rl.nkc;
+  if (tiles > 0x7FFFFFFFll || t.G + t.CM > 4096) return rl;
+  row_layout(t, g, NB, stage_k, rl);
+  if (rl.smem > 200 * 1024) return rl;
+  rl.tiles = int(tiles);
+  rl.ctas = int(std::min<int64_t>((tiles + kRowWarps - 1) / kRowWarps, 148 * 3));
+  if (const char* e = std::getenv("PM2L_ROW_CTAS")) {  // tuning experiments only
+    const int v = std::atoi(e);
+    if (v > 0) rl.ctas = std::min(rl.ctas, v);
+  }
+  *nb_out = NB;
+  return rl;
+}
+
+template <int NB, bool STAGE, int SEGW>
+cudaError_t launch_rows_k(const TablesDev& t, const GridDev& g, const RowLaunch& rl,
+                          const double* base, const LaunchOut& out, cudaStream_t s) {
+  auto* fn = grid_row_kernel<NB, STAGE, SEGW>;
+  if (rl.smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rl.smem));
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(rl.ctas));
+  cfg.blockDim = dim3(32 * kRowWarps);
+  cfg.dynamicSmemBytes = size_t(rl.smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, t, g, rl, base, out);
+}
+
+template <int NB>
+cudaError_t launch_rows_t(const TablesDev& t, const GridDev& g, const RowLaunch& rl,
+                          const double* base, const LaunchOut& out, cudaStream_t s) {
+  const bool stage = g.nK <= kKChunk;
+  if (rl.seg == 16)
+    return stage ? launch_rows_k<NB, true, 4>(t, g, rl, base, out, s)
+                 : launch_rows_k<NB, false, 4>(t, g, rl, base, out, s);
+  if (rl.seg == 32)
+    return stage ? launch_rows_k<NB, true, 8>(t, g, rl, base, out, s)
+                 : launch_rows_k<NB, false, 8>(t, g, rl, base, out, s);
+  return stage ? launch_rows_k<NB, true, 16>(t, g, rl, base, out, s)
+               : launch_rows_k<NB, false, 16>(t, g, rl, base, out, s);
+}
+
 bool grid_dims_ok(const GridDev& g, const GridLaunch& gl) {
   return g.nM * g.nN * gl.nbs <= 0x7FFFFFFFll && gl.nbs <= 65535 && g.nK <= 0x3FFFFFFFll &&
          g.nB <= 0x7FFFFFFFll;
@@ -698,6 +1189,12 @@ int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g) {
   return int64_t(t.C) * g.nK + g.n_fix;  // base table, then exact-hit values
 }
 
+int grid_kernel_path(const TablesDev& t, const GridDev& g, const LaunchOut& out) {
+  const GridLaunch gl = plan_grid(t, g, false);
+  int nb = 0;
+  return plan_rows(t, g, gl, out, &nb).tiles > 0 ? 3 : gl.near;
+}
+
 int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, double* ws,
                 int64_t ws_elems, const LaunchOut& out, void* stream, int stages) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -715,7 +1212,14 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   if ((stages & kStageBase) && (t.C > 0 || fixval)) launch_base_table(t, g, ws, fixval, s);
   const bool v = out.curve != nullptr;
   cudaError_t e = cudaSuccess;
-  if (stages & kStageGrid) {
+  int row_nb = 0;
+  const RowLaunch rl = plan_rows(t, g, gl, out, &row_nb);
+  if ((stages & kStageGrid) && rl.tiles > 0) {
+    e = row_nb == 8   ? launch_rows_t<8>(t, g, rl, base, out, s)
+        : row_nb == 4 ? launch_rows_t<4>(t, g, rl, base, out, s)
+        : row_nb == 2 ? launch_rows_t<2>(t, g, rl, base, out, s)
+                      : launch_rows_t<1>(t, g, rl, base, out, s);
+  } else if (stages & kStageGrid) {
     if (v) {
       e = gl.mode == 0 ? launch_grid_t<true, 0>(t, g, gl, base, out, s)
           : gl.mode == 1 ? launch_grid_t<true, 1>(t, g, gl, base, out, s)
@@ -753,6 +1257,12 @@ int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* ws, dou
   all_curves_kernel<<<grid, kThreads, smem, s>>>(t, g, gl, ws, out);
   return int(cudaGetLastError());
 }
+
+#ifdef PM2L_TIMING
+int row_timing_copy(unsigned long long* host, int n) {
+  return int(cudaMemcpyFromSymbol(host, g_row_dbg, sizeof(unsigned long long) * size_t(n)));
+}
+#endif
 
 int launch_nan_scan(const double* v, int64_t n, unsigned long long* first, void* stream) {
   if (n == 0) return 0;

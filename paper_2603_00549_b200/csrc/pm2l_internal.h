@@ -20,6 +20,14 @@ namespace pm2l {
 // of D_i over the candidates in scan order (built per (m, n) row in shared
 // memory).  Original scan indices are kept so ties break exactly as the
 // reference's strict '<' scan (_kernels.pyx:29-47).
+// Wave-class parameters (grid_row_kernel's W table inputs), one per class.
+struct alignas(16) WcParam {
+  uint64_t tm, tn, sk, bpw;
+  double rw;        // ref_waves
+  uint32_t dm[3];   // u32 division magic for tm, tn, bpw (common.cuh ceil_div_c)
+  uint32_t ds[3];
+};
+
 struct TablesDev {
   int32_t R = 0;        // candidate records
   int32_t C = 0;        // curves
@@ -56,6 +64,8 @@ struct TablesDev {
   const int32_t* g_idx = nullptr;    // original scan index
   const int32_t* cand_curve = nullptr; // by ORIGINAL index [R]
   const int32_t* g_curve = nullptr;    // curve of each candidate in GROUP order [R]
+  const int32_t* g_cw = nullptr;       // [2R] (curve, wave class) in GROUP order
+  const WcParam* wcp = nullptr;        // [NW]
   // groups [G]
   const double* grp_lk = nullptr;
   const int32_t* grp_start = nullptr;
@@ -76,6 +86,10 @@ struct TablesDev {
   const int32_t* ex_curve = nullptr;
   const int32_t* ex_rec = nullptr;    // position in the caller's exact arrays
 };
+
+// k chunk of the one-class lookup kernel: ranks of the per-k distance are
+// taken inside chunks of this many k values (one warp's byte maps)
+constexpr int kKChunk = 2048;
 
 // Per-k sweep info, 16 B (one 128-bit load in the grid kernel).
 struct alignas(16) KInfo {
@@ -105,6 +119,14 @@ struct GridDev {
   const double* logK = nullptr;
   // per k: {log2 k, sweep start = #groups with grp_lk < log2 k}, 16 B each
   const KInfo* kinfo = nullptr;
+  // one-class lookup path (null unless 1 <= G <= 255 and nK <= 65535):
+  // kfast[ik] = rank(ik) | gB(ik) << 16 | start(ik) << 24, where mn(ik) =
+  // distance from log2 k to the nearest k-group, gB = leftmost group
+  // attaining it, rank = position in the stable descending order of mn
+  // within ik's chunk of kKChunk k values; mn_sorted[chunk start + rank] =
+  // mn as ordered |double| bits
+  const uint32_t* kfast = nullptr;
+  const uint64_t* mn_sorted = nullptr;
   // exact-hit fix-ups: slice-relative flat index + coordinates + curve
   int64_t n_fix = 0;
   const int64_t* fix_pos = nullptr;
@@ -153,6 +175,10 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t max_group,
                 double* workspace, int64_t workspace_elems, const LaunchOut& out,
                 void* stream, int stages = kStageAll);
 int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g);
+int grid_kernel_path(const TablesDev& t, const GridDev& g, const LaunchOut& out);
+#ifdef PM2L_TIMING
+int row_timing_copy(unsigned long long* host, int n);  // diagnostic build only
+#endif
 int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* workspace,
                            double* out, void* stream);
 int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n,

@@ -37,7 +37,11 @@ class Blob {
   }
   template <class T>
   const T* add(const std::vector<T>& v) { return add(v.data(), v.size()); }
-  std::vector<uint8_t>& bytes() { return bytes_; }
+  // trailing slack: 16-byte bulk copies of the last section may read past it
+  std::vector<uint8_t>& bytes() {
+    bytes_.resize(((bytes_.size() + 255) & ~size_t(255)) + 256);
+    return bytes_;
+  }
 
  private:
   std::vector<uint8_t> bytes_;
@@ -204,6 +208,19 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
       wc_of[c] = it->second;
     }
   }
+  std::vector<int32_t> g_cw(2 * R);
+  for (int64_t p = 0; p < R; ++p) {
+    g_cw[2 * p] = g_curve[p];
+    g_cw[2 * p + 1] = g_curve[p] >= 0 ? wc_of[g_curve[p]] : -1;
+  }
+  std::vector<WcParam> wcp(wc_rep.size());
+  for (size_t w = 0; w < wc_rep.size(); ++w) {
+    const int32_t c = wc_rep[w];
+    WcParam& q = wcp[w];
+    q.tm = v->tile_m[c]; q.tn = v->tile_n[c]; q.sk = v->split_k[c]; q.bpw = v->blocks_per_wave[c];
+    q.rw = v->ref_waves[c];
+    for (int j = 0; j < 3; ++j) { q.dm[j] = dv_m[3 * c + j]; q.ds[j] = dv_s[3 * c + j]; }
+  }
   std::vector<int32_t> s_off(C + 1);
   for (int64_t c = 0; c <= C; ++c) s_off[c] = int32_t(v->sample_offsets[c]);
   std::vector<uint8_t> rowblock(C);
@@ -244,6 +261,8 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.g_idx = blob.add(g_idx);
   t.cand_curve = blob.add(cand_curve);
   t.g_curve = blob.add(g_curve);
+  t.g_cw = blob.add(g_cw);
+  t.wcp = blob.add(wcp);
   t.grp_lk = blob.add(grp_lk);
   t.grp_start = blob.add(grp_start);
   t.grp_size = blob.add(grp_size);
@@ -275,6 +294,7 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.g_lm = shift(o.g_lm, base); t.g_ln = shift(o.g_ln, base);
   t.g_idx = shift(o.g_idx, base); t.cand_curve = shift(o.cand_curve, base);
   t.g_curve = shift(o.g_curve, base);
+  t.g_cw = shift(o.g_cw, base); t.wcp = shift(o.wcp, base);
   t.grp_lk = shift(o.grp_lk, base); t.grp_start = shift(o.grp_start, base);
   t.grp_size = shift(o.grp_size, base); t.grp_class = shift(o.grp_class, base);
   t.cls_start = shift(o.cls_start, base); t.cls_size = shift(o.cls_size, base);
@@ -307,6 +327,52 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   std::vector<KInfo> kinfo(nK);
   for (int64_t i = 0; i < nK; ++i)
     kinfo[i] = {logs[2][i], int32_t(std::lower_bound(glk, glk + tt.G, logs[2][i]) - glk), 0};
+
+  // k-only part of the one-class nearest argmin (grid.cu, lookup path): per
+  // k, the distance mn(k) from log2 k to the nearest k-group, the leftmost
+  // group attaining it (gB), and rank(k) in the stable descending order of
+  // mn.  A row's cut points are thresholds on that order.  Same IEEE
+  // subtraction and |.| as the device (host double, no contraction).
+  std::vector<uint32_t> kfast;
+  std::vector<uint64_t> mn_sorted;
+  const bool fast_ok = tt.G >= 1 && tt.G <= 255 && nK >= 1 && nK <= 65535;
+  if (fast_ok) {
+    const int G = tt.G;
+    std::vector<uint64_t> mn(nK);
+    std::vector<int32_t> gB(nK);
+    auto dk = [&](int g, double qk) {
+      const double d = glk[g] - qk;
+      uint64_t u;
+      std::memcpy(&u, &d, 8);
+      return u & 0x7FFFFFFFFFFFFFFFull;
+    };
+    for (int64_t i = 0; i < nK; ++i) {
+      const double qk = kinfo[i].qk;
+      const int start = kinfo[i].start;
+      const uint64_t dkL = start > 0 ? dk(start - 1, qk) : ~0ull;
+      const uint64_t dkR = start < G ? dk(start, qk) : ~0ull;
+      mn[i] = std::min(dkL, dkR);
+      int g = start;
+      if (start > 0 && dkL == mn[i]) {
+        g = start - 1;
+        while (g > 0 && dk(g - 1, qk) == mn[i]) --g;
+      }
+      gB[i] = g;
+    }
+    kfast.resize(nK);
+    mn_sorted.resize(nK);
+    for (int64_t k0 = 0; k0 < nK; k0 += kKChunk) {
+      const int64_t k1 = std::min<int64_t>(nK, k0 + kKChunk);
+      std::vector<int32_t> ord(k1 - k0);
+      std::iota(ord.begin(), ord.end(), int32_t(k0));
+      std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return mn[a] > mn[b]; });
+      for (int64_t r = 0; r < k1 - k0; ++r) {
+        const int32_t i = ord[r];
+        mn_sorted[k0 + r] = mn[i];
+        kfast[i] = uint32_t(r) | (uint32_t(gB[i]) << 16) | (uint32_t(kinfo[i].start) << 24);
+      }
+    }
+  }
 
   // exact-hit fix-ups: every grid point whose (b, m, n, k) equals a recorded
   // shape takes the recorded kernel (_kernels.pyx:107-110) instead of the
@@ -383,6 +449,8 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   g.logN = blob.add(logs[1]);
   g.logK = blob.add(logs[2]);
   g.kinfo = blob.add(kinfo);
+  g.kfast = fast_ok ? blob.add(kfast) : nullptr;
+  g.mn_sorted = fast_ok ? blob.add(mn_sorted) : nullptr;
   g.n_fix = int64_t(fix_pos.size());
   g.fix_pos = blob.add(fix_pos);
   g.fix_coord = blob.add(fix_coord);
@@ -399,6 +467,10 @@ GridDev rebase(const GridDev& o, const void* base) {
   g.B = shift(o.B, base); g.M = shift(o.M, base); g.N = shift(o.N, base);
   g.K = shift(o.K, base); g.logM = shift(o.logM, base); g.logN = shift(o.logN, base);
   g.logK = shift(o.logK, base); g.kinfo = shift(o.kinfo, base);
+  if (o.kfast) {
+    g.kfast = shift(o.kfast, base);
+    g.mn_sorted = shift(o.mn_sorted, base);
+  }
   g.fix_pos = shift(o.fix_pos, base);
   g.fix_coord = shift(o.fix_coord, base); g.fix_curve = shift(o.fix_curve, base);
   g.fixr_off = shift(o.fixr_off, base); g.fixr = shift(o.fixr, base);

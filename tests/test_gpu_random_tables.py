@@ -117,3 +117,52 @@ def test_random_tables_grid(gpu, seed, R, C, nkv, rowblock, lattice):
     assert np.array_equal(got[4], ref[4])
     assert np.array_equal(got[5].view(np.uint64), ref[5].view(np.uint64))
     assert dt.groups == len(np.unique(t["log_k"]))
+
+
+@pytest.mark.parametrize("seed,R,C,nkv,nb,nm", [
+    (11, 540, 60, 9, 4, 40), (12, 90, 6, 9, 8, 36), (13, 400, 12, 40, 1, 12),
+    (14, 200, 20, 20, 2, 30), (15, 60, 4, 5, 4, 40), (16, 300, 9, 3, 8, 35)])
+def test_lookup_path_random_lattice(gpu, seed, R, C, nkv, nb, nm):
+    """One-member-class tables (every (b, m, n) recorded at every k), an even
+    k axis and full 1/2/4/8-value batch slabs: the one-class lookup kernel
+    (kernel path 3) against the oracle, bit for bit, plus NaN statistics."""
+    import torch
+    from paper_2603_00549_b200 import _native
+    rng = np.random.default_rng(seed)
+    t, pm, pn, pk = random_tables(rng, R, C, nkv, lattice=True)
+    dt = _native.DeviceTables(t, 0)
+    B = np.array([1, 2, 3, 4, 5, 7, 8, 9][:nb], np.uint64)
+    h = nm // 2
+    M = np.array(sorted(set(rng.choice(pm, h).tolist()) | set(rng.integers(1, 9000, nm - h).tolist())), np.uint64)
+    N = np.array(sorted(set(rng.choice(pn, h).tolist()) | set(rng.integers(1, 9000, nm - h).tolist())), np.uint64)
+    K = sorted(set(pk.tolist()) | set((pk + 1).tolist()) | set(rng.integers(1, 40000, 160).tolist()))
+    K = np.array(K[:len(K) // 2 * 2], np.uint64)
+    plan = _native.GridPlan(dt, (B, M, N, K))
+    dev = torch.device("cuda")
+    lat = torch.empty(plan.cardinality, dtype=torch.float64, device=dev)
+    assert plan.kernel_path(lat) == 3
+    stats = torch.tensor([-1, 0, 0], dtype=torch.int64, device=dev)
+    plan.launch(lat, nan_stats=stats)
+    o_lat, *_ = oracle.grid(t, (B, M, N, K), use_coords=True)
+    got = lat.cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), o_lat.view(np.uint64))
+    nan = np.isnan(o_lat)
+    st = stats.cpu().numpy()
+    assert st[1] == nan.sum()
+    if st[2] == 0:
+        assert st[0] == (int(np.argmax(nan)) if nan.any() else -1)
+
+
+def test_lookup_path_used_for_bench_grid(gpu):
+    """The C2 bench grid runs on the lookup kernel."""
+    import torch
+    import bench
+    from paper_2603_00549_b200 import _native
+    from paper_2603_00549_b200.compute import WaveModel
+    from paper_2603_00549_b200.nascache import PreparedGrid
+    ds = bench.load_bf16()
+    prep = PreparedGrid(ds, bench.grid_for(1), WaveModel(ds.device.sm_count))
+    plan = _native.GridPlan(prep.device_tables(0), prep.axis_arrays())
+    lat = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
+    assert plan.kernel_path(lat) == 3
+    assert plan.kernel_path(lat, verify=True) == 2

@@ -5,7 +5,7 @@ set -e
 cd "$(dirname "$0")/.."
 TAG=${1:-run}
 python -m paper_2603_00549_b200._build
-timeout 2400 /usr/local/graft/bin/gpurun --timeout 1500 -- "timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo rc=\$? >> gpurun_out/pytest_gpu.log; timeout 400 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; timeout 600 ncu --set full --clock-control none --import-source on -k regex:grid_kernel -s 2 -c 1 -o gpurun_out/prof_$TAG python tools/profile_grid.py 5 > gpurun_out/ncu_full.log 2>&1; ${2:-true}" 2>&1 | tail -1
+timeout 2400 /usr/local/graft/bin/gpurun --timeout 1500 -- "timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo rc=\$? >> gpurun_out/pytest_gpu.log; timeout 400 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; timeout 600 ncu --set full --clock-control none --import-source on -k regex:grid_ -s 2 -c 1 -o gpurun_out/prof_$TAG python tools/profile_grid.py 5 > gpurun_out/ncu_full.log 2>&1; ${2:-true}" 2>&1 | tail -1
 tail -2 gpurun_out/pytest_gpu.log
 python - "$TAG" <<'PY'
 import csv, json, subprocess, sys

@@ -1,0 +1,75 @@
+#!/usr/bin/env python3
+"""Per-phase timeline of the one-class lookup kernel (diagnostics).
+
+Build the instrumented library here:   python tools/row_timing.py --build
+Run on a B200:  PM2L_LIB_PATH=$PWD/paper_2603_00549_b200/libpm2l_timing.so python tools/row_timing.py
+
+Each warp's lane 0 stamps %globaltimer at: 0 kernel entry, 1 tile start
+(prologue done), 2 staircase, 3 W table, 4 cut searches, 5 byte maps,
+6 base table visible, 7 tile written.
+"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+LIB = os.path.join(ROOT, "paper_2603_00549_b200", "libpm2l_timing.so")
+
+
+def build():
+    from paper_2603_00549_b200 import _build
+    cmd = [_build.nvcc(), *_build.NVCC_FLAGS, "-DPM2L_TIMING",
+           f"-DPM2L_SOURCE_HASH=\"{_build.source_hash()}\"", *_build.SOURCES, "-o", LIB]
+    subprocess.run(cmd, cwd=_build.PKG, check=True)
+    print(LIB)
+
+
+def main():
+    import ctypes as C
+    import numpy as np
+    import torch
+    import bench
+    from paper_2603_00549_b200 import _native
+    from paper_2603_00549_b200.compute import WaveModel
+    from paper_2603_00549_b200.nascache import PreparedGrid
+    lib = _native.load()
+    fn = lib.pm2l_debug_row_timing
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p, C.c_int]
+    ds = bench.load_bf16()
+    prep = PreparedGrid(ds, bench.grid_for(1), WaveModel(ds.device.sm_count))
+    plan = _native.GridPlan(prep.device_tables(0), prep.axis_arrays())
+    out = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    print("kernel path", plan.kernel_path(out))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for _ in range(5):
+        flush.zero_()
+        ev[0].record()
+        plan.launch(out, stages=7)
+        ev[1].record()
+    torch.cuda.synchronize()
+    print("step ms (last)", ev[0].elapsed_time(ev[1]))
+    n = 16384 * 8
+    buf = np.zeros(n, np.uint64)
+    assert fn(buf.ctypes.data, n) == 0
+    tiles = 2500
+    t = buf[:tiles * 8].reshape(tiles, 8).astype(np.int64)
+    # entry stamp is per (cta, warp) == tile index for a one-tile-per-warp launch
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1000.0
+    names = ["entry", "prologue", "staircase", "W table", "cuts", "maps", "pdl wait", "emit"]
+    print("phase            median_us   p90_us   max_us")
+    for i in range(1, 8):
+        d = rel[:, i] - rel[:, i - 1]
+        print(f"{names[i]:<15} {np.median(d):9.2f} {np.percentile(d, 90):8.2f} {d.max():8.2f}")
+    print("entry spread us", rel[:, 0].max(), " end: median", np.median(rel[:, 7]),
+          "max", rel[:, 7].max())
+
+
+if __name__ == "__main__":
+    if "--build" in sys.argv:
+        build()
+    else:
+        main()
