@@ -124,7 +124,8 @@ int pm2l_grid_predict(pm2l_tables* t,
  * log2, the exact-hit fix-up list and the per-(curve, k) base workspace are
  * staged in HBM once; pm2l_grid_plan_launch then only launches kernels (no
  * host work, no copies — CUDA-graph capturable).  The tables must outlive the
- * plan.  nan_stats (DEVICE, 3 x u64, nullable; initialise to {~0, 0, 0}):
+ * plan.  nan_stats (DEVICE, 3 x u64, nullable; a launch that includes the
+ * base-table stage resets it to {~0, 0, 0} itself, otherwise initialise it):
  * [0] first NaN slice index (UnresolvedPoint semantics, nascache.py:298-306),
  * [1] NaN count, [2] set when [0] must be re-derived with pm2l_nan_scan.
  * stages: bitmask 1 = base table, 2 = grid kernel, 4 = exact fix-ups

@@ -38,11 +38,20 @@ constexpr int kMaxSmemSamples = 256;
 __global__ void __launch_bounds__(256) base_table_kernel(TablesDev t, GridDev g,
                                                          const uint64_t* __restrict__ K, int nK,
                                                          double* __restrict__ base,
-                                                         double* __restrict__ fixval) {
+                                                         double* __restrict__ fixval,
+                                                         unsigned long long* stats) {
   pdl_release();  // the grid kernel may start its (independent) row setup now
+  // the launch's unresolved-point statistics start here (the grid kernel
+  // touches them only after griddepcontrol.wait)
+  if (stats && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    stats[0] = ~0ull;
+    stats[1] = 0ull;
+    stats[2] = 0ull;
+  }
   __shared__ double sd[kMaxSmemSamples], sy[kMaxSmemSamples];
   const int c = blockIdx.y;
   if (c == t.C) {  // exact-record hits: their final latency, applied after the grid kernel
+    if (!fixval) return;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < g.n_fix;
          i += int64_t(gridDim.x) * blockDim.x) {
       const uint64_t* c4 = g.fix_coord + 4 * i;
@@ -536,9 +545,7 @@ __device__ unsigned long long g_row_dbg[16384 * 8];
 #define ROW_MARK(tile, i)                                                         \
   do {                                                                            \
     if (lane == 0 && (tile) < 16384) {                                            \
-      unsigned long long t_;                                                      \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                      \
-      g_row_dbg[(tile) * 8 + (i)] = t_;                                           \
+      g_row_dbg[(tile) * 8 + (i)] = clock64();                                    \
     }                                                                             \
   } while (0)
 #else
@@ -574,7 +581,7 @@ struct RowLaunch {
   int tiles, nbs, nkc, kc;   // tiles = rows * nbs * nkc; k chunk length (even)
   int seg;                   // byte-map bytes per lane (multiple of 16)
   int ctas;
-  int off_bar, off_gcur, off_glk, off_clm, off_cln, off_wcp, off_kf, off_ms, off_kq, off_warp;
+  int off_bar, off_gcur, off_glk, off_clm, off_cln, off_wcp, off_kf, off_ms, off_kq, off_kr, off_warp;
   int w_sD, w_sP, w_cut, w_W, w_rmap, w_gmap, warp_bytes;
   int64_t smem;
 };
@@ -586,7 +593,7 @@ void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_k, RowL
     o = (o + bytes + 15) & ~int64_t(15);
     return int(at);
   };
-  rl.off_bar = take(16);
+  rl.off_bar = take(16);  // two mbarriers
   rl.off_gcur = take(8ll * t.R);
   rl.off_glk = take(8ll * t.G);
   rl.off_clm = take(8ll * t.CM);
@@ -595,6 +602,7 @@ void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_k, RowL
   rl.off_kf = take(stage_k ? 4ll * g.nK : 0);
   rl.off_ms = take(stage_k ? 8ll * g.nK : 0);
   rl.off_kq = take(stage_k ? 8ll * g.nK : 0);
+  rl.off_kr = take(stage_k ? 4ll * rl.nkc * t.G : 0);
   rl.off_warp = int(o);
   int64_t w = 0;
   auto wtake = [&](int64_t bytes) {
@@ -613,78 +621,49 @@ void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_k, RowL
   rl.smem = o + kRowWarps * w;
 }
 
-// Two byte maps over [0, 32*seg), built in one interleaved pass:
-//   map_j[r] = #{s < ncut_j : cut_j[s] <= r}, and 0xFF from r = ff_j on
-//   (ff_j < 0: never).
-// Difference array (shared-memory byte increments at each cut) + prefix sum:
-// SIMD within each word (x*0x01010101 sums the bytes below each byte), a
-// running carry across the lane's segment, and a warp scan across lanes.
-// Counts stay < 256 (ncut <= 255).
+// Byte map over [0, 32*seg): map[r] = #{s < ncut : cut[s] <= r}, and 0xFF
+// from r = ff on (ff < 0: never); cut ascending.  Each lane owns SEGW words:
+// a lower bound over the (short, conflict-free) cut array gives the count
+// at its first byte, then the few cuts that fall inside the segment add
+// byte-wise increments (SIMD within a register).  Counts stay < 256.
 template <int SEGW>  // u32 words per lane
-__device__ __forceinline__ void build_count_maps(uint8_t* map0, const int32_t* cut0, int ncut0,
-                                                 int ff0, uint8_t* map1, const int32_t* cut1,
-                                                 int ncut1, int lane) {
-  uint32_t* mw0 = reinterpret_cast<uint32_t*>(map0) + lane * SEGW;
-  uint32_t* mw1 = reinterpret_cast<uint32_t*>(map1) + lane * SEGW;
-#pragma unroll
-  for (int q = 0; q < SEGW; q += 4) {
-    *reinterpret_cast<uint4*>(mw0 + q) = make_uint4(0u, 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(mw1 + q) = make_uint4(0u, 0u, 0u, 0u);
+__device__ __forceinline__ void build_count_map(uint8_t* map, const int32_t* cut, int ncut, int ff,
+                                                int lane) {
+  const int r0 = lane * SEGW * 4, r1 = r0 + SEGW * 4;
+  int lo = 0, hi = ncut;  // first s with cut[s] > r0
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (cut[mid] <= r0) lo = mid + 1; else hi = mid;
   }
-  __syncwarp();
-  constexpr int kLim = 32 * SEGW * 4;
-  for (int s = lane; s < max(ncut0, ncut1); s += 32) {
-    if (s < ncut0) {
-      const int e = cut0[s];
-      if (e < kLim) atomicAdd(reinterpret_cast<uint32_t*>(map0) + (e >> 2), 1u << (8 * (e & 3)));
-    }
-    if (s < ncut1) {
-      const int e = cut1[s];
-      if (e < kLim) atomicAdd(reinterpret_cast<uint32_t*>(map1) + (e >> 2), 1u << (8 * (e & 3)));
+  uint32_t w[SEGW];
+#pragma unroll
+  for (int q = 0; q < SEGW; ++q) w[q] = uint32_t(lo) * 0x01010101u;
+  for (int s = lo; s < ncut; ++s) {
+    const int e = cut[s];
+    if (e >= r1) break;
+#pragma unroll
+    for (int q = 0; q < SEGW; ++q) {
+      const int sh = e - r0 - 4 * q;  // bytes >= sh of word q count this cut
+      w[q] += sh <= 0 ? 0x01010101u : sh >= 4 ? 0u : (0x01010101u << (8 * sh));
     }
   }
-  __syncwarp();
-  uint32_t w0[SEGW], w1[SEGW];
+  if (ff >= 0) {
 #pragma unroll
-  for (int q = 0; q < SEGW; q += 4) {
-    const uint4 a = *reinterpret_cast<const uint4*>(mw0 + q);
-    const uint4 b = *reinterpret_cast<const uint4*>(mw1 + q);
-    w0[q] = a.x; w0[q + 1] = a.y; w0[q + 2] = a.z; w0[q + 3] = a.w;
-    w1[q] = b.x; w1[q + 1] = b.y; w1[q + 2] = b.z; w1[q + 3] = b.w;
-  }
-  uint32_t run0 = 0, run1 = 0;
-#pragma unroll
-  for (int q = 0; q < SEGW; ++q) {
-    const uint32_t p0 = w0[q] * 0x01010101u, p1 = w1[q] * 0x01010101u;
-    w0[q] = p0 + run0 * 0x01010101u;
-    w1[q] = p1 + run1 * 0x01010101u;
-    run0 += p0 >> 24;
-    run1 += p1 >> 24;
-  }
-  uint32_t e0 = run0, e1 = run1;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t o0 = __shfl_up_sync(0xFFFFFFFFu, e0, off);
-    const uint32_t o1 = __shfl_up_sync(0xFFFFFFFFu, e1, off);
-    if (lane >= off) { e0 += o0; e1 += o1; }
-  }
-  e0 -= run0;
-  e1 -= run1;
-  const int r0 = lane * SEGW * 4;
-#pragma unroll
-  for (int q = 0; q < SEGW; ++q) {
-    w0[q] += e0 * 0x01010101u;
-    w1[q] += e1 * 0x01010101u;
-    if (ff0 >= 0) {
-      const int sh = ff0 - r0 - 4 * q;
-      w0[q] |= sh <= 0 ? 0xFFFFFFFFu : sh >= 4 ? 0u : (0xFFFFFFFFu << (8 * sh));
+    for (int q = 0; q < SEGW; ++q) {
+      const int sh = ff - r0 - 4 * q;
+      w[q] |= sh <= 0 ? 0xFFFFFFFFu : sh >= 4 ? 0u : (0xFFFFFFFFu << (8 * sh));
     }
   }
+  uint32_t* mw = reinterpret_cast<uint32_t*>(map) + lane * SEGW;
 #pragma unroll
-  for (int q = 0; q < SEGW; q += 4) {
-    *reinterpret_cast<uint4*>(mw0 + q) = make_uint4(w0[q], w0[q + 1], w0[q + 2], w0[q + 3]);
-    *reinterpret_cast<uint4*>(mw1 + q) = make_uint4(w1[q], w1[q + 1], w1[q + 2], w1[q + 3]);
-  }
+  for (int q = 0; q < SEGW; q += 4)
+    *reinterpret_cast<uint4*>(mw + q) = make_uint4(w[q], w[q + 1], w[q + 2], w[q + 3]);
+}
+
+__device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ uint64_t ceil_div_w(const WcParam& p, int j, uint64_t a, uint64_t d) {
@@ -698,6 +677,28 @@ __device__ __forceinline__ uint64_t ceil_div_w(const WcParam& p, int j, uint64_t
   return num / d;
 }
 
+// Row scalars of one tile (loaded one tile ahead).
+template <int NB>
+struct RowIn {
+  double qm, qn;
+  uint64_t m, n;
+  uint64_t b[NB];
+};
+
+template <int NB>
+__device__ __forceinline__ RowIn<NB> load_row_in(const GridDev& g, const RowLaunch& rl, int tile) {
+  RowIn<NB> r;
+  const int rs = tile / rl.nkc, slab = rs % rl.nbs, row = rs / rl.nbs;
+  const int nN = int(g.nN), im = row / nN, jn = row - im * nN;
+  r.qm = g.logM[im];
+  r.qn = g.logN[jn];
+  r.m = g.M[im];
+  r.n = g.N[jn];
+#pragma unroll
+  for (int ib = 0; ib < NB; ++ib) r.b[ib] = g.B[g.b_lo + slab * NB + ib];
+  return r;
+}
+
 template <int NB, bool STAGE, int SEGW>
 __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t, GridDev g,
                                                                     RowLaunch rl,
@@ -709,40 +710,39 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t
   double* clm = reinterpret_cast<double*>(smem + rl.off_clm);
   double* cln = reinterpret_cast<double*>(smem + rl.off_cln);
   WcParam* wcp = reinterpret_cast<WcParam*>(smem + rl.off_wcp);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + rl.off_bar);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + rl.off_bar);  // [0] tables, [1] per-k
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   ROW_MARK(blockIdx.x * kRowWarps + warp, 0);
-  const uint32_t* kfs = g.kfast;
-  const uint64_t* ms = g.mn_sorted;
-  const double* kq = g.logK;
-  if (STAGE) {
-    kfs = reinterpret_cast<const uint32_t*>(smem + rl.off_kf);
-    ms = reinterpret_cast<const uint64_t*>(smem + rl.off_ms);
-    kq = reinterpret_cast<const double*>(smem + rl.off_kq);
-  }
-  // prologue: every CTA-constant table arrives by TMA bulk copies on one
-  // mbarrier (one round trip, no register staging)
+  const int G = t.G, CM = t.CM, NW = t.NW, nK = int(g.nK);
+  const uint32_t* kfs = STAGE ? reinterpret_cast<const uint32_t*>(smem + rl.off_kf) : g.kfast;
+  const int32_t* krt = STAGE ? reinterpret_cast<const int32_t*>(smem + rl.off_kr) : g.kright;
+  // prologue: CTA-constant tables by TMA bulk copies on two mbarriers, the
+  // small tables first (the staircase and W table need only those), the
+  // per-k tables behind them
   if (tid == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint32_t nk = uint32_t(g.nK);
-    uint32_t total = r16(8ll * t.R) + r16(8ll * t.G) + 2 * r16(8ll * t.CM) +
-                     r16(int64_t(sizeof(WcParam)) * t.NW);
-    if (STAGE) total += r16(4ll * nk) + 2 * r16(8ll * nk);
-    mbar_expect_tx(bar, total);
+    mbar_expect_tx(bar, r16(8ll * t.R) + r16(8ll * G) + 2 * r16(8ll * CM) +
+                            r16(int64_t(sizeof(WcParam)) * NW));
+    bulk_g2s(clm, t.cls_lm, r16(8ll * CM), bar);
+    bulk_g2s(cln, t.cls_ln, r16(8ll * CM), bar);
+    bulk_g2s(wcp, t.wcp, r16(int64_t(sizeof(WcParam)) * NW), bar);
+    bulk_g2s(glk, t.grp_lk, r16(8ll * G), bar);
     bulk_g2s(gcur, t.g_cw, r16(8ll * t.R), bar);
-    bulk_g2s(glk, t.grp_lk, r16(8ll * t.G), bar);
-    bulk_g2s(clm, t.cls_lm, r16(8ll * t.CM), bar);
-    bulk_g2s(cln, t.cls_ln, r16(8ll * t.CM), bar);
-    bulk_g2s(wcp, t.wcp, r16(int64_t(sizeof(WcParam)) * t.NW), bar);
     if (STAGE) {
-      bulk_g2s(smem + rl.off_kf, g.kfast, r16(4ll * nk), bar);
-      bulk_g2s(smem + rl.off_ms, g.mn_sorted, r16(8ll * nk), bar);
-      bulk_g2s(smem + rl.off_kq, g.logK, r16(8ll * nk), bar);
+      mbar_expect_tx(bar + 1, r16(4ll * nK) + 2 * r16(8ll * nK) + r16(4ll * rl.nkc * G));
+      bulk_g2s(smem + rl.off_ms, g.mn_sorted, r16(8ll * nK), bar + 1);
+      bulk_g2s(smem + rl.off_kq, g.logK, r16(8ll * nK), bar + 1);
+      bulk_g2s(smem + rl.off_kr, g.kright, r16(4ll * rl.nkc * G), bar + 1);
+      bulk_g2s(smem + rl.off_kf, g.kfast, r16(4ll * nK), bar + 1);
     }
   }
-  __syncthreads();  // mbarrier initialised before anyone waits on it
+  int tile = blockIdx.x * kRowWarps + warp;
+  RowIn<NB> rin = load_row_in<NB>(g, rl, min(tile, rl.tiles - 1));  // in flight during the wait
+  __syncthreads();  // mbarriers initialised before anyone waits on them
   mbar_wait(bar, 0);
+  const uint32_t ms_s = smem_u32(smem + rl.off_ms), kq_s = smem_u32(smem + rl.off_kq);
   uint8_t* wb = smem + rl.off_warp + warp * rl.warp_bytes;
   uint64_t* sD = reinterpret_cast<uint64_t*>(wb + rl.w_sD);
   int32_t* sP = reinterpret_cast<int32_t*>(wb + rl.w_sP);
@@ -750,24 +750,25 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t
   double* W = reinterpret_cast<double*>(wb + rl.w_W);
   uint8_t* rmap = wb + rl.w_rmap;
   uint8_t* gmap = wb + rl.w_gmap;
-  const int nN = int(g.nN), nK = int(g.nK), G = t.G, CM = t.CM, NW = t.NW;
   const int64_t plane = g.nM * g.nN * g.nK;
-  bool waited = false;
-  for (int tile = blockIdx.x * kRowWarps + warp; tile < rl.tiles;
-       tile += gridDim.x * kRowWarps) {
+  bool waited = false, staged = !STAGE;
+  for (; tile < rl.tiles; tile += gridDim.x * kRowWarps) {
     const int kcx = tile % rl.nkc, rs = tile / rl.nkc;
     const int slab = rs % rl.nbs, row = rs / rl.nbs;
-    const int im = row / nN, jn = row - im * nN;
     const int k0 = kcx * rl.kc, kc = min(rl.kc, nK - k0);
-    const double qm = g.logM[im], qn = g.logN[jn];
-    const uint64_t m = g.M[im], n = g.N[jn];
+    const RowIn<NB> cur = rin;
+    {
+      const int nt = tile + gridDim.x * kRowWarps;
+      if (nt < rl.tiles) rin = load_row_in<NB>(g, rl, nt);  // next tile's scalars
+    }
     ROW_MARK(tile, 1);
     // ---- staircase: prefix minimum of D_j = max(|lm_j-qm|, |ln_j-qn|)
     uint64_t dmin = ~0ull;
     int len = 0, lastpos = 0;
     for (int b0 = 0; b0 < CM; b0 += 32) {
       const int j = b0 + lane;
-      const uint64_t d = j < CM ? umax64(abs_bits(__dsub_rn(clm[j], qm)), abs_bits(__dsub_rn(cln[j], qn)))
+      const uint64_t d = j < CM ? umax64(abs_bits(__dsub_rn(clm[j], cur.qm)),
+                                         abs_bits(__dsub_rn(cln[j], cur.qn)))
                                 : ~0ull;
       uint64_t pm = d;
 #pragma unroll
@@ -791,51 +792,53 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t
       if (tail < dmin) dmin = tail;
     }
     ROW_MARK(tile, 2);
-    // ---- wave-scale table W[wave class][ib] of this (m, n) and batch slab
-    {
-      uint64_t bb[NB];
+    // ---- wave-scale table W[wave class][ib] of this (m, n) and batch slab;
+    // independent entries, unrolled for ILP
+#pragma unroll 2
+    for (int wc = lane; wc < NW; wc += 32) {
+      const WcParam p = wcp[wc];
+      const uint64_t tmn = ceil_div_w(p, 0, cur.m, p.tm) * ceil_div_w(p, 1, cur.n, p.tn) * p.sk;
 #pragma unroll
-      for (int ib = 0; ib < NB; ++ib) bb[ib] = g.B[g.b_lo + slab * NB + ib];
-      for (int wc = lane; wc < NW; wc += 32) {
-        const WcParam p = wcp[wc];
-        const uint64_t tmn = ceil_div_w(p, 0, m, p.tm) * ceil_div_w(p, 1, n, p.tn) * p.sk;
-#pragma unroll
-        for (int ib = 0; ib < NB; ++ib) {
-          const double w = __ull2double_rn(ceil_div_w(p, 2, bb[ib] * tmn, p.bpw));
-          W[wc * NB + ib] = p.rw == 1.0 ? w : __ddiv_rn(w, p.rw);
-        }
+      for (int ib = 0; ib < NB; ++ib) {
+        const double w = __ull2double_rn(ceil_div_w(p, 2, cur.b[ib] * tmn, p.bpw));
+        W[wc * NB + ib] = p.rw == 1.0 ? w : __ddiv_rn(w, p.rw);
       }
     }
     __syncwarp();
     ROW_MARK(tile, 3);
-    // ---- cut points: binary searches inside the k chunk
-    //   cut[s] (s < len-1): #{ranks with mn >= sD[s]}; cut[len-1]: #{mn > dmin}
-    //   cut[len + g]: first k index where group g is left of log2 k and
-    //                 farther than dmin from it
-    // fixed-trip branch-free binary searches, both kinds in one loop
-    // (lanes never diverge): i < len: rank cuts; i >= len: group cuts
-    //   rank cut: #{ranks r: mn(r) >= sD[i]} (i == len-1: > dmin); mn descends
-    //   group cut: #{k: NOT (group left of log2 k and farther than dmin)}
+    if (!staged) {
+      mbar_wait(bar + 1, 0);
+      staged = true;
+    }
+    // ---- cut points: fixed-trip branch-free binary searches, one shared
+    // load per step, both kinds in one loop (lanes never diverge)
+    //   i < len : #{ranks r: mn(r) >= sD[i]} (i == len-1: > dmin); mn descends
+    //   i >= len: #{k: NOT (group i-len left of log2 k and farther than dmin)}
+    //             = kright + #{k >= kright: log2 k - lk <= dmin}
     int top = 1;
     while (top * 2 <= kc) top *= 2;
     for (int i = lane; i < len + G; i += 32) {
       const bool rk = i < len, strict = i == len - 1;
       const int gg = rk ? 0 : i - len;
-      const uint64_t x = sD[rk ? i : 0];
+      const uint64_t x = rk ? sD[i] : dmin;
       const double lk = glk[gg];
+      const int kr = rk ? 0 : krt[kcx * G + gg];
       int lo = 0;
       for (int step = top; step; step >>= 1) {
         const int r = k0 + min(lo + step, kc) - 1;
-        const uint64_t v = ms[r];
-        const bool far = int(kfs[r] >> 24) > gg && abs_bits(__dsub_rn(lk, kq[r])) > dmin;
-        const bool adv = rk ? (v > x || (!strict && v == x)) : !far;
-        lo += (lo + step <= kc && adv) ? step : 0;
+        uint64_t v;
+        if (STAGE) v = lds_u64((rk ? ms_s : kq_s) + 8u * uint32_t(r));
+        else v = rk ? g.mn_sorted[r] : __double_as_longlong(g.logK[r]);
+        const bool keep = rk ? (v > x || (!strict && v == x))
+                             : (r - k0 < kr || abs_bits(__dsub_rn(__longlong_as_double(v), lk)) <= x);
+        lo += (lo + step <= kc && keep) ? step : 0;
       }
       cut[i] = lo;
     }
     __syncwarp();
     ROW_MARK(tile, 4);
-    build_count_maps<SEGW>(rmap, cut, len - 1, cut[len - 1], gmap, cut + len, G, lane);
+    build_count_map<SEGW>(rmap, cut, len - 1, cut[len - 1], lane);
+    build_count_map<SEGW>(gmap, cut + len, G, -1, lane);
     __syncwarp();
     ROW_MARK(tile, 5);
     if (!waited) {
@@ -923,9 +926,41 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t
         }
       }
     }
+    // exact-record hits of this tile take priority over the nearest result
+    // (_kernels.pyx:107-110): re-count them by their exact result
+    {
+      const int f0 = g.fixr_off[row], f1 = g.fixr_off[row + 1];
+      if (f1 > f0) {
+        __syncwarp();  // this warp's stores above are visible to every lane
+        for (int f = f0 + lane; f < f1; f += 32) {
+          const FixEntry fe = g.fixr[f];
+          if (fe.ik < k0 || fe.ik >= k0 + kc || fe.ib < slab * NB || fe.ib >= slab * NB + NB) continue;
+          double* o = out.lat + int64_t(fe.ib) * plane + int64_t(row) * nK + fe.ik;
+          const int ci = fe.curve;
+          if (out.nan_stats) {
+            const bool was_nan = *o != *o;
+            if (was_nan && ci >= 0) {
+              atomicAdd(out.nan_stats + 1, ~0ull);
+              atomicOr(out.nan_stats + 2, 1ull);
+            }
+            if (!was_nan && ci < 0) {
+              atomicAdd(out.nan_stats + 1, 1ull);
+              atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
+            }
+          }
+          if (ci < 0) {
+            *o = qnan();
+          } else {
+            const uint64_t* c4 = g.fix_coord + 4 * int64_t(fe.fix);
+            *o = predict_point(t, ci, c4[0], c4[1], c4[2], c4[3], base_tab[ci * nK + fe.ik]).lat;
+          }
+        }
+      }
+    }
     __syncwarp();  // the warp's state buffers are rewritten by the next tile
     ROW_MARK(tile, 7);
   }
+  if (!staged) mbar_wait(bar + 1, 0);  // never exit with bulk copies in flight
   if (!waited) pdl_wait();
 }
 
@@ -1177,10 +1212,10 @@ cudaError_t launch_grid_t(const TablesDev& t, const GridDev& g, const GridLaunch
 }
 
 void launch_base_table(const TablesDev& t, const GridDev& g, double* ws, double* fixval,
-                       cudaStream_t s) {
+                       unsigned long long* stats, cudaStream_t s) {
   const int chunks = int(std::min<int64_t>((g.nK + 255) / 256, 64));
-  const int ys = t.C + (fixval && g.n_fix > 0 ? 1 : 0);
-  base_table_kernel<<<dim3(chunks, ys), 256, 0, s>>>(t, g, g.K, int(g.nK), ws, fixval);
+  const int ys = std::max(1, t.C + (fixval && g.n_fix > 0 ? 1 : 0));
+  base_table_kernel<<<dim3(chunks, ys), 256, 0, s>>>(t, g, g.K, int(g.nK), ws, fixval, stats);
 }
 
 }  // namespace
@@ -1209,7 +1244,7 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   // exact-hit values are precomputed with the base table whenever it runs in
   // the same launch sequence (stage masks that skip it recompute in fixup_kernel)
   double* fixval = (g.n_fix > 0 && (stages & kStageBase)) ? ws + nbase : nullptr;
-  if ((stages & kStageBase) && (t.C > 0 || fixval)) launch_base_table(t, g, ws, fixval, s);
+  if (stages & kStageBase) launch_base_table(t, g, ws, fixval, out.nan_stats, s);
   const bool v = out.curve != nullptr;
   cudaError_t e = cudaSuccess;
   int row_nb = 0;
@@ -1231,7 +1266,9 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
     }
   }
   if (e != cudaSuccess) return int(e);
-  if (g.n_fix > 0 && (stages & kStageFixup)) {
+  // the row kernel applies its rows' exact hits itself
+  const bool fixed_in_grid = (stages & kStageGrid) && rl.tiles > 0;
+  if (g.n_fix > 0 && (stages & kStageFixup) && !fixed_in_grid) {
     const int nb = int((g.n_fix + 127) / 128);
     if (v) fixup_kernel<true><<<nb, 128, 0, s>>>(t, g, out, nullptr);
     else fixup_kernel<false><<<nb, 128, 0, s>>>(t, g, out, fixval);
@@ -1246,7 +1283,7 @@ int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* ws, dou
   if (card == 0 || t.C == 0) return 0;
   GridLaunch gl = plan_grid(t, g, true);
   if (!grid_dims_ok(g, gl) || t.C > 65535 || gl.tiles > 65535) return int(cudaErrorInvalidValue);
-  launch_base_table(t, g, ws, nullptr, s);
+  launch_base_table(t, g, ws, nullptr, nullptr, s);
   const int64_t smem = gl.mode == 0 ? ((8ll * t.C + 15) & ~15ll) + 8ll * t.C * gl.bper : 0;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(all_curves_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

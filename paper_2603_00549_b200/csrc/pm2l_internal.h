@@ -103,7 +103,7 @@ struct alignas(16) FixEntry {
   int32_t ik;     // k index
   int32_t ib;     // batch index, slice-relative
   int32_t curve;  // recorded kernel's curve (-1: no curve -> NaN)
-  int32_t pad;
+  int32_t fix;    // index into the flat fix-up list (fix_pos / fix_coord)
 };
 
 // Per-launch grid description (device pointers into one per-call upload).
@@ -127,6 +127,8 @@ struct GridDev {
   // mn as ordered |double| bits
   const uint32_t* kfast = nullptr;
   const uint64_t* mn_sorted = nullptr;
+  // [chunks x G]: first chunk-local k index with start(ik) > g
+  const int32_t* kright = nullptr;
   // exact-hit fix-ups: slice-relative flat index + coordinates + curve
   int64_t n_fix = 0;
   const int64_t* fix_pos = nullptr;

@@ -335,6 +335,7 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   // subtraction and |.| as the device (host double, no contraction).
   std::vector<uint32_t> kfast;
   std::vector<uint64_t> mn_sorted;
+  std::vector<int32_t> kright;
   const bool fast_ok = tt.G >= 1 && tt.G <= 255 && nK >= 1 && nK <= 65535;
   if (fast_ok) {
     const int G = tt.G;
@@ -361,6 +362,16 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
     }
     kfast.resize(nK);
     mn_sorted.resize(nK);
+    // per (chunk, group): first chunk-local k index whose log2 k lies right
+    // of the group (start(ik) > g)
+    for (int64_t k0 = 0; k0 < nK; k0 += kKChunk) {
+      const int64_t k1 = std::min<int64_t>(nK, k0 + kKChunk);
+      for (int g = 0; g < G; ++g) {
+        int64_t i = k0;
+        while (i < k1 && kinfo[i].start <= g) ++i;
+        kright.push_back(int32_t(i - k0));
+      }
+    }
     for (int64_t k0 = 0; k0 < nK; k0 += kKChunk) {
       const int64_t k1 = std::min<int64_t>(nK, k0 + kKChunk);
       std::vector<int32_t> ord(k1 - k0);
@@ -432,7 +443,7 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
     for (auto& [pos, val] : fix) {
       const int64_t ib = pos / inner, rem = pos - ib * inner;
       const int64_t row = rem / nK, ik = rem - row * nK;
-      fixr[fill[row]++] = FixEntry{int32_t(ik), int32_t(ib), val.second, 0};
+      fixr[fill[row]++] = FixEntry{int32_t(ik), int32_t(ib), val.second, int32_t(i)};
       ++i;
     }
   }
@@ -451,6 +462,7 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   g.kinfo = blob.add(kinfo);
   g.kfast = fast_ok ? blob.add(kfast) : nullptr;
   g.mn_sorted = fast_ok ? blob.add(mn_sorted) : nullptr;
+  g.kright = fast_ok ? blob.add(kright) : nullptr;
   g.n_fix = int64_t(fix_pos.size());
   g.fix_pos = blob.add(fix_pos);
   g.fix_coord = blob.add(fix_coord);
@@ -470,6 +482,7 @@ GridDev rebase(const GridDev& o, const void* base) {
   if (o.kfast) {
     g.kfast = shift(o.kfast, base);
     g.mn_sorted = shift(o.mn_sorted, base);
+    g.kright = shift(o.kright, base);
   }
   g.fix_pos = shift(o.fix_pos, base);
   g.fix_coord = shift(o.fix_coord, base); g.fix_curve = shift(o.fix_curve, base);

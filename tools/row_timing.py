@@ -5,7 +5,7 @@ Build the instrumented library here:   python tools/row_timing.py --build
 Run on a B200:  PM2L_LIB_PATH=$PWD/paper_2603_00549_b200/libpm2l_timing.so python tools/row_timing.py
 
 Each warp's lane 0 stamps %globaltimer at: 0 kernel entry, 1 tile start
-(prologue done), 2 staircase, 3 W table, 4 cut searches, 5 byte maps,
+(prologue done; SM clock64 cycles / SM_MHZ), 2 staircase, 3 W table, 4 cut searches, 5 byte maps,
 6 base table visible, 7 tile written.
 """
 import os
@@ -57,15 +57,15 @@ def main():
     tiles = 2500
     t = buf[:tiles * 8].reshape(tiles, 8).astype(np.int64)
     # entry stamp is per (cta, warp) == tile index for a one-tile-per-warp launch
-    t0 = t[:, 0].min()
-    rel = (t - t0) / 1000.0
+    # SM clock64 stamps: per-tile differences only (clocks differ across SMs)
+    mhz = float(os.environ.get("SM_MHZ", "1965"))
+    rel = (t - t[:, :1]) / mhz
     names = ["entry", "prologue", "staircase", "W table", "cuts", "maps", "pdl wait", "emit"]
     print("phase            median_us   p90_us   max_us")
     for i in range(1, 8):
         d = rel[:, i] - rel[:, i - 1]
         print(f"{names[i]:<15} {np.median(d):9.2f} {np.percentile(d, 90):8.2f} {d.max():8.2f}")
-    print("entry spread us", rel[:, 0].max(), " end: median", np.median(rel[:, 7]),
-          "max", rel[:, 7].max())
+    print("tile span us: median", np.median(rel[:, 7]), "max", rel[:, 7].max())
 
 
 if __name__ == "__main__":
