@@ -538,6 +538,9 @@ __global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g
 // tile's points; many independent tiles are in flight per SM and no barrier
 // couples warps.
 constexpr int kRowWarps = 8;
+constexpr int kRingProd = 4;   // grid_ring_kernel: default builder warps per CTA
+constexpr int kRingSlots = 6;  // default tile-state slots per CTA
+constexpr int kRingMaxSlots = 16;
 
 #ifdef PM2L_TIMING
 // diagnostic build only (tools/row_timing.py): per-tile phase timestamps
@@ -552,6 +555,7 @@ __device__ unsigned long long g_row_dbg[16384 * 8];
 #define ROW_MARK(tile, i) do {} while (0)
 #endif
 
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return uint32_t(__cvta_generic_to_shared(p));
 }
@@ -577,12 +581,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 __host__ __device__ constexpr uint32_t r16(int64_t b) { return uint32_t((b + 15) & ~int64_t(15)); }
 
+// n / d for n < 2^31 through a host-computed u32 magic (Granlund-Montgomery)
+struct FastDiv {
+  uint32_t m, s;  // multiplier, sh1 | sh2 << 8
+};
+inline FastDiv fast_div_for(uint32_t d) {
+  int l = 0;
+  while ((uint64_t(1) << l) < d) ++l;
+  const uint64_t m = ((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1;
+  return FastDiv{uint32_t(m), uint32_t(l < 1 ? l : 1) | (uint32_t(l > 1 ? l - 1 : 0) << 8)};
+}
+__device__ __forceinline__ int fdiv(int n, FastDiv f) {
+  const uint32_t q = __umulhi(f.m, uint32_t(n));
+  return int((q + ((uint32_t(n) - q) >> (f.s & 0xFF))) >> (f.s >> 8));
+}
+
 struct RowLaunch {
   int tiles, nbs, nkc, kc;   // tiles = rows * nbs * nkc; k chunk length (even)
+  FastDiv d_nkc, d_nbs, d_nN;
   int seg;                   // byte-map bytes per lane (multiple of 16)
+  int ring;                  // producer/consumer variant (grid_ring_kernel)
+  int prod, slots;           // ring: builder warps, tile-state slots
   int ctas;
   int off_bar, off_gcur, off_glk, off_clm, off_cln, off_wcp, off_kf, off_ms, off_kq, off_kr, off_warp;
-  int w_sD, w_sP, w_cut, w_W, w_rmap, w_gmap, warp_bytes;
+  int w_hdr, w_sD, w_sP, w_cut, w_W, w_rmap, w_gmap, warp_bytes;
   int64_t smem;
 };
 
@@ -593,12 +615,13 @@ void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_k, RowL
     o = (o + bytes + 15) & ~int64_t(15);
     return int(at);
   };
-  rl.off_bar = take(16);  // two mbarriers
+  rl.off_bar = take(8ll * (2 + 2 * kRingMaxSlots));  // prologue + ring FULL/EMPTY mbarriers
   rl.off_gcur = take(8ll * t.R);
   rl.off_glk = take(8ll * t.G);
   rl.off_clm = take(8ll * t.CM);
   rl.off_cln = take(8ll * t.CM);
   rl.off_wcp = take(int64_t(sizeof(WcParam)) * t.NW);
+  rl.seg = int(kmap_lane_bytes(g.nK));
   rl.off_kf = take(stage_k ? 4ll * g.nK : 0);
   rl.off_ms = take(stage_k ? 8ll * g.nK : 0);
   rl.off_kq = take(stage_k ? 8ll * g.nK : 0);
@@ -610,7 +633,7 @@ void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_k, RowL
     w = (w + bytes + 15) & ~int64_t(15);
     return int(at);
   };
-  rl.seg = ((rl.kc + 511) / 512) * 16;
+  rl.w_hdr = wtake(16);
   rl.w_sD = wtake(8ll * t.CM);
   rl.w_sP = wtake(4ll * t.CM);
   rl.w_cut = wtake(4ll * (t.CM + t.G + 1));
@@ -618,46 +641,7 @@ void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_k, RowL
   rl.w_rmap = wtake(32ll * rl.seg);
   rl.w_gmap = wtake(32ll * rl.seg);
   rl.warp_bytes = int(w);
-  rl.smem = o + kRowWarps * w;
-}
-
-// Byte map over [0, 32*seg): map[r] = #{s < ncut : cut[s] <= r}, and 0xFF
-// from r = ff on (ff < 0: never); cut ascending.  Each lane owns SEGW words:
-// a lower bound over the (short, conflict-free) cut array gives the count
-// at its first byte, then the few cuts that fall inside the segment add
-// byte-wise increments (SIMD within a register).  Counts stay < 256.
-template <int SEGW>  // u32 words per lane
-__device__ __forceinline__ void build_count_map(uint8_t* map, const int32_t* cut, int ncut, int ff,
-                                                int lane) {
-  const int r0 = lane * SEGW * 4, r1 = r0 + SEGW * 4;
-  int lo = 0, hi = ncut;  // first s with cut[s] > r0
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (cut[mid] <= r0) lo = mid + 1; else hi = mid;
-  }
-  uint32_t w[SEGW];
-#pragma unroll
-  for (int q = 0; q < SEGW; ++q) w[q] = uint32_t(lo) * 0x01010101u;
-  for (int s = lo; s < ncut; ++s) {
-    const int e = cut[s];
-    if (e >= r1) break;
-#pragma unroll
-    for (int q = 0; q < SEGW; ++q) {
-      const int sh = e - r0 - 4 * q;  // bytes >= sh of word q count this cut
-      w[q] += sh <= 0 ? 0x01010101u : sh >= 4 ? 0u : (0x01010101u << (8 * sh));
-    }
-  }
-  if (ff >= 0) {
-#pragma unroll
-    for (int q = 0; q < SEGW; ++q) {
-      const int sh = ff - r0 - 4 * q;
-      w[q] |= sh <= 0 ? 0xFFFFFFFFu : sh >= 4 ? 0u : (0xFFFFFFFFu << (8 * sh));
-    }
-  }
-  uint32_t* mw = reinterpret_cast<uint32_t*>(map) + lane * SEGW;
-#pragma unroll
-  for (int q = 0; q < SEGW; q += 4)
-    *reinterpret_cast<uint4*>(mw + q) = make_uint4(w[q], w[q + 1], w[q + 2], w[q + 3]);
+  rl.smem = o + int64_t(rl.ring ? rl.slots : kRowWarps) * w;
 }
 
 __device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
@@ -681,164 +665,441 @@ __device__ __forceinline__ uint64_t ceil_div_w(const WcParam& p, int j, uint64_t
 template <int NB>
 struct RowIn {
   double qm, qn;
-  uint64_t m, n;
+  int im, jn;
   uint64_t b[NB];
+  uint64_t cm[2], cn[2];  // tile counts of wave classes lane, lane + 32
 };
 
 template <int NB>
-__device__ __forceinline__ RowIn<NB> load_row_in(const GridDev& g, const RowLaunch& rl, int tile) {
+__device__ __forceinline__ RowIn<NB> load_row_in(const GridDev& g, const RowLaunch& rl, int tile,
+                                                 int NW, int lane) {
   RowIn<NB> r;
-  const int rs = tile / rl.nkc, slab = rs % rl.nbs, row = rs / rl.nbs;
-  const int nN = int(g.nN), im = row / nN, jn = row - im * nN;
+  const int rs = fdiv(tile, rl.d_nkc), row = fdiv(rs, rl.d_nbs), slab = rs - row * rl.nbs;
+  const int im = fdiv(row, rl.d_nN), jn = row - im * int(g.nN);
   r.qm = g.logM[im];
   r.qn = g.logN[jn];
-  r.m = g.M[im];
-  r.n = g.N[jn];
+  r.im = im;
+  r.jn = jn;
 #pragma unroll
   for (int ib = 0; ib < NB; ++ib) r.b[ib] = g.B[g.b_lo + slab * NB + ib];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int wc = min(lane + 32 * h, NW - 1);
+    r.cm[h] = g.cm_tab[im * NW + wc];
+    r.cn[h] = g.cn_tab[jn * NW + wc];
+  }
   return r;
 }
 
+// Shared-memory views and table pointers common to the row kernels.
+template <bool STAGE>
+struct RowCtx {
+  int2* gcur;
+  double *glk, *clm, *cln;
+  WcParam* wcp;
+  const uint32_t* kfs;
+  const uint64_t* ms;    // per-k tables (shared when STAGE)
+  const double* kq;
+  const int32_t* krt;    // [chunk x G] kright
+  uint32_t ms_s, kq_s;   // shared addresses of ms / kq (STAGE)
+  int G, CM, NW, nK;
+  int64_t plane;
+};
+
+template <bool STAGE>
+__device__ __forceinline__ RowCtx<STAGE> row_ctx(uint8_t* smem, const TablesDev& t, const GridDev& g,
+                                                 const RowLaunch& rl) {
+  RowCtx<STAGE> c;
+  c.gcur = reinterpret_cast<int2*>(smem + rl.off_gcur);
+  c.glk = reinterpret_cast<double*>(smem + rl.off_glk);
+  c.clm = reinterpret_cast<double*>(smem + rl.off_clm);
+  c.cln = reinterpret_cast<double*>(smem + rl.off_cln);
+  c.wcp = reinterpret_cast<WcParam*>(smem + rl.off_wcp);
+  c.kfs = STAGE ? reinterpret_cast<const uint32_t*>(smem + rl.off_kf) : g.kfast;
+  c.ms = STAGE ? reinterpret_cast<const uint64_t*>(smem + rl.off_ms) : g.mn_sorted;
+  c.kq = STAGE ? reinterpret_cast<const double*>(smem + rl.off_kq) : g.logK;
+  c.krt = STAGE ? reinterpret_cast<const int32_t*>(smem + rl.off_kr) : g.kright;
+  c.ms_s = smem_u32(smem + rl.off_ms);
+  c.kq_s = smem_u32(smem + rl.off_kq);
+  c.G = t.G; c.CM = t.CM; c.NW = t.NW; c.nK = int(g.nK);
+  c.plane = g.nM * g.nN * g.nK;
+  return c;
+}
+
+// Prologue (thread 0): CTA-constant tables by TMA bulk copies on two
+// mbarriers, the small tables first (the staircase and W table need only
+// those), the per-k tables behind them.
+template <bool STAGE>
+__device__ __forceinline__ void row_prologue(uint8_t* smem, const RowCtx<STAGE>& c, const TablesDev& t,
+                                             const GridDev& g, const RowLaunch& rl, uint64_t* bar) {
+  mbar_expect_tx(bar, r16(8ll * t.R) + r16(8ll * c.G) + 2 * r16(8ll * c.CM) +
+                          r16(int64_t(sizeof(WcParam)) * c.NW));
+  bulk_g2s(c.clm, t.cls_lm, r16(8ll * c.CM), bar);
+  bulk_g2s(c.cln, t.cls_ln, r16(8ll * c.CM), bar);
+  bulk_g2s(c.wcp, t.wcp, r16(int64_t(sizeof(WcParam)) * c.NW), bar);
+  bulk_g2s(c.glk, t.grp_lk, r16(8ll * c.G), bar);
+  bulk_g2s(c.gcur, t.g_cw, r16(8ll * t.R), bar);
+  if (STAGE) {
+    mbar_expect_tx(bar + 1, r16(4ll * c.nK) + 2 * r16(8ll * c.nK) + r16(4ll * rl.nkc * c.G));
+    bulk_g2s(smem + rl.off_ms, g.mn_sorted, r16(8ll * c.nK), bar + 1);
+    bulk_g2s(smem + rl.off_kq, g.logK, r16(8ll * c.nK), bar + 1);
+    bulk_g2s(smem + rl.off_kr, g.kright, r16(4ll * rl.nkc * c.G), bar + 1);
+    bulk_g2s(smem + rl.off_kf, g.kfast, r16(4ll * c.nK), bar + 1);
+  }
+}
+
+// Tile coordinates: tile = (row * nbs + slab) * nkc + k chunk.
+struct TileXY {
+  int row, slab, kcx, k0, kc;
+};
+__device__ __forceinline__ TileXY tile_xy(const RowLaunch& rl, int tile, int nK) {
+  TileXY x;
+  const int rs = fdiv(tile, rl.d_nkc);
+  x.kcx = tile - rs * rl.nkc;
+  x.row = fdiv(rs, rl.d_nbs);
+  x.slab = rs - x.row * rl.nbs;
+  x.k0 = x.kcx * rl.kc;
+  x.kc = min(rl.kc, nK - x.k0);
+  return x;
+}
+
+// One tile's lookup state (one warp): staircase, wave-scale table, cut
+// points, byte maps, written into the slot `wb`; len / lastpos into its
+// header.
+template <int NB, bool STAGE, int SEGW>
+__device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev& g,
+                                           const RowLaunch& rl, const TileXY& x,
+                                           const RowIn<NB>& cur, uint8_t* wb, int lane,
+                                           int mark_tile = 1 << 30) {
+  uint64_t* sD = reinterpret_cast<uint64_t*>(wb + rl.w_sD);
+  int32_t* sP = reinterpret_cast<int32_t*>(wb + rl.w_sP);
+  double* W = reinterpret_cast<double*>(wb + rl.w_W);
+  int32_t* hdr = reinterpret_cast<int32_t*>(wb + rl.w_hdr);
+  const int CM = c.CM, NW = c.NW;
+  // ---- staircase: prefix minimum of D_j = max(|lm_j-qm|, |ln_j-qn|)
+  uint64_t dmin = ~0ull;
+  int len = 0, lastpos = 0;
+  auto dist = [&](int j) {
+    return umax64(abs_bits(__dsub_rn(c.clm[j], cur.qm)), abs_bits(__dsub_rn(c.cln[j], cur.qn)));
+  };
+  if (CM <= 64) {
+    // one warp scan: members 2*lane, 2*lane + 1 per lane
+    const int ja = 2 * lane, jb = ja + 1;
+    const uint64_t da = ja < CM ? dist(ja) : ~0ull, db = jb < CM ? dist(jb) : ~0ull;
+    uint64_t pm = umin64(da, db);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
+      if (lane >= off && o < pm) pm = o;
+    }
+    uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
+    if (lane == 0) excl = ~0ull;
+    const bool ra = ja < CM && da < excl;
+    const bool rb = jb < CM && db < umin64(excl, da);
+    const unsigned ma = __ballot_sync(0xFFFFFFFFu, ra), mb = __ballot_sync(0xFFFFFFFFu, rb);
+    const unsigned below = (1u << lane) - 1u;
+    const int pa = __popc(ma & below) + __popc(mb & below);
+    if (ra) { sD[pa] = da; sP[pa] = ja; }
+    if (rb) { sD[pa + ra] = db; sP[pa + ra] = jb; }
+    len = __popc(ma) + __popc(mb);
+    const int hi = 31 - __clz(ma | mb);  // ma | mb != 0: member 0 is a record
+    lastpos = ((mb >> hi) & 1u) ? 2 * hi + 1 : 2 * hi;
+    dmin = __shfl_sync(0xFFFFFFFFu, pm, 31);
+  } else for (int b0 = 0; b0 < CM; b0 += 32) {
+    const int j = b0 + lane;
+    const uint64_t d = j < CM ? dist(j) : ~0ull;
+    uint64_t pm = d;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
+      if (lane >= off && o < pm) pm = o;
+    }
+    uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
+    if (lane == 0) excl = ~0ull;
+    if (dmin < excl) excl = dmin;
+    const bool rec = j < CM && d < excl;
+    const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
+    if (rec) {
+      const int pos = len + __popc(mask & ((1u << lane) - 1u));
+      sD[pos] = d;
+      sP[pos] = j;
+    }
+    if (mask) lastpos = b0 + 31 - __clz(mask);
+    len += __popc(mask);
+    const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
+    if (tail < dmin) dmin = tail;
+  }
+  ROW_MARK(mark_tile, 5);
+  // ---- wave-scale table W[wave class][ib] of this (m, n) and batch slab
+  for (int wc = lane; wc < NW; wc += 32) {
+    const WcParam& p = c.wcp[wc];
+    const uint64_t tmn = wc < 64 ? cur.cm[wc >> 5] * cur.cn[wc >> 5]
+                                 : g.cm_tab[cur.im * NW + wc] * g.cn_tab[cur.jn * NW + wc];
+    const double rw = p.rw;
+#pragma unroll
+    for (int ib = 0; ib < NB; ++ib) {
+      const double w = __ull2double_rn(ceil_div_w(p, 2, cur.b[ib] * tmn, p.bpw));
+      W[wc * NB + ib] = rw == 1.0 ? w : __ddiv_rn(w, rw);
+    }
+  }
+  __syncwarp();
+  ROW_MARK(mark_tile, 6);
+  // ---- cut points: fixed-trip branch-free binary searches, one shared
+  // load per step, both kinds in one loop (lanes never diverge)
+  //   i < len : #{ranks r: mn(r) >= sD[i]} (i == len-1: > dmin); mn descends
+  //   i >= len: #{k: NOT (group i-len left of log2 k and farther than dmin)}
+  //             = kright + #{k >= kright: log2 k - lk <= dmin}
+  constexpr int SL = SEGW * 4;
+  int32_t* cut = reinterpret_cast<int32_t*>(wb + rl.w_cut);
+  {
+    const int k0 = x.k0, kc = x.kc;
+    int top = 1;
+    while (top * 2 <= kc) top *= 2;
+    for (int i = lane; i < len + c.G; i += 32) {
+      const bool rk = i < len, strict = i == len - 1;
+      const int gg = rk ? 0 : i - len;
+      const uint64_t xv = rk ? sD[i] : dmin;
+      const double lk = c.glk[gg];
+      const int kr = rk ? 0 : c.krt[x.kcx * c.G + gg];
+      int lo = 0;
+      for (int step = top; step; step >>= 1) {
+        const int r = k0 + min(lo + step, kc) - 1;
+        uint64_t v;
+        if (STAGE) v = lds_u64((rk ? c.ms_s : c.kq_s) + 8u * uint32_t(r));
+        else v = rk ? c.ms[r] : __double_as_longlong(c.kq[r]);
+        const bool keep = rk ? (v > xv || (!strict && v == xv))
+                             : (r - k0 < kr || abs_bits(__dsub_rn(__longlong_as_double(v), lk)) <= xv);
+        lo += (lo + step <= kc && keep) ? step : 0;
+      }
+      cut[i] = lo;
+    }
+  }
+  __syncwarp();
+  ROW_MARK(mark_tile, 7);
+  // ---- byte maps: map[r] = #{cuts <= r} (+ 0xFF from cut[len-1] on for
+  // the rank map), one lane per SL consecutive bytes: a broadcast count of
+  // the cuts before the segment, then SIMD increments for the few inside
+  {
+    constexpr int QW = SL / 8;  // u64 words per lane
+    constexpr uint64_t kOnes = 0x0101010101010101ull;
+    const int r0 = lane * SL;
+    const int nr = len - 1, ng = c.G, ff = cut[len - 1];
+    // first s with cut[s] > r0 in each cut list, both searches interleaved
+    int b0 = 0, h0 = nr, b1 = 0, h1 = ng;
+    const int32_t* cg = cut + len;
+    while (b0 < h0 || b1 < h1) {
+      const int m0 = (b0 + h0) >> 1, m1 = (b1 + h1) >> 1;
+      const bool a0 = b0 < h0, a1 = b1 < h1;
+      const int c0 = a0 ? cut[m0] : 0, c1 = a1 ? cg[m1] : 0;
+      if (a0) { if (c0 <= r0) b0 = m0 + 1; else h0 = m0; }
+      if (a1) { if (c1 <= r0) b1 = m1 + 1; else h1 = m1; }
+    }
+    uint64_t w0[QW], w1[QW];
+#pragma unroll
+    for (int q = 0; q < QW; ++q) {
+      w0[q] = uint64_t(b0) * kOnes;
+      w1[q] = uint64_t(b1) * kOnes;
+    }
+    auto bump = [&](uint64_t* w, int e) {
+#pragma unroll
+      for (int q = 0; q < QW; ++q) {
+        const int sh = e - 8 * q;  // bytes >= sh of word q count this cut
+        w[q] += sh <= 0 ? kOnes : sh >= 8 ? 0ull : (kOnes << (8 * sh));
+      }
+    };
+    for (int s = b0; s < nr; ++s) {
+      const int e = cut[s] - r0;
+      if (e >= SL) break;
+      bump(w0, e);
+    }
+    for (int s = b1; s < ng; ++s) {
+      const int e = cut[len + s] - r0;
+      if (e >= SL) break;
+      bump(w1, e);
+    }
+#pragma unroll
+    for (int q = 0; q < QW; ++q) {
+      const int sh = ff - r0 - 8 * q;
+      w0[q] |= sh <= 0 ? ~0ull : sh >= 8 ? 0ull : (~0ull << (8 * sh));
+    }
+    uint64_t* mw0 = reinterpret_cast<uint64_t*>(wb + rl.w_rmap) + lane * QW;
+    uint64_t* mw1 = reinterpret_cast<uint64_t*>(wb + rl.w_gmap) + lane * QW;
+#pragma unroll
+    for (int q = 0; q < QW; q += 2) {
+      *reinterpret_cast<ulonglong2*>(mw0 + q) = make_ulonglong2(w0[q], w0[q + 1]);
+      *reinterpret_cast<ulonglong2*>(mw1 + q) = make_ulonglong2(w1[q], w1[q + 1]);
+    }
+  }
+  if (lane == 0) {
+    hdr[0] = len;
+    hdr[1] = lastpos;
+  }
+}
+
+// Write one tile's points from its slot: 32-pair blocks b0, b0 + bstep, ...
+// (two adjacent k per lane, one 16-byte store per batch value), then the
+// exact-record hits that fall in those blocks.
+template <int NB, bool STAGE>
+__device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDev& t,
+                                          const GridDev& g, const RowLaunch& rl, const TileXY& x,
+                                          const uint8_t* wb, const double* __restrict__ base_tab,
+                                          const LaunchOut& out, int b0, int bstep, int lane) {
+  const int32_t* sP = reinterpret_cast<const int32_t*>(wb + rl.w_sP);
+  const double* W = reinterpret_cast<const double*>(wb + rl.w_W);
+  const uint8_t* rmap = wb + rl.w_rmap;
+  const uint8_t* gmap = wb + rl.w_gmap;
+  const int32_t* hdr = reinterpret_cast<const int32_t*>(wb + rl.w_hdr);
+  const int lastpos = hdr[1], CM = c.CM, nK = c.nK, k0 = x.k0;
+  const int64_t plane = c.plane;
+  double* const obase = out.lat + int64_t(x.slab * NB) * plane + int64_t(x.row) * nK + k0;
+  const double* const bbase = base_tab + k0;
+  const int nP = x.kc >> 1, nB = (nP + 31) >> 5;
+  auto lookup = [&](uint32_t kf, int ikl) -> int2 {
+    const uint32_t sb = rmap[kf & 0xFFFFu];
+    const bool a = sb == 0xFFu;
+    const int gg = a ? int(gmap[ikl]) : int((kf >> 16) & 0xFFu);
+    const int pos = a ? lastpos : sP[sb];
+    return c.gcur[gg * CM + pos];  // one class: group g's members at g * CM
+  };
+  constexpr int U = 4;
+  for (int bq = b0; bq < nB; bq += U * bstep) {  // warp-uniform trip count (__all_sync)
+    int2 v[U][2];
+    int pp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      pp[u] = (bq + u * bstep) * 32 + lane;
+      const int p = min(pp[u], nP - 1);
+      const uint2 kf = *reinterpret_cast<const uint2*>(c.kfs + k0 + 2 * p);
+      v[u][0] = lookup(kf.x, 2 * p);
+      v[u][1] = lookup(kf.y, 2 * p + 1);
+    }
+    bool all_ok = true;
+#pragma unroll
+    for (int u = 0; u < U; ++u) all_ok = all_ok && v[u][0].x >= 0 && v[u][1].x >= 0;
+    if (__all_sync(0xFFFFFFFFu, all_ok)) {
+      double bv[U][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = min(pp[u], nP - 1);
+        bv[u][0] = bbase[v[u][0].x * nK + 2 * p];
+        bv[u][1] = bbase[v[u][1].x * nK + 2 * p + 1];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = pp[u];
+        if (p >= nP) continue;
+        double* o = obase + 2 * p;
+        const double* w0 = W + v[u][0].y * NB;
+        const double* w1 = W + v[u][1].y * NB;
+#pragma unroll
+        for (int ib = 0; ib < NB; ib += (NB >= 2 ? 2 : 1)) {
+          double a0, a1, b0v, b1v;
+          if (NB >= 2) {
+            const double2 xw = *reinterpret_cast<const double2*>(w0 + ib);
+            const double2 yw = *reinterpret_cast<const double2*>(w1 + ib);
+            a0 = xw.x; a1 = xw.y; b0v = yw.x; b1v = yw.y;
+          } else {
+            a0 = w0[ib]; b0v = w1[ib]; a1 = b1v = 0.0;
+          }
+          *reinterpret_cast<double2*>(o + ib * plane) =
+              make_double2(__dmul_rn(bv[u][0], a0), __dmul_rn(bv[u][1], b0v));
+          if (NB >= 2)
+            *reinterpret_cast<double2*>(o + (ib + 1) * plane) =
+                make_double2(__dmul_rn(bv[u][0], a1), __dmul_rn(bv[u][1], b1v));
+        }
+      }
+    } else {
+      // some k resolves to a record without a curve: NaN + statistics
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = pp[u];
+        if (p >= nP) continue;
+        double* o = obase + 2 * p;
+        const bool ok0 = v[u][0].x >= 0, ok1 = v[u][1].x >= 0;
+        const double bb0 = ok0 ? bbase[v[u][0].x * nK + 2 * p] : 0.0;
+        const double bb1 = ok1 ? bbase[v[u][1].x * nK + 2 * p + 1] : 0.0;
+        if (!(ok0 && ok1) && out.nan_stats) {
+          atomicMin(out.nan_stats, (unsigned long long)(o - out.lat + (ok0 ? 1 : 0)));
+          atomicAdd(out.nan_stats + 1, (unsigned long long)(NB * (2 - ok0 - ok1)));
+        }
+        const double* w0 = W + (ok0 ? v[u][0].y : 0) * NB;
+        const double* w1 = W + (ok1 ? v[u][1].y : 0) * NB;
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib)
+          *reinterpret_cast<double2*>(o + ib * plane) =
+              make_double2(ok0 ? __dmul_rn(bb0, w0[ib]) : qnan(), ok1 ? __dmul_rn(bb1, w1[ib]) : qnan());
+      }
+    }
+  }
+  // exact-record hits in these blocks take priority over the nearest result
+  // (_kernels.pyx:107-110): re-count them by their exact result
+  const int f0 = g.fixr_off[x.row], f1 = g.fixr_off[x.row + 1];
+  if (f1 > f0) {
+    __syncwarp();  // this warp's stores above are visible to every lane
+    for (int f = f0 + lane; f < f1; f += 32) {
+      const FixEntry fe = g.fixr[f];
+      const int ikl = fe.ik - k0;
+      if (ikl < 0 || ikl >= x.kc || fe.ib < x.slab * NB || fe.ib >= x.slab * NB + NB) continue;
+      if (((ikl >> 6) - b0) % bstep != 0 || (ikl >> 6) < b0) continue;  // another warp's block
+      double* o = out.lat + int64_t(fe.ib) * plane + int64_t(x.row) * nK + fe.ik;
+      const int ci = fe.curve;
+      if (out.nan_stats) {
+        const bool was_nan = *o != *o;
+        if (was_nan && ci >= 0) {
+          atomicAdd(out.nan_stats + 1, ~0ull);
+          atomicOr(out.nan_stats + 2, 1ull);
+        }
+        if (!was_nan && ci < 0) {
+          atomicAdd(out.nan_stats + 1, 1ull);
+          atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
+        }
+      }
+      if (ci < 0) {
+        *o = qnan();
+      } else {
+        const uint64_t* c4 = g.fix_coord + 4 * int64_t(fe.fix);
+        *o = predict_point(t, ci, c4[0], c4[1], c4[2], c4[3], base_tab[ci * nK + fe.ik]).lat;
+      }
+    }
+  }
+}
+
+// Warp-autonomous variant: each warp builds and writes its own tiles.
 template <int NB, bool STAGE, int SEGW>
 __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t, GridDev g,
                                                                     RowLaunch rl,
                                                                     const double* __restrict__ base_tab,
                                                                     LaunchOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
-  int2* gcur = reinterpret_cast<int2*>(smem + rl.off_gcur);
-  double* glk = reinterpret_cast<double*>(smem + rl.off_glk);
-  double* clm = reinterpret_cast<double*>(smem + rl.off_clm);
-  double* cln = reinterpret_cast<double*>(smem + rl.off_cln);
-  WcParam* wcp = reinterpret_cast<WcParam*>(smem + rl.off_wcp);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + rl.off_bar);  // [0] tables, [1] per-k
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   ROW_MARK(blockIdx.x * kRowWarps + warp, 0);
-  const int G = t.G, CM = t.CM, NW = t.NW, nK = int(g.nK);
-  const uint32_t* kfs = STAGE ? reinterpret_cast<const uint32_t*>(smem + rl.off_kf) : g.kfast;
-  const int32_t* krt = STAGE ? reinterpret_cast<const int32_t*>(smem + rl.off_kr) : g.kright;
-  // prologue: CTA-constant tables by TMA bulk copies on two mbarriers, the
-  // small tables first (the staircase and W table need only those), the
-  // per-k tables behind them
+  const RowCtx<STAGE> c = row_ctx<STAGE>(smem, t, g, rl);
   if (tid == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar, r16(8ll * t.R) + r16(8ll * G) + 2 * r16(8ll * CM) +
-                            r16(int64_t(sizeof(WcParam)) * NW));
-    bulk_g2s(clm, t.cls_lm, r16(8ll * CM), bar);
-    bulk_g2s(cln, t.cls_ln, r16(8ll * CM), bar);
-    bulk_g2s(wcp, t.wcp, r16(int64_t(sizeof(WcParam)) * NW), bar);
-    bulk_g2s(glk, t.grp_lk, r16(8ll * G), bar);
-    bulk_g2s(gcur, t.g_cw, r16(8ll * t.R), bar);
-    if (STAGE) {
-      mbar_expect_tx(bar + 1, r16(4ll * nK) + 2 * r16(8ll * nK) + r16(4ll * rl.nkc * G));
-      bulk_g2s(smem + rl.off_ms, g.mn_sorted, r16(8ll * nK), bar + 1);
-      bulk_g2s(smem + rl.off_kq, g.logK, r16(8ll * nK), bar + 1);
-      bulk_g2s(smem + rl.off_kr, g.kright, r16(4ll * rl.nkc * G), bar + 1);
-      bulk_g2s(smem + rl.off_kf, g.kfast, r16(4ll * nK), bar + 1);
-    }
+    row_prologue<STAGE>(smem, c, t, g, rl, bar);
   }
   int tile = blockIdx.x * kRowWarps + warp;
-  RowIn<NB> rin = load_row_in<NB>(g, rl, min(tile, rl.tiles - 1));  // in flight during the wait
+  RowIn<NB> rin = load_row_in<NB>(g, rl, min(tile, rl.tiles - 1), t.NW, lane);  // in flight during the wait
   __syncthreads();  // mbarriers initialised before anyone waits on them
   mbar_wait(bar, 0);
-  const uint32_t ms_s = smem_u32(smem + rl.off_ms), kq_s = smem_u32(smem + rl.off_kq);
   uint8_t* wb = smem + rl.off_warp + warp * rl.warp_bytes;
-  uint64_t* sD = reinterpret_cast<uint64_t*>(wb + rl.w_sD);
-  int32_t* sP = reinterpret_cast<int32_t*>(wb + rl.w_sP);
-  int32_t* cut = reinterpret_cast<int32_t*>(wb + rl.w_cut);
-  double* W = reinterpret_cast<double*>(wb + rl.w_W);
-  uint8_t* rmap = wb + rl.w_rmap;
-  uint8_t* gmap = wb + rl.w_gmap;
-  const int64_t plane = g.nM * g.nN * g.nK;
   bool waited = false, staged = !STAGE;
   for (; tile < rl.tiles; tile += gridDim.x * kRowWarps) {
-    const int kcx = tile % rl.nkc, rs = tile / rl.nkc;
-    const int slab = rs % rl.nbs, row = rs / rl.nbs;
-    const int k0 = kcx * rl.kc, kc = min(rl.kc, nK - k0);
+    const TileXY x = tile_xy(rl, tile, c.nK);
     const RowIn<NB> cur = rin;
     {
       const int nt = tile + gridDim.x * kRowWarps;
-      if (nt < rl.tiles) rin = load_row_in<NB>(g, rl, nt);  // next tile's scalars
+      if (nt < rl.tiles) rin = load_row_in<NB>(g, rl, nt, t.NW, lane);  // next tile's scalars
     }
     ROW_MARK(tile, 1);
-    // ---- staircase: prefix minimum of D_j = max(|lm_j-qm|, |ln_j-qn|)
-    uint64_t dmin = ~0ull;
-    int len = 0, lastpos = 0;
-    for (int b0 = 0; b0 < CM; b0 += 32) {
-      const int j = b0 + lane;
-      const uint64_t d = j < CM ? umax64(abs_bits(__dsub_rn(clm[j], cur.qm)),
-                                         abs_bits(__dsub_rn(cln[j], cur.qn)))
-                                : ~0ull;
-      uint64_t pm = d;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pm, off);
-        if (lane >= off && o < pm) pm = o;
-      }
-      uint64_t excl = __shfl_up_sync(0xFFFFFFFFu, pm, 1);
-      if (lane == 0) excl = ~0ull;
-      if (dmin < excl) excl = dmin;
-      const bool rec = j < CM && d < excl;
-      const unsigned mask = __ballot_sync(0xFFFFFFFFu, rec);
-      if (rec) {
-        const int pos = len + __popc(mask & ((1u << lane) - 1u));
-        sD[pos] = d;
-        sP[pos] = j;
-      }
-      if (mask) lastpos = b0 + 31 - __clz(mask);
-      len += __popc(mask);
-      const uint64_t tail = __shfl_sync(0xFFFFFFFFu, pm, 31);
-      if (tail < dmin) dmin = tail;
-    }
-    ROW_MARK(tile, 2);
-    // ---- wave-scale table W[wave class][ib] of this (m, n) and batch slab;
-    // independent entries, unrolled for ILP
-#pragma unroll 2
-    for (int wc = lane; wc < NW; wc += 32) {
-      const WcParam p = wcp[wc];
-      const uint64_t tmn = ceil_div_w(p, 0, cur.m, p.tm) * ceil_div_w(p, 1, cur.n, p.tn) * p.sk;
-#pragma unroll
-      for (int ib = 0; ib < NB; ++ib) {
-        const double w = __ull2double_rn(ceil_div_w(p, 2, cur.b[ib] * tmn, p.bpw));
-        W[wc * NB + ib] = p.rw == 1.0 ? w : __ddiv_rn(w, p.rw);
-      }
-    }
-    __syncwarp();
-    ROW_MARK(tile, 3);
     if (!staged) {
       mbar_wait(bar + 1, 0);
       staged = true;
     }
-    // ---- cut points: fixed-trip branch-free binary searches, one shared
-    // load per step, both kinds in one loop (lanes never diverge)
-    //   i < len : #{ranks r: mn(r) >= sD[i]} (i == len-1: > dmin); mn descends
-    //   i >= len: #{k: NOT (group i-len left of log2 k and farther than dmin)}
-    //             = kright + #{k >= kright: log2 k - lk <= dmin}
-    int top = 1;
-    while (top * 2 <= kc) top *= 2;
-    for (int i = lane; i < len + G; i += 32) {
-      const bool rk = i < len, strict = i == len - 1;
-      const int gg = rk ? 0 : i - len;
-      const uint64_t x = rk ? sD[i] : dmin;
-      const double lk = glk[gg];
-      const int kr = rk ? 0 : krt[kcx * G + gg];
-      int lo = 0;
-      for (int step = top; step; step >>= 1) {
-        const int r = k0 + min(lo + step, kc) - 1;
-        uint64_t v;
-        if (STAGE) v = lds_u64((rk ? ms_s : kq_s) + 8u * uint32_t(r));
-        else v = rk ? g.mn_sorted[r] : __double_as_longlong(g.logK[r]);
-        const bool keep = rk ? (v > x || (!strict && v == x))
-                             : (r - k0 < kr || abs_bits(__dsub_rn(__longlong_as_double(v), lk)) <= x);
-        lo += (lo + step <= kc && keep) ? step : 0;
-      }
-      cut[i] = lo;
-    }
-    __syncwarp();
-    ROW_MARK(tile, 4);
-    build_count_map<SEGW>(rmap, cut, len - 1, cut[len - 1], lane);
-    build_count_map<SEGW>(gmap, cut + len, G, -1, lane);
+    build_tile<NB, STAGE, SEGW>(c, g, rl, x, cur, wb, lane);
     __syncwarp();
     ROW_MARK(tile, 5);
     if (!waited) {
@@ -846,122 +1107,90 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t
       waited = true;
     }
     ROW_MARK(tile, 6);
-    // ---- points: two adjacent k per lane (16-byte stores), U pairs in flight
-    double* const obase = out.lat + int64_t(slab * NB) * plane + int64_t(row) * nK + k0;
-    const double* const bbase = base_tab + k0;
-    const int nP = kc >> 1;
-    auto lookup = [&](uint32_t kf, int ikl) -> int2 {
-      const uint32_t sb = rmap[kf & 0xFFFFu];
-      const bool a = sb == 0xFFu;
-      const int gg = a ? int(gmap[ikl]) : int((kf >> 16) & 0xFFu);
-      const int pos = a ? lastpos : sP[sb];
-      return gcur[gg * CM + pos];  // one class: group g's members at g * CM
-    };
-    constexpr int U = 4;
-    for (int q0 = 0; q0 < nP; q0 += 32 * U) {  // warp-uniform trip count (__all_sync)
-      const int p0 = q0 + lane;
-      int2 v[U][2];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int p = min(p0 + 32 * u, nP - 1);
-        const uint2 kf = *reinterpret_cast<const uint2*>(kfs + k0 + 2 * p);
-        v[u][0] = lookup(kf.x, 2 * p);
-        v[u][1] = lookup(kf.y, 2 * p + 1);
-      }
-      bool all_ok = true;
-#pragma unroll
-      for (int u = 0; u < U; ++u) all_ok = all_ok && v[u][0].x >= 0 && v[u][1].x >= 0;
-      if (__all_sync(0xFFFFFFFFu, all_ok)) {
-        double bv[U][2];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int p = min(p0 + 32 * u, nP - 1);
-          bv[u][0] = bbase[v[u][0].x * nK + 2 * p];
-          bv[u][1] = bbase[v[u][1].x * nK + 2 * p + 1];
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int p = p0 + 32 * u;
-          if (p >= nP) break;
-          double* o = obase + 2 * p;
-          const double* w0 = W + v[u][0].y * NB;
-          const double* w1 = W + v[u][1].y * NB;
-#pragma unroll
-          for (int ib = 0; ib < NB; ib += (NB >= 2 ? 2 : 1)) {
-            double a0, a1, b0, b1;
-            if (NB >= 2) {
-              const double2 x = *reinterpret_cast<const double2*>(w0 + ib);
-              const double2 y = *reinterpret_cast<const double2*>(w1 + ib);
-              a0 = x.x; a1 = x.y; b0 = y.x; b1 = y.y;
-            } else {
-              a0 = w0[ib]; b0 = w1[ib]; a1 = b1 = 0.0;
-            }
-            *reinterpret_cast<double2*>(o + ib * plane) =
-                make_double2(__dmul_rn(bv[u][0], a0), __dmul_rn(bv[u][1], b0));
-            if (NB >= 2)
-              *reinterpret_cast<double2*>(o + (ib + 1) * plane) =
-                  make_double2(__dmul_rn(bv[u][0], a1), __dmul_rn(bv[u][1], b1));
-          }
-        }
-      } else {
-        // some k resolves to a record without a curve: NaN + statistics
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int p = p0 + 32 * u;
-          if (p >= nP) break;
-          double* o = obase + 2 * p;
-          const bool ok0 = v[u][0].x >= 0, ok1 = v[u][1].x >= 0;
-          const double b0 = ok0 ? bbase[v[u][0].x * nK + 2 * p] : 0.0;
-          const double b1 = ok1 ? bbase[v[u][1].x * nK + 2 * p + 1] : 0.0;
-          if (!(ok0 && ok1) && out.nan_stats) {
-            atomicMin(out.nan_stats, (unsigned long long)(o - out.lat + (ok0 ? 1 : 0)));
-            atomicAdd(out.nan_stats + 1, (unsigned long long)(NB * (2 - ok0 - ok1)));
-          }
-          const double* w0 = W + (ok0 ? v[u][0].y : 0) * NB;
-          const double* w1 = W + (ok1 ? v[u][1].y : 0) * NB;
-#pragma unroll
-          for (int ib = 0; ib < NB; ++ib)
-            *reinterpret_cast<double2*>(o + ib * plane) =
-                make_double2(ok0 ? __dmul_rn(b0, w0[ib]) : qnan(), ok1 ? __dmul_rn(b1, w1[ib]) : qnan());
-        }
-      }
-    }
-    // exact-record hits of this tile take priority over the nearest result
-    // (_kernels.pyx:107-110): re-count them by their exact result
-    {
-      const int f0 = g.fixr_off[row], f1 = g.fixr_off[row + 1];
-      if (f1 > f0) {
-        __syncwarp();  // this warp's stores above are visible to every lane
-        for (int f = f0 + lane; f < f1; f += 32) {
-          const FixEntry fe = g.fixr[f];
-          if (fe.ik < k0 || fe.ik >= k0 + kc || fe.ib < slab * NB || fe.ib >= slab * NB + NB) continue;
-          double* o = out.lat + int64_t(fe.ib) * plane + int64_t(row) * nK + fe.ik;
-          const int ci = fe.curve;
-          if (out.nan_stats) {
-            const bool was_nan = *o != *o;
-            if (was_nan && ci >= 0) {
-              atomicAdd(out.nan_stats + 1, ~0ull);
-              atomicOr(out.nan_stats + 2, 1ull);
-            }
-            if (!was_nan && ci < 0) {
-              atomicAdd(out.nan_stats + 1, 1ull);
-              atomicMin(out.nan_stats, (unsigned long long)(o - out.lat));
-            }
-          }
-          if (ci < 0) {
-            *o = qnan();
-          } else {
-            const uint64_t* c4 = g.fix_coord + 4 * int64_t(fe.fix);
-            *o = predict_point(t, ci, c4[0], c4[1], c4[2], c4[3], base_tab[ci * nK + fe.ik]).lat;
-          }
-        }
-      }
-    }
+    emit_tile<NB, STAGE>(c, t, g, rl, x, wb, base_tab, out, 0, 1, lane);
     __syncwarp();  // the warp's state buffers are rewritten by the next tile
     ROW_MARK(tile, 7);
   }
   if (!staged) mbar_wait(bar + 1, 0);  // never exit with bulk copies in flight
   if (!waited) pdl_wait();
+}
+
+// Producer/consumer variant: kRingProd builder warps fill kRingSlots
+// shared-memory slots (mbarrier FULL/EMPTY per slot) with tile states, in
+// the CTA's tile order; the other warps write the points, each taking every
+// (kRowWarps - kRingProd)-th 32-pair block of a tile.  Writing starts after
+// one tile's build and later builds proceed under the store stream.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int NB, bool STAGE, int SEGW>
+__global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev t, GridDev g,
+                                                                     RowLaunch rl,
+                                                                     const double* __restrict__ base_tab,
+                                                                     LaunchOut out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + rl.off_bar);  // [0] tables, [1] per-k
+  const int P = rl.prod, S = rl.slots, NC = kRowWarps - P;
+  uint64_t* full = bar + 2;
+  uint64_t* empty = full + S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const RowCtx<STAGE> c = row_ctx<STAGE>(smem, t, g, rl);
+#ifdef PM2L_TIMING
+  const unsigned long long t_entry = clock64();
+#endif
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 32);
+      mbar_init(empty + s, 32 * NC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    row_prologue<STAGE>(smem, c, t, g, rl, bar);
+  }
+  __syncthreads();  // mbarriers initialised before anyone waits on them
+  if (warp < P) {
+    int j = warp;
+    int tile = blockIdx.x + j * gridDim.x;
+    RowIn<NB> rin = load_row_in<NB>(g, rl, min(tile, rl.tiles - 1), t.NW, lane);
+    mbar_wait(bar, 0);
+    if (STAGE) mbar_wait(bar + 1, 0);
+    for (; tile < rl.tiles; j += P, tile += P * gridDim.x) {
+      const int slot = j % S, use = j / S;
+      const RowIn<NB> cur = rin;
+      {
+        const int nt = tile + P * gridDim.x;
+        if (nt < rl.tiles) rin = load_row_in<NB>(g, rl, nt, t.NW, lane);
+      }
+      if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
+#ifdef PM2L_TIMING
+      if (lane == 0 && tile < 16384) g_row_dbg[tile * 8] = t_entry;
+#endif
+      ROW_MARK(tile, 1);
+      build_tile<NB, STAGE, SEGW>(c, g, rl, tile_xy(rl, tile, c.nK), cur,
+                                  smem + rl.off_warp + slot * rl.warp_bytes, lane, tile);
+      __syncwarp();
+      ROW_MARK(tile, 2);
+      mbar_arrive(full + slot);
+    }
+  } else {
+    const int cw = warp - P;
+    mbar_wait(bar, 0);
+    if (STAGE) mbar_wait(bar + 1, 0);
+    pdl_wait();  // base table complete and visible
+    for (int j = 0, tile = blockIdx.x; tile < rl.tiles; ++j, tile += gridDim.x) {
+      const int slot = j % S, use = j / S;
+      mbar_wait(full + slot, use & 1);
+      if (cw == 0) ROW_MARK(tile, 3);
+      emit_tile<NB, STAGE>(c, t, g, rl, tile_xy(rl, tile, c.nK),
+                           smem + rl.off_warp + slot * rl.warp_bytes, base_tab, out, cw, NC,
+                           lane);
+      __syncwarp();
+      if (cw == 0) ROW_MARK(tile, 4);
+      mbar_arrive(empty + slot);
+    }
+  }
 }
 
 // Exact-record hits take priority over the nearest result (_kernels.pyx:107-110).
@@ -1124,18 +1353,29 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
       (reinterpret_cast<uintptr_t>(out.lat) & 15) != 0 || t.CM > 254 || t.CM < 1 ||
       g.nM * g.nN > 0x7FFFFFFFll)
     return rl;
+  if (!g.cm_tab || t.NW < 1) return rl;
   int NB = 8;
   while (nb % NB) NB >>= 1;
   rl.nbs = int(nb / NB);
   rl.kc = int(std::min<int64_t>(g.nK, kKChunk));
   rl.nkc = int((g.nK + rl.kc - 1) / rl.kc);
+  rl.d_nkc = fast_div_for(uint32_t(rl.nkc));
+  rl.d_nbs = fast_div_for(uint32_t(rl.nbs));
+  rl.d_nN = fast_div_for(uint32_t(g.nN));
   const bool stage_k = g.nK <= kKChunk;
+  rl.ring = 1;
+  rl.prod = kRingProd;
+  rl.slots = kRingSlots;
+  if (const char* e = std::getenv("PM2L_ROW_RING")) rl.ring = std::atoi(e);  // experiments
+  if (const char* e = std::getenv("PM2L_RING_PROD")) rl.prod = std::min(std::max(std::atoi(e), 1), kRowWarps - 1);
+  if (const char* e = std::getenv("PM2L_RING_SLOTS")) rl.slots = std::min(std::max(std::atoi(e), 1), kRingMaxSlots);
   const int64_t tiles = g.nM * g.nN * rl.nbs * rl.nkc;
   if (tiles > 0x7FFFFFFFll || t.G + t.CM > 4096) return rl;
   row_layout(t, g, NB, stage_k, rl);
   if (rl.smem > 200 * 1024) return rl;
   rl.tiles = int(tiles);
   rl.ctas = int(std::min<int64_t>((tiles + kRowWarps - 1) / kRowWarps, 148 * 3));
+  if (rl.ring) rl.ctas = int(std::min<int64_t>(tiles, 148 * 3));
   if (const char* e = std::getenv("PM2L_ROW_CTAS")) {  // tuning experiments only
     const int v = std::atoi(e);
     if (v > 0) rl.ctas = std::min(rl.ctas, v);
@@ -1147,7 +1387,7 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
 template <int NB, bool STAGE, int SEGW>
 cudaError_t launch_rows_k(const TablesDev& t, const GridDev& g, const RowLaunch& rl,
                           const double* base, const LaunchOut& out, cudaStream_t s) {
-  auto* fn = grid_row_kernel<NB, STAGE, SEGW>;
+  auto* fn = rl.ring ? grid_ring_kernel<NB, STAGE, SEGW> : grid_row_kernel<NB, STAGE, SEGW>;
   if (rl.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rl.smem));
     if (e != cudaSuccess) return e;

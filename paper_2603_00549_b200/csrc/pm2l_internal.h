@@ -90,6 +90,11 @@ struct TablesDev {
 // k chunk of the one-class lookup kernel: ranks of the per-k distance are
 // taken inside chunks of this many k values (one warp's byte maps)
 constexpr int kKChunk = 2048;
+// byte-map bytes per lane for a k axis of nK values (16, 32 or 64)
+inline int64_t kmap_lane_bytes(int64_t nK) {
+  const int64_t kc = nK < kKChunk ? nK : kKChunk;
+  return ((kc + 511) / 512) * 16;
+}
 
 // Per-k sweep info, 16 B (one 128-bit load in the grid kernel).
 struct alignas(16) KInfo {
@@ -129,6 +134,9 @@ struct GridDev {
   const uint64_t* mn_sorted = nullptr;
   // [chunks x G]: first chunk-local k index with start(ik) > g
   const int32_t* kright = nullptr;
+  // all-GEMM tables: [nM x NW] ceil(m / tile_m), [nN x NW] ceil(n / tile_n) * split_k
+  const uint64_t* cm_tab = nullptr;
+  const uint64_t* cn_tab = nullptr;
   // exact-hit fix-ups: slice-relative flat index + coordinates + curve
   int64_t n_fix = 0;
   const int64_t* fix_pos = nullptr;

@@ -333,6 +333,22 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   // group attaining it (gB), and rank(k) in the stable descending order of
   // mn.  A row's cut points are thresholds on that order.  Same IEEE
   // subtraction and |.| as the device (host double, no contraction).
+  // per (m value, wave class): ceil(m / tile_m); per (n value, wave class):
+  // ceil(n / tile_n) * split_k -- the row kernel's W table inputs (u64,
+  // wrapping exactly like the reference's block product, _kernels.pyx:126)
+  std::vector<uint64_t> cm_tab, cn_tab;
+  if (tt.all_gemm && tt.NW > 0) {
+    const WcParam* wcp = reinterpret_cast<const WcParam*>(
+        th.blob.data() + reinterpret_cast<uintptr_t>(tt.wcp));
+    cm_tab.resize(size_t(nM) * tt.NW);
+    cn_tab.resize(size_t(nN) * tt.NW);
+    for (int64_t i = 0; i < nM; ++i)
+      for (int w = 0; w < tt.NW; ++w)
+        cm_tab[i * tt.NW + w] = (axes[1][i] + wcp[w].tm - 1) / wcp[w].tm;
+    for (int64_t j = 0; j < nN; ++j)
+      for (int w = 0; w < tt.NW; ++w)
+        cn_tab[j * tt.NW + w] = ((axes[2][j] + wcp[w].tn - 1) / wcp[w].tn) * wcp[w].sk;
+  }
   std::vector<uint32_t> kfast;
   std::vector<uint64_t> mn_sorted;
   std::vector<int32_t> kright;
@@ -362,16 +378,6 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
     }
     kfast.resize(nK);
     mn_sorted.resize(nK);
-    // per (chunk, group): first chunk-local k index whose log2 k lies right
-    // of the group (start(ik) > g)
-    for (int64_t k0 = 0; k0 < nK; k0 += kKChunk) {
-      const int64_t k1 = std::min<int64_t>(nK, k0 + kKChunk);
-      for (int g = 0; g < G; ++g) {
-        int64_t i = k0;
-        while (i < k1 && kinfo[i].start <= g) ++i;
-        kright.push_back(int32_t(i - k0));
-      }
-    }
     for (int64_t k0 = 0; k0 < nK; k0 += kKChunk) {
       const int64_t k1 = std::min<int64_t>(nK, k0 + kKChunk);
       std::vector<int32_t> ord(k1 - k0);
@@ -381,6 +387,16 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
         const int32_t i = ord[r];
         mn_sorted[k0 + r] = mn[i];
         kfast[i] = uint32_t(r) | (uint32_t(gB[i]) << 16) | (uint32_t(kinfo[i].start) << 24);
+      }
+    }
+    // per (chunk, group): first chunk-local k index whose log2 k lies right
+    // of the group (start(ik) > g)
+    for (int64_t k0 = 0; k0 < nK; k0 += kKChunk) {
+      const int64_t k1 = std::min<int64_t>(nK, k0 + kKChunk);
+      for (int g = 0; g < G; ++g) {
+        int64_t i = k0;
+        while (i < k1 && kinfo[i].start <= g) ++i;
+        kright.push_back(int32_t(i - k0));
       }
     }
   }
@@ -463,6 +479,8 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   g.kfast = fast_ok ? blob.add(kfast) : nullptr;
   g.mn_sorted = fast_ok ? blob.add(mn_sorted) : nullptr;
   g.kright = fast_ok ? blob.add(kright) : nullptr;
+  g.cm_tab = cm_tab.empty() ? nullptr : blob.add(cm_tab);
+  g.cn_tab = cn_tab.empty() ? nullptr : blob.add(cn_tab);
   g.n_fix = int64_t(fix_pos.size());
   g.fix_pos = blob.add(fix_pos);
   g.fix_coord = blob.add(fix_coord);
@@ -483,6 +501,10 @@ GridDev rebase(const GridDev& o, const void* base) {
     g.kfast = shift(o.kfast, base);
     g.mn_sorted = shift(o.mn_sorted, base);
     g.kright = shift(o.kright, base);
+  }
+  if (o.cm_tab) {
+    g.cm_tab = shift(o.cm_tab, base);
+    g.cn_tab = shift(o.cn_tab, base);
   }
   g.fix_pos = shift(o.fix_pos, base);
   g.fix_coord = shift(o.fix_coord, base); g.fix_curve = shift(o.fix_curve, base);

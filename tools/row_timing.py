@@ -60,6 +60,17 @@ def main():
     # SM clock64 stamps: per-tile differences only (clocks differ across SMs)
     mhz = float(os.environ.get("SM_MHZ", "1965"))
     rel = (t - t[:, :1]) / mhz
+    if os.environ.get("PM2L_ROW_RING", "1") != "0":
+        # ring kernel: 0 CTA entry, 1 build start, 2 build end, 3 emit start, 4 emit end
+        names = ["entry", "build start", "build end", "emit start", "emit end"]
+        for i in range(1, 5):
+            print(f"{names[i]:<12} (from CTA entry) median {np.median(rel[:, i]):6.2f}  "
+                  f"p10 {np.percentile(rel[:, i], 10):6.2f}  p90 {np.percentile(rel[:, i], 90):6.2f}  max {rel[:, i].max():6.2f}")
+        d = lambda a, b: np.median(rel[:, b] - rel[:, a])  # noqa: E731
+        print(f"build: staircase {d(1, 5):.2f}  W {d(5, 6):.2f}  cuts {d(6, 7):.2f}  maps {d(7, 2):.2f}")
+        print("build dur median", np.median(rel[:, 2] - rel[:, 1]), " emit dur median",
+              np.median(rel[:, 4] - rel[:, 3]), " wait full median", np.median(rel[:, 3] - rel[:, 2]))
+        return
     names = ["entry", "prologue", "staircase", "W table", "cuts", "maps", "pdl wait", "emit"]
     print("phase            median_us   p90_us   max_us")
     for i in range(1, 8):
