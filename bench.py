@@ -56,6 +56,16 @@ def grid_for(world: int):
         "n": tuple(range(96, 96 + 53 * 50, 53)), "k": tuple(range(32, 32 + 17 * 1000, 17))})
 
 
+def c2_config(world: int, n_pts: int = 10_000_000):
+    return {"workload": "C2: BF16 matmul NN grid 4x50x50x1000 = 10M (b,m,n,k) points "
+                        "per GPU vs bf16 seed-11 tables (540 recorded configs, 60 kernels)",
+            "points_per_gpu": n_pts, "global_points": world * n_pts,
+            "parallelism": f"dp{world}: contiguous batch-slab shards, "
+                           f"all-gather of first-NaN/count stats",
+            "l2": "flushed between steps (256 MiB write, outside event window)",
+            "output": "f64 latency per point, canonical order, HBM-resident"}
+
+
 def load_bf16():
     from paper_2603_00549_b200 import load_dataset
     return load_dataset(os.path.join(ROOT, "tests", "golden", "datasets", "bf16.json"))
@@ -85,9 +95,12 @@ def time_reference(steps: int, warmup: int):
     mod = oracle.reference_kernels()
     ncpu = len(os.sched_getaffinity(0))
     if mod is not None:
-        jobs = max(1, min(ncpu, len(axes[0])))
+        # the reference's own pool threads only the batch axis (backend.py:78-82,
+        # 4 values here); to give it every host core, its unmodified Cython
+        # kernel is called on (batch value x m range) sub-grids from ncpu threads
+        jobs = ncpu
         kind = "reference"
-        fn = lambda: oracle.reference_predict_grid(mod, prep.tables(), axes, jobs=jobs)  # noqa
+        fn = lambda: oracle.reference_predict_grid_tiles(mod, prep.tables(), axes, jobs)  # noqa
     else:
         jobs = 1
         kind = "port"
@@ -100,7 +113,7 @@ def time_reference(steps: int, warmup: int):
         fn()
         rates.append(g.cardinality / (time.perf_counter() - t0))
     sample = (f"{g.cardinality} points (C2 grid restricted to the first 12 of 50 m values), "
-              f"{'reference Cython predict_grid_slice, ' + str(jobs) + ' batch-slab threads' if kind == 'reference' else 'C oracle port, 1 thread'}"
+              f"{'reference Cython predict_grid_slice (unmodified) on (batch value x m range) sub-grids, ' + str(jobs) + ' threads' if kind == 'reference' else 'C oracle port, 1 thread'}"
               f" on {ncpu} visible cores")
     return rates, {"kind": kind, "cores": jobs, "sample": sample}
 
@@ -195,8 +208,9 @@ def run_reference(args, rank):
             "ms_per_step": 1e3 * cpu_sample_grid().cardinality / value,
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": value / PUBLISHED_PRED_PER_S, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 BF16 matmul NN sweep (CPU sample, see cpu_baseline)",
-                       "points": cpu_sample_grid().cardinality},
+            "config": dict(c2_config(args.gpus),
+                           sample_per_step=f"{cpu_sample_grid().cardinality} points of the "
+                                           f"workload (first 12 of 50 m values)"),
             "cpu_baseline": dict(base, value=value, unit=UNIT),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -312,17 +326,10 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": value / PUBLISHED_PRED_PER_S,
         "vs_baseline_basis": "PAPER.md:761 0.045 ms/prediction (CPU) = 22,222 pred/s",
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2: BF16 matmul NN grid 4x50x50x1000 = 10M (b,m,n,k) points "
-                               "per GPU vs bf16 seed-11 tables (540 recorded configs, "
-                               "60 kernels)",
-                   "points_per_gpu": n_pts, "global_points": world * n_pts,
-                   "parallelism": f"dp{world}: contiguous batch-slab shards, "
-                                  f"all-gather of first-NaN/count stats",
-                   "l2": "flushed between steps (256 MiB write, outside event window)",
-                   "output": "f64 latency per point, canonical order, HBM-resident"},
+        "config": c2_config(world, n_pts),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": profiled_traffic(),
-                     "kernel": "grid_row_kernel" if kpath == 3 else "grid_kernel",
+                     "kernel": "grid_ring_kernel" if kpath == 3 else "grid_kernel",
                      "bytes_per_launch": BYTES_PER_PRED * n_pts,
                      "kernel_ms": grid_avg,
                      "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy r+w)"},

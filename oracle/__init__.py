@@ -179,6 +179,39 @@ def reference_kernels():
     return None
 
 
+def reference_predict_grid_tiles(kernels, tables: dict, axes, threads: int) -> np.ndarray:
+    """The reference's Cython predict_grid_slice (unmodified) over every host
+    thread: the grid is cut into (batch value, m range) sub-grids, each one
+    contiguous in the canonical output, and each computed by one nogil call
+    (_kernels.pyx:76-133) from a thread pool.  Per-point arithmetic does not
+    depend on the other axis values, so the output equals the single call's."""
+    B, M, N, K = (np.ascontiguousarray(a, dtype=np.uint64) for a in axes)
+    nN, nK = len(N), len(K)
+    inner = len(M) * nN * nK
+    out = np.empty(len(B) * inner, np.float64)
+    t = tables
+    per_b = max(1, -(-threads // max(1, len(B))))
+    m_bounds = np.linspace(0, len(M), min(per_b, max(1, len(M))) + 1, dtype=int)
+    tasks = [(b, int(m0), int(m1)) for b in range(len(B))
+             for m0, m1 in zip(m_bounds[:-1], m_bounds[1:]) if m1 > m0]
+
+    def run(task):
+        b, m0, m1 = task
+        Ms = np.ascontiguousarray(M[m0:m1])
+        o = b * inner + m0 * nN * nK
+        kernels.predict_grid_slice(
+            B, Ms, N, K, b, b + 1, t["exact_keys"], t["exact_curve"], t["log_m"], t["log_n"],
+            t["log_k"], t["cand_curve"], t["sample_offsets"], t["sample_dims"],
+            t["sample_thrs"], t["ref_dim"], t["ref_dur"], t["ref_thr"], t["ref_waves"],
+            t["tile_m"], t["tile_n"], t["split_k"], t["blocks_per_wave"],
+            t["family_rowblock"], out[o:o + (m1 - m0) * nN * nK])
+
+    with ThreadPoolExecutor(max_workers=max(1, threads)) as pool:
+        for f in [pool.submit(run, task) for task in tasks]:
+            f.result()
+    return out
+
+
 def reference_predict_grid(kernels, tables: dict, axes, jobs: int = 1) -> np.ndarray:
     """The reference's _predict_grid_compiled (backend.py:58-88): thread pool
     over batch slabs, each calling the Cython predict_grid_slice (nogil)."""

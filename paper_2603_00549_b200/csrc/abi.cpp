@@ -6,7 +6,12 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <condition_variable>
+#include <immintrin.h>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -429,9 +434,40 @@ uint64_t fnv(uint64_t h, const void* p, size_t n) {
   return h;
 }
 
+// memcpy with non-temporal stores for the destination (the caller's result
+// buffer is written once and not read back here: no read-for-ownership of
+// its lines, which halves the host memory traffic of the copy-out)
+__attribute__((target("avx2"))) void copy_nt_avx2(uint8_t* dst, const uint8_t* src, size_t n) {
+  size_t head = (32 - (reinterpret_cast<uintptr_t>(dst) & 31)) & 31;
+  if (head > n) head = n;
+  std::memcpy(dst, src, head);
+  dst += head; src += head; n -= head;
+  size_t i = 0;
+  for (; i + 128 <= n; i += 128) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 32));
+    const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 64));
+    const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 96));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 32), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 64), c);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 96), d);
+  }
+  std::memcpy(dst + i, src + i, n - i);
+  _mm_sfence();
+}
+
+void copy_out(void* dst, const void* src, size_t n) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2) copy_nt_avx2(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), n);
+  else std::memcpy(dst, src, n);
+}
+
 // Persistent host worker threads for the pinned-staging -> caller-buffer
 // copies of the drop-in's result (a single memcpy thread reaches a fraction
 // of the host's memory bandwidth; the caller's numpy buffer is pageable).
+// Workers spin briefly for the next job before sleeping, so a job costs
+// microseconds to dispatch within a call and nothing between calls.
 class CopyPool {
  public:
   explicit CopyPool(int workers) {
@@ -440,63 +476,67 @@ class CopyPool {
   ~CopyPool() {
     {
       std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
+      stop_.store(true);
     }
     cv_.notify_all();
     for (auto& th : threads_) th.join();
   }
   int parts() const { return int(threads_.size()) + 1; }
-  // memcpy(dst, src, n) split over the workers and the calling thread
+  // copy_out(dst, src, n) split over the workers and the calling thread
   void copy(void* dst, const void* src, size_t n) {
     const int P = parts();
-    const size_t piece = ((n + P - 1) / P + 4095) & ~size_t(4095);
+    piece_ = ((n + P - 1) / P + 4095) & ~size_t(4095);
+    dst_ = static_cast<uint8_t*>(dst);
+    src_ = static_cast<const uint8_t*>(src);
+    n_ = n;
+    pending_.store(int(threads_.size()), std::memory_order_relaxed);
     {
       std::lock_guard<std::mutex> lk(mu_);
-      dst_ = static_cast<uint8_t*>(dst);
-      src_ = static_cast<const uint8_t*>(src);
-      n_ = n;
-      piece_ = piece;
-      pending_ = int(threads_.size());
-      ++gen_;
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     part(0);
-    std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    while (pending_.load(std::memory_order_acquire) != 0) _mm_pause();
   }
 
  private:
   void part(int p) {
     const size_t lo = std::min(n_, size_t(p) * piece_), hi = std::min(n_, lo + piece_);
-    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+    if (hi > lo) copy_out(dst_ + lo, src_ + lo, hi - lo);
   }
   void run(int i) {
     uint64_t seen = 0;
     for (;;) {
-      {
-        std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
-        seen = gen_;
+      // spin ~100 us for the next job, then sleep
+      bool got = false;
+      for (int k = 0; k < 20000 && !got; ++k) {
+        if (stop_.load(std::memory_order_relaxed)) return;
+        got = gen_.load(std::memory_order_acquire) != seen;
+        if (!got) _mm_pause();
       }
+      if (!got) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_.load() || gen_.load() != seen; });
+        if (stop_.load()) return;
+      }
+      seen = gen_.load(std::memory_order_acquire);
       part(i + 1);
-      std::lock_guard<std::mutex> lk(mu_);
-      if (--pending_ == 0) done_cv_.notify_one();
+      pending_.fetch_sub(1, std::memory_order_release);
     }
   }
   std::vector<std::thread> threads_;
   std::mutex mu_;
-  std::condition_variable cv_, done_cv_;
-  bool stop_ = false;
-  uint64_t gen_ = 0;
-  int pending_ = 0;
+  std::condition_variable cv_;
+  std::atomic<bool> stop_{false};
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> pending_{0};
   uint8_t* dst_ = nullptr;
   const uint8_t* src_ = nullptr;
   size_t n_ = 0, piece_ = 0;
 };
 
-constexpr int kStageBufs = 3;
-constexpr size_t kStageChunk = size_t(4) << 20;  // bytes per D2H chunk
+constexpr int kStageBufs = 4;
+constexpr size_t kStageChunk = size_t(8) << 20;  // bytes per D2H chunk
 
 struct SliceDevice {
   DeviceBuf out;                    // device result
@@ -518,8 +558,10 @@ SliceCache g_slice;
 // chunks are in flight over PCIe.
 int drain_to_host(SliceDevice& sd, const double* d_out, double* out, size_t bytes) {
   if (!g_slice.pool) {
+    // about half the host threads: the copy-out saturates host memory
+    // bandwidth well before every core is busy (measured on the B200 host)
     const unsigned hc = std::thread::hardware_concurrency();
-    g_slice.pool.reset(new CopyPool(int(std::min(7u, hc > 1 ? hc - 1 : 0u))));
+    g_slice.pool.reset(new CopyPool(int(std::min(7u, hc > 3 ? hc / 2 - 1 : 0u))));
   }
   for (int i = 0; i < kStageBufs; ++i) {
     PM2L_CUDA(sd.stage[i].reserve(kStageChunk));
@@ -536,14 +578,26 @@ int drain_to_host(SliceDevice& sd, const double* d_out, double* out, size_t byte
   };
   for (size_t c = 0; c < std::min<size_t>(n, kStageBufs); ++c)
     if (int rc = issue(c)) return rc;
+  static const bool trace = std::getenv("PM2L_E2E_TRACE") != nullptr;  // diagnostics
+  double t_wait = 0, t_copy = 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t_start = now();
   for (size_t c = 0; c < n; ++c) {
     const int b = int(c % kStageBufs);
+    const auto t0 = now();
     PM2L_CUDA(cudaEventSynchronize(sd.ready[b]));
+    const auto t1 = now();
     const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
     g_slice.pool->copy(reinterpret_cast<uint8_t*>(out) + off, sd.stage[b].ptr, len);
+    t_wait += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t_copy += std::chrono::duration<double, std::milli>(now() - t1).count();
     if (c + kStageBufs < n)
       if (int rc = issue(c + kStageBufs)) return rc;
   }
+  if (trace)
+    std::fprintf(stderr, "pm2l drain: %zu chunks, wait %.3f ms, copy %.3f ms, total %.3f ms\n", n,
+                 t_wait, t_copy,
+                 std::chrono::duration<double, std::milli>(now() - t_start).count());
   return PM2L_OK;
 }
 

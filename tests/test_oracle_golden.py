@@ -73,6 +73,11 @@ def test_reference_cython_kernel_matches_oracle():
         ref = oracle.reference_predict_grid(mod, prep.tables(), prep.axis_arrays(), jobs=3)
         ours = oracle.grid(prep.tables(), prep.axis_arrays(), verify=False)
         assert np.array_equal(ref.view(np.uint64), ours.view(np.uint64))
+        # the all-cores CPU baseline (sub-grid calls of the same kernel) is
+        # the same function
+        for threads in (1, 5):
+            tiles = oracle.reference_predict_grid_tiles(mod, prep.tables(), prep.axis_arrays(), threads)
+            assert np.array_equal(tiles.view(np.uint64), ref.view(np.uint64))
 
 
 def _triple_tables(tmeta):
