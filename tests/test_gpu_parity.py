@@ -282,3 +282,34 @@ def test_no_cpu_fallback_flag(gpu):
     from paper_2603_00549_b200.errors import BackendUnavailable
     with pytest.raises(BackendUnavailable):
         backend.predict_grid(prepared(GRIDS["mk_grid"]), force_python=True)
+
+
+def test_sharded_predict_over_nccl_matches_single_process(gpu, tmp_path):
+    """The §8e multi-GPU host path on the device: NCCL process group (one
+    rank on the test box), GPU slab prediction, stats all-gather, rank-0
+    gather and store write."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2603_00549_b200 import backend, shard
+    from paper_2603_00549_b200.compute import WaveModel
+    from paper_2603_00549_b200.nascache import write_store
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        meta = GRIDS["exact_mix_bf16"]
+        prep = prepared(meta)
+        res = shard.predict_sharded(prep, gather=True)
+        ref = backend.predict_grid(prep)
+        assert np.array_equal(_bits(res.full), _bits(ref))
+        assert res.first_unresolved == -1 and res.unresolved == 0
+        ds = dataset(meta["dataset"])
+        a, b = tmp_path / "a.bin", tmp_path / "b.bin"
+        shard.precompute_sharded(prep.grid, ds, WaveModel(ds.device.sm_count), a)
+        write_store(b, prep.grid, ds, ref)
+        assert a.read_bytes() == b.read_bytes()
+    finally:
+        dist.destroy_process_group()
