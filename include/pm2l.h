@@ -22,6 +22,8 @@
  *   pm2l_points_predict_curve  <- compute.py:150-193   predict_generic with an explicit
  *                                 kernel (no resolution; "mode X")
  *   pm2l_membound_predict      <- membound.py:117-127  predict_membound, batched
+ *   pm2l_store_encode          <- nascache.py:308-333  precompute's record writer
+ *                                 (big-endian records of resolved points)
  *   pm2l_segment_fsum          <- aggregate.py:193     math.fsum of per-layer latencies,
  *                                 per model segment (correctly rounded)
  */
@@ -206,6 +208,19 @@ int pm2l_membound_predict(const double* features, const int32_t* model_ids, int6
  * gives a NaN total.  Exact warp-segmented fixed-point reduction. */
 int pm2l_segment_fsum(const double* values, const int64_t* offsets, int64_t n_segments,
                       double* out_totals, void* stream);
+
+/* Store encoder (nascache.py:308-333 record section): for the
+ * grid slice whose canonical latencies are lat[0..n) (DEVICE) and whose axis
+ * values are B/M/N/K (DEVICE u64; batch = the slice's batch values), write
+ * the 40-byte big-endian records (b, m, n, k, latency) of every resolved
+ * (non-NaN) point in canonical order into `records` (DEVICE, >= 40*n bytes)
+ * and their number into *count (DEVICE i64).  workspace: DEVICE, at least
+ * pm2l_store_encode_workspace(n) bytes.  Stream-ordered, no host sync. */
+int64_t pm2l_store_encode_workspace(int64_t n);
+int pm2l_store_encode(const double* lat, int64_t n, const uint64_t* batch_vals,
+                      const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals, int64_t n_n,
+                      const uint64_t* k_vals, int64_t n_k, void* workspace, uint8_t* records,
+                      int64_t* count, void* stream);
 
 /* ------------------------------------------------ reference FFI drop-in ---
  * Exactly pm2lat._kernels.predict_grid_slice (_kernels.pyx:76-133): HOST

@@ -15,7 +15,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB_NAME = "libpm2l_b200.so"
 LIB_PATH = os.path.join(PKG, LIB_NAME)
-SOURCES = ["csrc/grid.cu", "csrc/points.cu", "csrc/reduce.cu", "csrc/tables.cpp", "csrc/abi.cpp"]
+SOURCES = ["csrc/grid.cu", "csrc/points.cu", "csrc/reduce.cu", "csrc/store.cu", "csrc/tables.cpp",
+           "csrc/abi.cpp"]
 HEADERS = ["csrc/pm2l_internal.h", "csrc/common.cuh", "../include/pm2l.h"]
 
 NVCC_FLAGS = [

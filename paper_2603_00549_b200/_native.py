@@ -63,6 +63,8 @@ SIGNATURES = {
     "pm2l_points_predict_curve": (_i32, [_p, _p, _p, _i64, _p, _p, _p, _p]),
     "pm2l_membound_predict": (_i32, [_p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "pm2l_segment_fsum": (_i32, [_p, _p, _i64, _p, _p]),
+    "pm2l_store_encode_workspace": (_i64, [_i64]),
+    "pm2l_store_encode": (_i32, [_p, _i64, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p, _p, _p]),
     "pm2l_predict_grid_slice": (_i32, [_p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
                                        _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _i64,
                                        _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
@@ -96,6 +98,8 @@ def load(required: bool = True):
             try:
                 want = _build.source_hash()
             except OSError:      # sources not shipped: nothing to compare against
+                want = None
+            if os.environ.get("PM2L_LIB_PATH"):  # diagnostic / A-B builds
                 want = None
             got = lib.pm2l_source_hash().decode()
             if want is not None and got != want:

@@ -105,3 +105,19 @@ def predict_grid_all_curves(prep, b_lo: int = 0, b_hi=None, stream=None, device:
         dt.handle, pb, lb, pm, lm, pn, ln, pk, lk, b_lo, b_hi, _native.ptr(out),
         _native.stream_handle(stream)), "pm2l_grid_predict_all_curves")
     return out
+
+
+def synchronize():
+    """Wait for the device work queued on the current stream."""
+    _device.torch().cuda.current_stream().synchronize()
+
+
+def first_nan(lat) -> int:
+    """Flat index of the first NaN of a CUDA float64 tensor (pm2l_nan_scan),
+    -1 if none."""
+    t = _device.torch()
+    first = t.full((1,), -1, dtype=t.int64, device=lat.device)
+    _native.check(_native.load().pm2l_nan_scan(lat.data_ptr(), int(lat.numel()), first.data_ptr(),
+                                              _native.stream_handle()), "pm2l_nan_scan")
+    v = int(first.item())
+    return -1 if v < 0 else v

@@ -425,6 +425,25 @@ int pm2l_segment_fsum(const double* values, const int64_t* offsets, int64_t n_se
   return PM2L_OK;
 }
 
+int64_t pm2l_store_encode_workspace(int64_t n) { return n < 0 ? -1 : store_encode_workspace(n); }
+
+int pm2l_store_encode(const double* lat, int64_t n, const uint64_t* batch_vals,
+                      const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals, int64_t n_n,
+                      const uint64_t* k_vals, int64_t n_k, void* workspace, uint8_t* records,
+                      int64_t* count, void* stream) {
+  if (n < 0 || n_m < 0 || n_n < 0 || n_k < 0) return fail(PM2L_ERR_INVALID, "negative size");
+  if (!count) return fail(PM2L_ERR_INVALID, "null count");
+  if (n > 0 && (!lat || !batch_vals || !m_vals || !n_vals || !k_vals || !workspace || !records))
+    return fail(PM2L_ERR_INVALID, "null store_encode argument");
+  if (n > 0 && n % (n_m * n_n * n_k) != 0)
+    return fail(PM2L_ERR_INVALID, "n is not a whole number of batch planes");
+  if (int rc = check_device()) return rc;
+  const int rc = launch_store_encode(lat, n, batch_vals, m_vals, n_m, n_vals, n_n, k_vals, n_k,
+                                     workspace, records, count, stream);
+  if (rc) return cuda_fail(cudaError_t(rc), "store encode launch");
+  return PM2L_OK;
+}
+
 // ------------------------------------------------------------------ drop-in
 namespace {
 

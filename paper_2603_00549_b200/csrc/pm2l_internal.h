@@ -202,6 +202,10 @@ int launch_membound(const double* f, const int32_t* mid, int64_t n, const double
                     const double* b, const double* floors, int64_t n_models, double* out,
                     uint8_t* floored, void* stream);
 int launch_nan_scan(const double* v, int64_t n, unsigned long long* first, void* stream);
+int64_t store_encode_workspace(int64_t n);
+int launch_store_encode(const double* lat, int64_t n, const uint64_t* B, const uint64_t* M,
+                        int64_t nM, const uint64_t* N, int64_t nN, const uint64_t* K, int64_t nK,
+                        void* workspace, uint8_t* records, int64_t* count, void* stream);
 int launch_segment_fsum(const double* v, const int64_t* off, int64_t nseg, double* out,
                         void* stream);
 

@@ -200,8 +200,50 @@ def encode_records(grid: GridSpec, latencies: np.ndarray) -> np.ndarray:
     return rec
 
 
-def write_store(path, grid: GridSpec, dataset: Dataset, latencies: np.ndarray) -> int:
-    rec = encode_records(grid, latencies)
+def encode_records_device(grid: GridSpec, latencies, b_lo: int = 0, device: int = 0) -> np.ndarray:
+    """encode_records on the B200 (pm2l_store_encode): ``latencies`` is the
+    CUDA float64 tensor of batch indices [b_lo, b_lo + len/inner) of the
+    grid; records are built, compacted and byte-swapped on the device and
+    only the record bytes come back."""
+    from . import _device, _native
+    t = _device.torch()
+    dev = _device.device(device)
+    n = int(latencies.numel())
+    nb, nm, nn, nk = grid.shape()
+    inner = nm * nn * nk
+    if n == 0:
+        return np.empty(0, _RECORD_DTYPE)
+    if n % inner:
+        raise ValidationError("latency count is not a whole number of batch planes")
+    b_hi = b_lo + n // inner
+    if not 0 <= b_lo < b_hi <= nb:
+        raise ValidationError(f"batch slice [{b_lo}, {b_hi}) out of range")
+    axes = [t.from_numpy(np.ascontiguousarray(np.asarray(grid.axes[a], dtype=np.uint64)))
+            .to(dev) for a in AXIS_ORDER]
+    axes[0] = axes[0][b_lo:b_hi].contiguous()
+    lib = _native.load()
+    ws = t.empty(int(lib.pm2l_store_encode_workspace(n)), dtype=t.uint8, device=dev)
+    rec = t.empty(n * RECORD_SIZE, dtype=t.uint8, device=dev)
+    count = t.zeros(1, dtype=t.int64, device=dev)
+    lat = latencies.contiguous()
+    _native.check(lib.pm2l_store_encode(
+        lat.data_ptr(), n, axes[0].data_ptr(), axes[1].data_ptr(), nm, axes[2].data_ptr(), nn,
+        axes[3].data_ptr(), nk, ws.data_ptr(), rec.data_ptr(), count.data_ptr(),
+        _native.stream_handle()), "pm2l_store_encode")
+    c = int(count.item())
+    # pinned landing buffer (torch's caching host allocator: reused across
+    # calls), one DMA of the record bytes; the array keeps the buffer alive
+    host = t.empty(c * RECORD_SIZE, dtype=t.uint8, pin_memory=True)
+    if c:
+        host.copy_(rec[:c * RECORD_SIZE])
+    return host.numpy().view(_RECORD_DTYPE)
+
+
+def write_store(path, grid: GridSpec, dataset: Dataset, latencies: np.ndarray = None,
+                records: np.ndarray = None) -> int:
+    """Write the store (nascache.py:308-333) from host latencies, or from
+    records already encoded (encode_records_device)."""
+    rec = records if records is not None else encode_records(grid, latencies)
     header = {"device_id": dataset.device.device_id,
               "dataset_fingerprint": dataset.fingerprint(),
               "grid_fingerprint": grid.fingerprint(),
@@ -213,7 +255,7 @@ def write_store(path, grid: GridSpec, dataset: Dataset, latencies: np.ndarray) -
         fh.write(struct.pack(">H", FORMAT_VERSION))
         fh.write(struct.pack(">I", len(hb)))
         fh.write(hb)
-        fh.write(rec.tobytes())
+        fh.write(memoryview(np.ascontiguousarray(rec)).cast("B"))
     return int(rec.size)
 
 
@@ -226,18 +268,22 @@ def precompute(grid: GridSpec, dataset: Dataset, wm: Optional[WaveModel], out_pa
     from . import backend
     wm = wm or WaveModel(sm_count=dataset.device.sm_count)
     prep = PreparedGrid(dataset, grid, wm)
+    total = grid.cardinality
     start = time.perf_counter()
-    latencies = backend.predict_grid(prep, jobs=jobs)
+    lat = backend.predict_grid_device(prep) if total else None
+    if lat is not None:
+        backend.synchronize()
     elapsed = time.perf_counter() - start
-    nan = np.isnan(latencies)
-    skipped = int(np.count_nonzero(nan))
+    # the records are encoded and compacted on the device (pm2l_store_encode)
+    rec = encode_records_device(grid, lat) if total else encode_records(grid, np.empty(0))
+    skipped = total - int(rec.size)
     if skipped and not skip_unresolved:
-        b, m, n, k = point_at(grid, int(np.argmax(nan)))
+        first = backend.first_nan(lat)
+        b, m, n, k = point_at(grid, first)
         raise UnresolvedPoint(
             f"grid point batch={b} m={m} n={n} k={k} ({grid.family}, {grid.dtype.value}, "
             f"{grid.transpose_mode.value}) has no usable kernel configuration")
-    total = grid.cardinality
-    write_store(out_path, grid, dataset, latencies)
+    write_store(out_path, grid, dataset, records=rec)
     return PrecomputeSummary(total_points=total, entries_written=total - skipped,
                              skipped=skipped, elapsed_s=elapsed,
                              mean_us_per_prediction=elapsed / total * 1e6 if total else 0.0,

@@ -313,3 +313,51 @@ def test_sharded_predict_over_nccl_matches_single_process(gpu, tmp_path):
         assert a.read_bytes() == b.read_bytes()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", list(GRIDS))
+def test_device_store_encoder_matches_host_encoder(gpu, name):
+    """pm2l_store_encode == the host encoder (the
+    reference's record bytes, nascache.py:325-333), slabs included."""
+    from paper_2603_00549_b200 import backend
+    from paper_2603_00549_b200.nascache import encode_records, encode_records_device
+    prep = prepared(GRIDS[name])
+    lat = backend.predict_grid_device(prep)
+    host = encode_records(prep.grid, lat.cpu().numpy())
+    dev = encode_records_device(prep.grid, lat)
+    assert dev.tobytes() == host.tobytes()
+    nb = len(prep.grid.axes["batch"])
+    if nb > 1:
+        inner = prep.grid.cardinality // nb
+        part = encode_records_device(prep.grid, lat[inner:], b_lo=1)
+        all_host = lat.cpu().numpy()
+        from paper_2603_00549_b200.nascache import GridSpec
+        sub = GridSpec(prep.grid.family, prep.grid.dtype, prep.grid.transpose_mode,
+                       dict(prep.grid.axes, batch=tuple(prep.grid.axes["batch"][1:])))
+        assert part.tobytes() == encode_records(sub, all_host[inner:]).tobytes()
+
+
+def test_device_store_encoder_compacts_unresolved_points(gpu):
+    """Random tables with kernels lacking curves: NaN points are dropped and
+    the survivors keep canonical order (skip_unresolved)."""
+    import torch
+    from test_gpu_random_tables import random_tables
+    from paper_2603_00549_b200 import _native
+    from paper_2603_00549_b200.core import DType, TransposeMode
+    from paper_2603_00549_b200.nascache import GridSpec, encode_records, encode_records_device
+    rng = np.random.default_rng(5)
+    t, pm, pn, pk = random_tables(rng, 300, 20, 40)
+    dt = _native.DeviceTables(t, 0)
+    B = np.array([1, 2, 3, 5], np.uint64)
+    M = np.array(sorted(set(rng.integers(1, 6000, 9).tolist())), np.uint64)
+    N = np.array(sorted(set(rng.integers(1, 6000, 7).tolist())), np.uint64)
+    K = np.array(sorted(set(rng.integers(1, 30000, 700).tolist())), np.uint64)
+    plan = _native.GridPlan(dt, (B, M, N, K))
+    lat = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
+    plan.launch(lat)
+    host_lat = lat.cpu().numpy()
+    assert np.isnan(host_lat).any() and not np.isnan(host_lat).all()
+    grid = GridSpec("matmul", DType.BF16, TransposeMode.NN,
+                    {"batch": tuple(int(x) for x in B), "m": tuple(int(x) for x in M),
+                     "n": tuple(int(x) for x in N), "k": tuple(int(x) for x in K)})
+    assert encode_records_device(grid, lat).tobytes() == encode_records(grid, host_lat).tobytes()
