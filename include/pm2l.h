@@ -24,6 +24,7 @@
  *   pm2l_membound_predict      <- membound.py:117-127  predict_membound, batched
  *   pm2l_store_encode          <- nascache.py:308-333  precompute's record writer
  *                                 (big-endian records of resolved points)
+ *   pm2l_store_lookup          <- nascache.py:408-424  CacheStore.lookup, batched
  *   pm2l_segment_fsum          <- aggregate.py:193     math.fsum of per-layer latencies,
  *                                 per model segment (correctly rounded)
  */
@@ -221,6 +222,18 @@ int pm2l_store_encode(const double* lat, int64_t n, const uint64_t* batch_vals,
                       const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals, int64_t n_n,
                       const uint64_t* k_vals, int64_t n_k, void* workspace, uint8_t* records,
                       int64_t* count, void* stream);
+
+/* Batched CacheStore.lookup (nascache.py:408-424):
+ * records = the store's record section (DEVICE, n_records x 40 bytes,
+ * sorted), queries = n x 4 u64 (batch, m, n, k) (DEVICE).  out[i] = the
+ * stored latency or NaN when absent; *first_missing (DEVICE u64, initialise
+ * to ~0) = the smallest absent query index.  axes/axis_lens (DEVICE axes of
+ * the store's grid, may be NULL): when given and the store is dense (every
+ * grid point present, n_records == product of the lengths) a query is
+ * direct-indexed instead of binary-searched. */
+int pm2l_store_lookup(const uint8_t* records, int64_t n_records, const uint64_t* const* axes,
+                      const int64_t* axis_lens, const uint64_t* queries, int64_t n, double* out,
+                      uint64_t* first_missing, void* stream);
 
 /* ------------------------------------------------ reference FFI drop-in ---
  * Exactly pm2lat._kernels.predict_grid_slice (_kernels.pyx:76-133): HOST

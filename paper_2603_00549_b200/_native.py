@@ -65,6 +65,7 @@ SIGNATURES = {
     "pm2l_segment_fsum": (_i32, [_p, _p, _i64, _p, _p]),
     "pm2l_store_encode_workspace": (_i64, [_i64]),
     "pm2l_store_encode": (_i32, [_p, _i64, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p, _p, _p]),
+    "pm2l_store_lookup": (_i32, [_p, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "pm2l_predict_grid_slice": (_i32, [_p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
                                        _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _i64,
                                        _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),

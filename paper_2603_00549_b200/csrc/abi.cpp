@@ -444,6 +444,33 @@ int pm2l_store_encode(const double* lat, int64_t n, const uint64_t* batch_vals,
   return PM2L_OK;
 }
 
+int pm2l_store_lookup(const uint8_t* records, int64_t n_records, const uint64_t* const* axes,
+                      const int64_t* axis_lens, const uint64_t* queries, int64_t n, double* out,
+                      uint64_t* first_missing, void* stream) {
+  if (n < 0 || n_records < 0) return fail(PM2L_ERR_INVALID, "negative size");
+  if (n > 0 && (!queries || !out || !first_missing || (n_records > 0 && !records)))
+    return fail(PM2L_ERR_INVALID, "null store_lookup argument");
+  if (int rc = check_device()) return rc;
+  const uint64_t* ax[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t lens[4] = {0, 0, 0, 0};
+  bool dense = axes != nullptr && axis_lens != nullptr;
+  if (dense) {
+    int64_t prod = 1;
+    for (int a = 0; a < 4; ++a) {
+      ax[a] = axes[a];
+      lens[a] = axis_lens[a];
+      if (!ax[a] || lens[a] < 1) dense = false;
+      prod *= lens[a];
+    }
+    dense = dense && prod == n_records;
+  }
+  const int rc = launch_store_lookup(records, n_records, dense ? ax : nullptr, lens, queries, n,
+                                     out, reinterpret_cast<unsigned long long*>(first_missing),
+                                     stream);
+  if (rc) return cuda_fail(cudaError_t(rc), "store lookup launch");
+  return PM2L_OK;
+}
+
 // ------------------------------------------------------------------ drop-in
 namespace {
 

@@ -28,6 +28,12 @@ __device__ __forceinline__ uint64_t abs_bits(double x) {
 
 __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
+// byte order reversal of a 64-bit word (the store's big-endian fields)
+__device__ __forceinline__ uint64_t bswap64_ext(uint64_t v) {
+  const uint32_t lo = uint32_t(v), hi = uint32_t(v >> 32);
+  return (uint64_t(__byte_perm(lo, 0, 0x0123)) << 32) | __byte_perm(hi, 0, 0x0123);
+}
+
 // (a + b - 1) / b in u64 exactly as the Cython kernel writes it
 // (_kernels.pyx:124,126,127); 32-bit hardware path when both operands fit.
 __device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) {

@@ -206,6 +206,9 @@ int64_t store_encode_workspace(int64_t n);
 int launch_store_encode(const double* lat, int64_t n, const uint64_t* B, const uint64_t* M,
                         int64_t nM, const uint64_t* N, int64_t nN, const uint64_t* K, int64_t nK,
                         void* workspace, uint8_t* records, int64_t* count, void* stream);
+int launch_store_lookup(const uint8_t* records, int64_t n_rec, const uint64_t* const axes[4],
+                        const int64_t lens[4], const uint64_t* queries, int64_t nq, double* out,
+                        unsigned long long* first_missing, void* stream);
 int launch_segment_fsum(const double* v, const int64_t* off, int64_t nseg, double* out,
                         void* stream);
 

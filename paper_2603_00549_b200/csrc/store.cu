@@ -8,6 +8,8 @@
 //   store_scan_kernel    exclusive scan of the tile counts (one CTA)
 //   store_encode_kernel  per tile: ballot/warp-prefix compaction, byte-swap,
 //                        five 8-byte stores per record
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace pm2l {
@@ -19,10 +21,7 @@ constexpr int kEncThreads = 256;
 constexpr int kEncRows = 4;                       // points per thread
 constexpr int kEncTile = kEncThreads * kEncRows;  // points per CTA
 
-__device__ __forceinline__ uint64_t bswap64(uint64_t v) {
-  const uint32_t lo = uint32_t(v), hi = uint32_t(v >> 32);
-  return (uint64_t(__byte_perm(lo, 0, 0x0123)) << 32) | __byte_perm(hi, 0, 0x0123);
-}
+__device__ __forceinline__ uint64_t bswap64(uint64_t v) { return bswap64_ext(v); }
 
 struct EncAxes {
   const uint64_t *B, *M, *N, *K;
@@ -142,6 +141,88 @@ int launch_store_encode(const double* lat, int64_t n, const uint64_t* B, const u
   store_encode_kernel<<<unsigned(nt), kEncThreads, 0, s>>>(lat, n, ax, offs, rec);
   cudaError_t e = cudaMemcpyAsync(count, offs + nt, sizeof(int64_t), cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return int(e);
+  return int(cudaGetLastError());
+}
+
+}  // namespace pm2l
+
+// ----------------------------------------------------------- batched lookup
+// CacheStore.lookup (pm2lat/nascache.py:408-424) for many points at once:
+// each query is a binary search over the sorted big-endian record keys, or,
+// for a dense store (every point of its grid present), a direct index from
+// per-axis searches (then one record read, key re-checked).  A missing point
+// gives NaN and the smallest missing query index in *first_missing.
+namespace pm2l {
+namespace {
+
+struct LookupAxes {
+  const uint64_t* ax[4];
+  int64_t len[4];
+  int dense;
+};
+
+__device__ __forceinline__ int cmp_key(const uint64_t* rec, const uint64_t q[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint64_t v = dev::bswap64_ext(rec[j]);
+    if (v != q[j]) return v < q[j] ? -1 : 1;
+  }
+  return 0;
+}
+
+__global__ void store_lookup_kernel(const uint64_t* __restrict__ rec, int64_t n_rec, LookupAxes la,
+                                    const uint64_t* __restrict__ qs, int64_t nq,
+                                    double* __restrict__ out,
+                                    unsigned long long* __restrict__ first_missing) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nq;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t q[4] = {qs[4 * i], qs[4 * i + 1], qs[4 * i + 2], qs[4 * i + 3]};
+    int64_t hit = -1;
+    if (la.dense) {
+      int64_t flat = 0;
+      bool ok = true;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        int64_t lo = 0, hi = la.len[a];
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (la.ax[a][mid] < q[a]) lo = mid + 1; else hi = mid;
+        }
+        ok = ok && lo < la.len[a] && la.ax[a][lo] == q[a];
+        flat = flat * la.len[a] + lo;
+      }
+      if (ok && flat < n_rec && cmp_key(rec + 5 * flat, q) == 0) hit = flat;
+    } else {
+      int64_t lo = 0, hi = n_rec;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const int c = cmp_key(rec + 5 * mid, q);
+        if (c == 0) { hit = mid; break; }
+        if (c < 0) lo = mid + 1; else hi = mid;
+      }
+    }
+    if (hit >= 0) {
+      out[i] = __longlong_as_double(static_cast<long long>(dev::bswap64_ext(rec[5 * hit + 4])));
+    } else {
+      out[i] = dev::qnan();
+      atomicMin(first_missing, (unsigned long long)i);
+    }
+  }
+}
+
+}  // namespace
+
+int launch_store_lookup(const uint8_t* records, int64_t n_rec, const uint64_t* const axes[4],
+                        const int64_t lens[4], const uint64_t* queries, int64_t nq, double* out,
+                        unsigned long long* first_missing, void* stream) {
+  if (nq == 0) return 0;
+  LookupAxes la{};
+  la.dense = axes != nullptr;
+  if (la.dense)
+    for (int a = 0; a < 4; ++a) { la.ax[a] = axes[a]; la.len[a] = lens[a]; }
+  const int nb = int(std::min<int64_t>((nq + 255) / 256, 148 * 16));
+  store_lookup_kernel<<<nb, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint64_t*>(records), n_rec, la, queries, nq, out, first_missing);
   return int(cudaGetLastError());
 }
 

@@ -368,6 +368,57 @@ class CacheStore:
                 return struct.unpack(">d", self._mm[off + 32:off + 40])[0]
         raise MissingEntry(f"point batch={batch} m={m} n={n} k={k} is not in the store")
 
+    def device_records(self, device: int = 0):
+        """The record section staged in HBM once (a CUDA uint8 tensor)."""
+        from . import _device
+        cache = self.__dict__.setdefault("_dev_records", {})
+        if device not in cache:
+            t = _device.torch()
+            raw = np.frombuffer(self._mm, np.uint8, count=self.entry_count * RECORD_SIZE,
+                                offset=self._records_at) if self.entry_count else np.zeros(8, np.uint8)
+            cache[device] = t.from_numpy(raw.copy()).to(_device.device(device))
+        return cache[device]
+
+    def lookup_many(self, points, missing: str = "raise", device: int = 0) -> np.ndarray:
+        """lookup() for an (n, 4) array of (batch, m, n, k) points at once on
+        the B200 (pm2l_store_lookup): a binary search per point over the
+        staged records, or a direct index when the store holds every point of
+        its grid.  missing="raise" raises MissingEntry naming the first absent
+        point (as lookup would); missing="nan" returns NaN for it."""
+        from . import _device, _native
+        if missing not in ("raise", "nan"):
+            raise ValidationError("missing must be 'raise' or 'nan'")
+        q = np.ascontiguousarray(np.asarray(points, dtype=np.uint64).reshape(-1, 4))
+        n = len(q)
+        if n == 0:
+            return np.empty(0, np.float64)
+        t = _device.torch()
+        dev = _device.device(device)
+        rec = self.device_records(device)
+        qd = t.from_numpy(q).to(dev)
+        out = t.empty(n, dtype=t.float64, device=dev)
+        first = t.full((1,), -1, dtype=t.int64, device=dev)
+        axes_ptr = lens_ptr = None
+        keep = []
+        grid = self.header.get("grid")
+        if grid and self.entry_count:
+            axes = [np.ascontiguousarray(np.asarray(grid["axes"][a], dtype=np.uint64)) for a in AXIS_ORDER]
+            if int(np.prod([len(a) for a in axes])) == self.entry_count:
+                dax = [t.from_numpy(a).to(dev) for a in axes]
+                ptrs = np.array([a.data_ptr() for a in dax], np.uint64)
+                lens = np.array([len(a) for a in axes], np.int64)
+                keep = [dax, ptrs, lens]
+                axes_ptr, lens_ptr = ptrs.ctypes.data, lens.ctypes.data
+        _native.check(_native.load().pm2l_store_lookup(
+            rec.data_ptr(), self.entry_count, axes_ptr, lens_ptr, qd.data_ptr(), n,
+            out.data_ptr(), first.data_ptr(), _native.stream_handle()), "pm2l_store_lookup")
+        f = int(first.item())
+        del keep
+        if f >= 0 and missing == "raise":
+            b, m, nn, k = (int(v) for v in q[f])
+            raise MissingEntry(f"point batch={b} m={m} n={nn} k={k} is not in the store")
+        return out.cpu().numpy()
+
     def iter_entries(self) -> Iterator[Tuple[Tuple[int, int, int, int], float]]:
         for r in self.records():
             yield (int(r["b"]), int(r["m"]), int(r["n"]), int(r["k"])), float(r["lat"])

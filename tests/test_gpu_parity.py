@@ -361,3 +361,43 @@ def test_device_store_encoder_compacts_unresolved_points(gpu):
                     {"batch": tuple(int(x) for x in B), "m": tuple(int(x) for x in M),
                      "n": tuple(int(x) for x in N), "k": tuple(int(x) for x in K)})
     assert encode_records_device(grid, lat).tobytes() == encode_records(grid, host_lat).tobytes()
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_batched_store_lookup_matches_scalar_lookup(gpu, tmp_path, sparse):
+    """CacheStore.lookup_many == lookup (nascache.py:408-424)
+    point by point: dense stores are direct-indexed, sparse ones searched;
+    absent points are NaN or raise MissingEntry naming the first one."""
+    from paper_2603_00549_b200 import backend
+    from paper_2603_00549_b200.errors import MissingEntry
+    from paper_2603_00549_b200.nascache import CacheStore, point_at, write_store
+    meta = GRIDS["exact_mix_bf16"]
+    prep = prepared(meta)
+    lat = backend.predict_grid(prep)
+    rng = np.random.default_rng(3)
+    if sparse:
+        lat = lat.copy()
+        lat[rng.choice(len(lat), len(lat) // 3, replace=False)] = np.nan
+    path = tmp_path / "s.bin"
+    write_store(path, prep.grid, dataset(meta["dataset"]), lat)
+    with CacheStore(path) as st:
+        pts = np.array([point_at(prep.grid, i) for i in range(prep.grid.cardinality)], np.uint64)
+        extra = pts[rng.choice(len(pts), 50)].copy()
+        extra[:, 3] += 1  # mostly absent points
+        q = np.concatenate([pts, extra])
+        got = st.lookup_many(q, missing="nan")
+        for i, p in enumerate(q):
+            try:
+                ref = st.lookup(*(int(v) for v in p))
+                assert got[i].view(np.uint64) == np.float64(ref).view(np.uint64)
+            except MissingEntry:
+                assert np.isnan(got[i])
+        want = lat.view(np.uint64)
+        present = ~np.isnan(lat)
+        assert np.array_equal(got[:len(pts)][present].view(np.uint64), want[present])
+        absent = np.nonzero(np.isnan(got))[0]
+        if len(absent):
+            with pytest.raises(MissingEntry) as exc:
+                st.lookup_many(q)
+            b, m, n, k = (int(v) for v in q[absent[0]])
+            assert f"batch={b} m={m} n={n} k={k}" in str(exc.value)
