@@ -66,6 +66,13 @@ def main():
         for i in range(1, 5):
             print(f"{names[i]:<12} (from CTA entry) median {np.median(rel[:, i]):6.2f}  "
                   f"p10 {np.percentile(rel[:, i], 10):6.2f}  p90 {np.percentile(rel[:, i], 90):6.2f}  max {rel[:, i].max():6.2f}")
+        # static CTA-strided tiles: tile = cta + j * ctas
+        ctas = int(os.environ.get("RING_CTAS", "444"))
+        cta_end = np.array([rel[c::ctas, 4].max() for c in range(ctas)])
+        cta_n = np.array([len(rel[c::ctas]) for c in range(ctas)])
+        for nt in sorted(set(cta_n.tolist())):
+            e = cta_end[cta_n == nt]
+            print(f"CTAs with {nt} tiles: {len(e)}, end median {np.median(e):.2f} p90 {np.percentile(e, 90):.2f} max {e.max():.2f}")
         d = lambda a, b: np.median(rel[:, b] - rel[:, a])  # noqa: E731
         print(f"build: staircase {d(1, 5):.2f}  W {d(5, 6):.2f}  cuts {d(6, 7):.2f}  maps {d(7, 2):.2f}")
         print("build dur median", np.median(rel[:, 2] - rel[:, 1]), " emit dur median",
