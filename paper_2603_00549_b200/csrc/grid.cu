@@ -95,7 +95,8 @@ constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kWsThreads = 32 * (kProducerWarps + kConsumerWarps);
 
 struct GridLaunch {
-  int tiles;     // rows * nbs
+  int tiles;     // rows * nbs * nkt
+  int nkt, kt;   // k tiles per (row, slab) and k values per k tile
   int kpt;       // k values per consumer thread
   int nbs;       // batch slabs
   int bper;      // batch values per slab
@@ -333,6 +334,7 @@ template <bool VERIFY, int MODE, int NEAR, int NB>
 __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& g,
                                              const GridLaunch& gl, const double* base_tab,
                                              const LaunchOut& out, int ctid, int row, int slab,
+                                             int k_lo, int k_hi,
                                              const uint8_t* buf, const int2* gcur,
                                              const int32_t* gst, const double* glk) {
   const uint64_t* sD = reinterpret_cast<const uint64_t*>(buf + gl.b_sD);
@@ -357,19 +359,19 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
     // then all nearest searches, then all base-table loads in flight
     // together, then the stores
     constexpr int U = 4;
-    for (int k0 = 0; k0 < nK; k0 += U * kConsumers) {
+    for (int k0 = k_lo; k0 < k_hi; k0 += U * kConsumers) {
       double2 ki[U];
       int ik[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         ik[u] = k0 + u * kConsumers + ctid;
-        ki[u] = ik[u] < nK ? *reinterpret_cast<const double2*>(&g.kinfo[ik[u]])
-                           : make_double2(0.0, 0.0);
+        ki[u] = ik[u] < k_hi ? *reinterpret_cast<const double2*>(&g.kinfo[ik[u]])
+                             : make_double2(0.0, 0.0);
       }
       int ci[U], wc[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (ik[u] < nK) {
+        if (ik[u] < k_hi) {
           const int2 gp = nearest_one_class(t.G, glk, rv, dmin1, lastpos1, ki[u].x,
                                             __double2loint(ki[u].y));
           const int2 cw = gcur[gst[gp.x] + gp.y];
@@ -404,7 +406,7 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
     return;
   }
   const int im = row / nN, jn = row - im * nN;
-  for (int ik = ctid; ik < nK; ik += kConsumers) {
+  for (int ik = k_lo + ctid; ik < k_hi; ik += kConsumers) {
     const double2 ki = *reinterpret_cast<const double2*>(&g.kinfo[ik]);
     const int start = __double2loint(ki.y);
     int ci;
@@ -488,13 +490,14 @@ __global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g
   if (warp < kProducerWarps) {
     int it = 0;
     int tile = blockIdx.x;
-    RowPre cur = tile < gl.tiles ? load_row(g, tile / gl.nbs) : RowPre{};
+    // tile = (row * nbs + slab) * nkt + k tile
+    RowPre cur = tile < gl.tiles ? load_row(g, tile / gl.nkt / gl.nbs) : RowPre{};
     for (; tile < gl.tiles; tile += gridDim.x, ++it) {
       const int nt = tile + gridDim.x;
-      const RowPre nxt = nt < gl.tiles ? load_row(g, nt / gl.nbs) : cur;  // prefetch
+      const RowPre nxt = nt < gl.tiles ? load_row(g, nt / gl.nkt / gl.nbs) : cur;  // prefetch
       const int b = it & 1;
       if (it >= 2) named_sync(kBarEmpty + b, kWsThreads);
-      produce_tile(t, g, gl, warp, lane, cur, tile % gl.nbs, bufs + b * gl.buf_bytes);
+      produce_tile(t, g, gl, warp, lane, cur, (tile / gl.nkt) % gl.nbs, bufs + b * gl.buf_bytes);
       named_arrive(kBarFull + b, kWsThreads);
       cur = nxt;
     }
@@ -507,9 +510,11 @@ __global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g
     for (int tile = blockIdx.x; tile < gl.tiles; tile += gridDim.x, ++it) {
       const int b = it & 1;
       named_sync(kBarFull + b, kWsThreads);
-      consume_tile<VERIFY, MODE, NEAR, NB>(t, g, gl, base_tab, out, ctid, tile / gl.nbs,
-                                           tile % gl.nbs, bufs + b * gl.buf_bytes, gcur, gst,
-                                           glk);
+      const int rs = tile / gl.nkt, kx = tile - rs * gl.nkt;
+      const int k_lo = kx * gl.kt, k_hi = min(int(g.nK), k_lo + gl.kt);
+      consume_tile<VERIFY, MODE, NEAR, NB>(t, g, gl, base_tab, out, ctid, rs / gl.nbs,
+                                           rs % gl.nbs, k_lo, k_hi, bufs + b * gl.buf_bytes,
+                                           gcur, gst, glk);
       named_arrive(kBarEmpty + b, kWsThreads);
     }
   }
@@ -1328,7 +1333,18 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
   if (rows < target_tiles && nb > 1) nbs = std::min<int64_t>(nb, (target_tiles + rows - 1) / rows);
   gl.bper = int((nb + nbs - 1) / nbs);
   gl.nbs = int((nb + gl.bper - 1) / gl.bper);
-  gl.tiles = int(rows * gl.nbs);
+  // too few (row, slab) tiles (attention grids: one (m, n) row, long k axis):
+  // split the k axis too, >= 1024 k values per tile
+  gl.nkt = 1;
+  gl.kt = int(g.nK);
+  if (rows * gl.nbs < target_tiles && g.nK > 1024)
+    gl.nkt = int(std::min<int64_t>((target_tiles + rows * gl.nbs - 1) / (rows * gl.nbs),
+                                   (g.nK + 1023) / 1024));
+  if (gl.nkt > 1) {
+    gl.kt = int((g.nK + gl.nkt - 1) / gl.nkt);
+    gl.nkt = int((g.nK + gl.kt - 1) / gl.kt);
+  }
+  gl.tiles = int(std::min<int64_t>(rows * gl.nbs * std::max(gl.nkt, 1), 0x7FFFFFFFll));
   gl.kpt = int((g.nK + kConsumers - 1) / kConsumers);
   gl.mode = t.all_gemm ? 0 : 2;
   gl.near = (t.NC == 1 && t.lowest_wins) ? 2 : (t.G <= 32 ? 1 : 0);
@@ -1420,7 +1436,7 @@ cudaError_t launch_rows_t(const TablesDev& t, const GridDev& g, const RowLaunch&
 }
 
 bool grid_dims_ok(const GridDev& g, const GridLaunch& gl) {
-  return g.nM * g.nN * gl.nbs <= 0x7FFFFFFFll && gl.nbs <= 65535 && g.nK <= 0x3FFFFFFFll &&
+  return g.nM * g.nN * gl.nbs * std::max(gl.nkt, 1) <= 0x7FFFFFFFll && gl.nbs <= 65535 && g.nK <= 0x3FFFFFFFll &&
          g.nB <= 0x7FFFFFFFll;
 }
 

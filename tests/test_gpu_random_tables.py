@@ -166,3 +166,40 @@ def test_lookup_path_used_for_bench_grid(gpu):
     lat = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
     assert plan.kernel_path(lat) == 3
     assert plan.kernel_path(lat, verify=True) == 2
+
+
+@pytest.mark.parametrize("seed,rowblock,lattice", [(21, True, False), (22, True, True), (23, False, False)])
+def test_long_k_axis_few_rows_is_k_tiled(gpu, seed, rowblock, lattice):
+    """Attention-shaped grids (m = n = 1, many batch values, a long k axis):
+    the general grid kernel splits the k axis into tiles; bit-exact against
+    the oracle, verify and latency-only launches alike."""
+    import torch
+    from paper_2603_00549_b200 import _native
+    rng = np.random.default_rng(seed)
+    t, pm, pn, pk = random_tables(rng, 120, 8, 12, rowblock=rowblock, lattice=lattice)
+    dt = _native.DeviceTables(t, 0)
+    B = np.array([8, 12, 16, 24, 40, 64, 96], np.uint64)
+    M = np.array([1], np.uint64) if rowblock else np.array([int(pm[0])], np.uint64)
+    N = np.array([1], np.uint64) if rowblock else np.array([int(pn[0])], np.uint64)
+    K = np.array(sorted(set(rng.integers(1, 60000, 6001).tolist()) | set(pk.tolist())), np.uint64)
+    plan = _native.GridPlan(dt, (B, M, N, K))
+    n = plan.cardinality
+    dev = torch.device("cuda")
+    lat = torch.empty(n, dtype=torch.float64, device=dev)
+    cur = torch.empty(n, dtype=torch.int32, device=dev)
+    blk = torch.empty(n, dtype=torch.int64, device=dev)
+    wav = torch.empty(n, dtype=torch.int64, device=dev)
+    plan.launch(lat, cur, blk, wav)
+    o_lat, o_cur, o_blk, o_wav = oracle.grid(t, (B, M, N, K), use_coords=True)
+    assert np.array_equal(lat.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+    assert np.array_equal(cur.cpu().numpy(), o_cur)
+    assert np.array_equal(wav.cpu().numpy().view(np.uint64), o_wav)
+    fast = torch.empty(n, dtype=torch.float64, device=dev)
+    stats = torch.tensor([-1, 0, 0], dtype=torch.int64, device=dev)
+    plan.launch(fast, nan_stats=stats)
+    assert np.array_equal(fast.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+    nan = np.isnan(o_lat)
+    st = stats.cpu().numpy()
+    assert st[1] == nan.sum()
+    if st[2] == 0:
+        assert st[0] == (int(np.argmax(nan)) if nan.any() else -1)
