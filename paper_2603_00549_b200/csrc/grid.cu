@@ -620,7 +620,7 @@ void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_k, RowL
     o = (o + bytes + 15) & ~int64_t(15);
     return int(at);
   };
-  rl.off_bar = take(8ll * (2 + 2 * kRingMaxSlots));  // prologue + ring FULL/EMPTY mbarriers
+  rl.off_bar = take(8ll * (2 + 3 * kRingMaxSlots));  // prologue + ring FULL/EMPTY/W-ready mbarriers
   rl.off_gcur = take(8ll * t.R);
   rl.off_glk = take(8ll * t.G);
   rl.off_clm = take(8ll * t.CM);
@@ -768,6 +768,24 @@ __device__ __forceinline__ TileXY tile_xy(const RowLaunch& rl, int tile, int nK)
   return x;
 }
 
+// Wave-scale table W[wave class][ib] of one tile's (m, n) and batch slab.
+template <int NB, bool STAGE>
+__device__ __forceinline__ void build_w_table(const RowCtx<STAGE>& c, const GridDev& g,
+                                              const RowIn<NB>& cur, double* W, int lane) {
+  const int NW = c.NW;
+  for (int wc = lane; wc < NW; wc += 32) {
+    const WcParam& p = c.wcp[wc];
+    const uint64_t tmn = wc < 64 ? cur.cm[wc >> 5] * cur.cn[wc >> 5]
+                                 : g.cm_tab[cur.im * NW + wc] * g.cn_tab[cur.jn * NW + wc];
+    const double rw = p.rw;
+#pragma unroll
+    for (int ib = 0; ib < NB; ++ib) {
+      const double w = __ull2double_rn(ceil_div_w(p, 2, cur.b[ib] * tmn, p.bpw));
+      W[wc * NB + ib] = rw == 1.0 ? w : __ddiv_rn(w, rw);
+    }
+  }
+}
+
 // One tile's lookup state (one warp): staircase, wave-scale table, cut
 // points, byte maps, written into the slot `wb`; len / lastpos into its
 // header.
@@ -775,7 +793,7 @@ template <int NB, bool STAGE, int SEGW>
 __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev& g,
                                            const RowLaunch& rl, const TileXY& x,
                                            const RowIn<NB>& cur, uint8_t* wb, int lane,
-                                           int mark_tile = 1 << 30) {
+                                           int mark_tile = 1 << 30, bool with_w = true) {
   uint64_t* sD = reinterpret_cast<uint64_t*>(wb + rl.w_sD);
   int32_t* sP = reinterpret_cast<int32_t*>(wb + rl.w_sP);
   double* W = reinterpret_cast<double*>(wb + rl.w_W);
@@ -836,17 +854,7 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
   }
   ROW_MARK(mark_tile, 5);
   // ---- wave-scale table W[wave class][ib] of this (m, n) and batch slab
-  for (int wc = lane; wc < NW; wc += 32) {
-    const WcParam& p = c.wcp[wc];
-    const uint64_t tmn = wc < 64 ? cur.cm[wc >> 5] * cur.cn[wc >> 5]
-                                 : g.cm_tab[cur.im * NW + wc] * g.cn_tab[cur.jn * NW + wc];
-    const double rw = p.rw;
-#pragma unroll
-    for (int ib = 0; ib < NB; ++ib) {
-      const double w = __ull2double_rn(ceil_div_w(p, 2, cur.b[ib] * tmn, p.bpw));
-      W[wc * NB + ib] = rw == 1.0 ? w : __ddiv_rn(w, rw);
-    }
-  }
+  if (with_w) build_w_table<NB, STAGE>(c, g, cur, W, lane);
   __syncwarp();
   ROW_MARK(mark_tile, 6);
   // ---- cut points: fixed-trip branch-free binary searches, one shared
@@ -1139,6 +1147,10 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
   const int P = rl.prod, S = rl.slots, NC = kRowWarps - P;
   uint64_t* full = bar + 2;
   uint64_t* empty = full + S;
+  // first P positions: writer warp w computes the W table of builder w's
+  // first tile while that builder runs its staircase and searches
+  uint64_t* wready = empty + S;
+  const int nhelp = min(P, min(NC, S));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const RowCtx<STAGE> c = row_ctx<STAGE>(smem, t, g, rl);
 #ifdef PM2L_TIMING
@@ -1151,6 +1163,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       mbar_init(full + s, 32);
       mbar_init(empty + s, 32 * NC);
     }
+    for (int s = 0; s < nhelp; ++s) mbar_init(wready + s, 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     row_prologue<STAGE>(smem, c, t, g, rl, bar);
   }
@@ -1174,19 +1187,34 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
 #endif
       ROW_MARK(tile, 1);
       build_tile<NB, STAGE, SEGW>(c, g, rl, tile_xy(rl, tile, c.nK), cur,
-                                  smem + rl.off_warp + slot * rl.warp_bytes, lane, tile);
+                                  smem + rl.off_warp + slot * rl.warp_bytes, lane, tile,
+                                  /*with_w=*/j >= nhelp);
       __syncwarp();
       ROW_MARK(tile, 2);
       mbar_arrive(full + slot);
     }
   } else {
     const int cw = warp - P;
+    if (cw < nhelp) {
+      // W table of builder cw's first tile (position cw, slot cw)
+      const int tile0 = blockIdx.x + cw * gridDim.x;
+      if (tile0 < rl.tiles) {
+        const RowIn<NB> r0 = load_row_in<NB>(g, rl, tile0, t.NW, lane);
+        mbar_wait(bar, 0);
+        build_w_table<NB, STAGE>(c, g, r0,
+                                 reinterpret_cast<double*>(smem + rl.off_warp + cw * rl.warp_bytes + rl.w_W),
+                                 lane);
+      }
+      __syncwarp();
+      mbar_arrive(wready + cw);
+    }
     mbar_wait(bar, 0);
     if (STAGE) mbar_wait(bar + 1, 0);
     pdl_wait();  // base table complete and visible
     for (int j = 0, tile = blockIdx.x; tile < rl.tiles; ++j, tile += gridDim.x) {
       const int slot = j % S, use = j / S;
       mbar_wait(full + slot, use & 1);
+      if (j < nhelp) mbar_wait(wready + j, 0);
       if (cw == 0) ROW_MARK(tile, 3);
       emit_tile<NB, STAGE>(c, t, g, rl, tile_xy(rl, tile, c.nK),
                            smem + rl.off_warp + slot * rl.warp_bytes, base_tab, out, cw, NC,
