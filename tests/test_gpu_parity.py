@@ -401,3 +401,26 @@ def test_batched_store_lookup_matches_scalar_lookup(gpu, tmp_path, sparse):
                 st.lookup_many(q)
             b, m, n, k = (int(v) for v in q[absent[0]])
             assert f"batch={b} m={m} n={n} k={k}" in str(exc.value)
+
+
+def test_device_table_set_serves_mixed_grids(gpu):
+    """Grids of several triples through one DeviceTableSet: each triple's
+    tables are uploaded once and predictions equal fresh PreparedGrids'."""
+    from paper_2603_00549_b200 import backend
+    from paper_2603_00549_b200.compute import WaveModel
+    from paper_2603_00549_b200.nascache import GridSpec, PreparedGrid
+    from paper_2603_00549_b200.staging import DeviceTableSet
+    ds = dataset("bf16")
+    st = DeviceTableSet(ds)
+    assert st.stage_all() == len(st.triples())
+    handles = {}
+    for fam, dt, tm in st.triples():
+        for ks in ((32, 700, 4096), (100, 9000)):
+            grid = GridSpec(fam, dt, tm, {"batch": (1, 3), "m": (64, 200, 1000), "n": (96, 512),
+                                          "k": ks})
+            prep = st.prepared(grid, ds)
+            handles.setdefault((fam, dt, tm), set()).add(id(prep.device_tables(0)))
+            got = backend.predict_grid(prep)
+            want = backend.predict_grid(PreparedGrid(ds, grid, WaveModel(ds.device.sm_count)))
+            assert np.array_equal(_bits(got), _bits(want))
+    assert all(len(v) == 1 for v in handles.values())

@@ -223,3 +223,33 @@ def test_membound_fit_matches_reference_fit():
         assert np.array_equal(np.array(m.weights), z["weights"][i])
         assert m.intercept == z["intercept"][i]
         assert m.max_rel_err == z["max_rel_err"][i]
+
+
+def test_device_table_set_stages_every_triple_once():
+    """one host build per (family, dtype, transpose) triple,
+    identical to PreparedGrid.tables(); fingerprint-guarded reuse."""
+    import numpy as np
+    from conftest import dataset
+    from paper_2603_00549_b200.compute import WaveModel
+    from paper_2603_00549_b200.core import DType, TransposeMode
+    from paper_2603_00549_b200.errors import StaleCache
+    from paper_2603_00549_b200.nascache import GridSpec, PreparedGrid
+    from paper_2603_00549_b200.staging import DeviceTableSet
+    ds = dataset("bf16")
+    st = DeviceTableSet(ds)
+    fams = {t[0] for t in st.triples()}
+    assert {"matmul", "linear", "batched_matmul"} <= fams
+    for fam, dt, tm in st.triples():
+        grid = GridSpec(fam, dt, tm, {"batch": (1, 2), "m": (64, 128), "n": (96,), "k": (32, 4096)})
+        ref = PreparedGrid(ds, grid, WaveModel(ds.device.sm_count)).tables()
+        got = st.host_tables(fam, dt, tm)
+        assert set(ref) == set(got)
+        for k in ref:
+            a, b = ref[k], got[k]
+            if a is None:
+                assert b is None
+            else:
+                assert np.array_equal(np.asarray(a), np.asarray(b)), k
+    st.verify(ds)
+    with pytest.raises(StaleCache):
+        st.verify(dataset("fp32"))
