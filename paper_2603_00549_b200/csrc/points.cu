@@ -120,7 +120,58 @@ __device__ int nearest_point(const TablesDev& t, const PointSmem& S, double qm, 
   return best_i;
 }
 
-template <bool G32>
+// One member class (every shipped preset; equal logs imply equal
+// coordinates): the grid kernel's nearest_one_class decision per op, with
+// the row part from ONE pass over the members -- dmin and its first member
+// (case A: mn(k) <= dmin) and the first member within mn(k) (case B).
+// Returns the original candidate scan index; *out_best = the distance.
+__device__ int nearest_point_one_class(const TablesDev& t, const PointSmem& S, double qm,
+                                       double qn, double qk, uint64_t* out_best) {
+  const int G = t.G;
+  int lo = 0, hi = G;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (S.glk[mid] < qk) lo = mid + 1; else hi = mid;
+  }
+  const int start = lo;
+  auto dk = [&](int g) { return abs_bits(__dsub_rn(S.glk[g], qk)); };
+  const uint64_t dkL = start > 0 ? dk(start - 1) : ~0ull;
+  const uint64_t dkR = start < G ? dk(start) : ~0ull;
+  const uint64_t mn = dkL < dkR ? dkL : dkR;
+  const int CM = S.csize[0];
+  uint64_t dmin = ~0ull;
+  int argmin = 0, first_mn = -1;
+  for (int j = 0; j < CM; ++j) {
+    const uint64_t d = member_d(S, j, qm, qn);
+    if (d < dmin) { dmin = d; argmin = j; }
+    if (first_mn < 0 && d <= mn) first_mn = j;
+  }
+  int g, pos;
+  uint64_t best;
+  if (mn <= dmin) {  // best == dmin: the leftmost group within dmin, member argmin
+    if (dkL <= dmin) {
+      g = start - 1;
+      while (g > 0 && dk(g - 1) <= dmin) --g;
+    } else {
+      g = start;
+    }
+    pos = argmin;
+    best = dmin;
+  } else {           // best == mn: the leftmost nearest group, first member within mn
+    if (dkL == mn) {
+      g = start - 1;
+      while (g > 0 && dk(g - 1) == mn) --g;
+    } else {
+      g = start;
+    }
+    pos = first_mn;
+    best = mn;
+  }
+  *out_best = best;
+  return S.gidx[S.gstart[g] + pos];
+}
+
+template <int NEARK>  // 0 general sweep, 1 sweep + tie mask (G <= 32), 2 one member class
 __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uint4* __restrict__ shapes,
                                                           int64_t n, const double* __restrict__ lut,
                                                           int64_t lut_n, double* __restrict__ out_lat,
@@ -168,7 +219,8 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
       match = 0;
     } else if (t.R > 0) {
       uint64_t best;
-      rec = nearest_point<G32>(t, S, lut[s.y], lut[s.z], lut[s.w], &best);
+      rec = NEARK == 2 ? nearest_point_one_class(t, S, lut[s.y], lut[s.z], lut[s.w], &best)
+                       : nearest_point<NEARK == 1>(t, S, lut[s.y], lut[s.z], lut[s.w], &best);
       ci = t.cand_curve[rec];
       dist = __longlong_as_double(static_cast<long long>(best));
       match = 1;
@@ -225,7 +277,8 @@ int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const d
   if (n == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t smem = 16ll * t.CM + 8ll * t.G + 8ll * t.G + 8ll * t.NC + 4ll * t.R + 64;
-  auto* fn = t.G <= 32 ? points_kernel<true> : points_kernel<false>;
+  auto* fn = (t.NC == 1 && t.lowest_wins) ? points_kernel<2>
+             : t.G <= 32 ? points_kernel<1> : points_kernel<0>;
   if (smem > 227 * 1024) return int(cudaErrorInvalidValue);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
