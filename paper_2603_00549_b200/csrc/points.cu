@@ -139,13 +139,17 @@ __device__ int nearest_point_one_class(const TablesDev& t, const PointSmem& S, d
   const uint64_t dkR = start < G ? dk(start) : ~0ull;
   const uint64_t mn = dkL < dkR ? dkL : dkR;
   const int CM = S.csize[0];
-  uint64_t dmin = ~0ull;
+  // distances are non-negative finite doubles, so FP64 order is the order
+  // of their |.| bits (member_d): compare them as doubles (DMNMX / DSETP)
+  const double mnd = __longlong_as_double(static_cast<long long>(mn));
+  double dminf = __longlong_as_double(0x7FF0000000000000ll);  // +inf
   int argmin = 0, first_mn = -1;
   for (int j = 0; j < CM; ++j) {
-    const uint64_t d = member_d(S, j, qm, qn);
-    if (d < dmin) { dmin = d; argmin = j; }
-    if (first_mn < 0 && d <= mn) first_mn = j;
+    const double d = fmax(fabs(__dsub_rn(S.lm[j], qm)), fabs(__dsub_rn(S.ln[j], qn)));
+    if (d < dminf) { dminf = d; argmin = j; }
+    if (first_mn < 0 && d <= mnd) first_mn = j;
   }
+  const uint64_t dmin = abs_bits(dminf);
   int g, pos;
   uint64_t best;
   if (mn <= dmin) {  // best == dmin: the leftmost group within dmin, member argmin
