@@ -550,6 +550,7 @@ constexpr int kRingMaxSlots = 16;
 #ifdef PM2L_TIMING
 // diagnostic build only (tools/row_timing.py): per-tile phase timestamps
 __device__ unsigned long long g_row_dbg[16384 * 8];
+__device__ unsigned long long g_pdl_dbg[4096 * 4];  // per CTA: entry, before/after pdl wait, first FULL
 #define ROW_MARK(tile, i)                                                         \
   do {                                                                            \
     if (lane == 0 && (tile) < 16384) {                                            \
@@ -1210,11 +1211,23 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
     }
     mbar_wait(bar, 0);
     if (STAGE) mbar_wait(bar + 1, 0);
+#ifdef PM2L_TIMING
+    if (cw == 0 && lane == 0 && blockIdx.x < 4096) {
+      g_pdl_dbg[blockIdx.x * 4] = t_entry;
+      g_pdl_dbg[blockIdx.x * 4 + 1] = clock64();
+    }
+#endif
     pdl_wait();  // base table complete and visible
+#ifdef PM2L_TIMING
+    if (cw == 0 && lane == 0 && blockIdx.x < 4096) g_pdl_dbg[blockIdx.x * 4 + 2] = clock64();
+#endif
     for (int j = 0, tile = blockIdx.x; tile < rl.tiles; ++j, tile += gridDim.x) {
       const int slot = j % S, use = j / S;
       mbar_wait(full + slot, use & 1);
       if (j < nhelp) mbar_wait(wready + j, 0);
+#ifdef PM2L_TIMING
+      if (j == 0 && cw == 0 && lane == 0 && blockIdx.x < 4096) g_pdl_dbg[blockIdx.x * 4 + 3] = clock64();
+#endif
       if (cw == 0) ROW_MARK(tile, 3);
       emit_tile<NB, STAGE>(c, t, g, rl, tile_xy(rl, tile, c.nK),
                            smem + rl.off_warp + slot * rl.warp_bytes, base_tab, out, cw, NC,
@@ -1581,6 +1594,7 @@ int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* ws, dou
 
 #ifdef PM2L_TIMING
 int row_timing_copy(unsigned long long* host, int n) {
+  if (n < 0) return int(cudaMemcpyFromSymbol(host, g_pdl_dbg, sizeof(unsigned long long) * size_t(-n)));
   return int(cudaMemcpyFromSymbol(host, g_row_dbg, sizeof(unsigned long long) * size_t(n)));
 }
 #endif

@@ -73,6 +73,13 @@ def main():
         for nt in sorted(set(cta_n.tolist())):
             e = cta_end[cta_n == nt]
             print(f"CTAs with {nt} tiles: {len(e)}, end median {np.median(e):.2f} p90 {np.percentile(e, 90):.2f} max {e.max():.2f}")
+        pd = np.zeros(4096 * 4, np.uint64)
+        assert fn(pd.ctypes.data, -len(pd)) == 0
+        pd = pd.reshape(-1, 4)[:ctas].astype(np.int64)
+        pr = (pd - pd[:, :1]) / mhz
+        print(f"writers (CTA entry=0): reach pdl wait median {np.median(pr[:, 1]):.2f}, leave "
+              f"median {np.median(pr[:, 2]):.2f} max {pr[:, 2].max():.2f}, first FULL median "
+              f"{np.median(pr[:, 3]):.2f} max {pr[:, 3].max():.2f} us")
         d = lambda a, b: np.median(rel[:, b] - rel[:, a])  # noqa: E731
         print(f"build: staircase {d(1, 5):.2f}  W {d(5, 6):.2f}  cuts {d(6, 7):.2f}  maps {d(7, 2):.2f}")
         print("build dur median", np.median(rel[:, 2] - rel[:, 1]), " emit dur median",
