@@ -572,6 +572,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -621,7 +624,7 @@ void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_k, RowL
     o = (o + bytes + 15) & ~int64_t(15);
     return int(at);
   };
-  rl.off_bar = take(8ll * (2 + 3 * kRingMaxSlots));  // prologue + ring FULL/EMPTY/W-ready mbarriers
+  rl.off_bar = take(8ll * (2 + 4 * kRingMaxSlots));  // prologue + ring FULL/EMPTY/W-/stair-ready
   rl.off_gcur = take(8ll * t.R);
   rl.off_glk = take(8ll * t.G);
   rl.off_clm = take(8ll * t.CM);
@@ -794,7 +797,10 @@ template <int NB, bool STAGE, int SEGW>
 __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev& g,
                                            const RowLaunch& rl, const TileXY& x,
                                            const RowIn<NB>& cur, uint8_t* wb, int lane,
-                                           int mark_tile = 1 << 30, bool with_w = true) {
+                                           int mark_tile = 1 << 30, bool with_w = true,
+                                           uint64_t* stair_ready = nullptr) {
+  // stair_ready != nullptr: a helper warp builds the group cuts and gmap of
+  // this tile (help_group_map) once the staircase is published
   uint64_t* sD = reinterpret_cast<uint64_t*>(wb + rl.w_sD);
   int32_t* sP = reinterpret_cast<int32_t*>(wb + rl.w_sP);
   double* W = reinterpret_cast<double*>(wb + rl.w_W);
@@ -854,6 +860,15 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
     if (tail < dmin) dmin = tail;
   }
   ROW_MARK(mark_tile, 5);
+  const bool with_g = stair_ready == nullptr;
+  if (!with_g) {  // publish len and dmin for the helper
+    if (lane == 0) {
+      hdr[0] = len;
+      *reinterpret_cast<uint64_t*>(hdr + 2) = dmin;
+    }
+    __syncwarp();
+    mbar_arrive(stair_ready);
+  }
   // ---- wave-scale table W[wave class][ib] of this (m, n) and batch slab
   if (with_w) build_w_table<NB, STAGE>(c, g, cur, W, lane);
   __syncwarp();
@@ -869,7 +884,7 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
     const int k0 = x.k0, kc = x.kc;
     int top = 1;
     while (top * 2 <= kc) top *= 2;
-    for (int i = lane; i < len + c.G; i += 32) {
+    for (int i = lane; i < len + (with_g ? c.G : 0); i += 32) {
       const bool rk = i < len, strict = i == len - 1;
       const int gg = rk ? 0 : i - len;
       const uint64_t xv = rk ? sD[i] : dmin;
@@ -897,7 +912,7 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
     constexpr int QW = SL / 8;  // u64 words per lane
     constexpr uint64_t kOnes = 0x0101010101010101ull;
     const int r0 = lane * SL;
-    const int nr = len - 1, ng = c.G, ff = cut[len - 1];
+    const int nr = len - 1, ng = with_g ? c.G : 0, ff = cut[len - 1];
     // first s with cut[s] > r0 in each cut list, both searches interleaved
     int b0 = 0, h0 = nr, b1 = 0, h1 = ng;
     const int32_t* cg = cut + len;
@@ -941,13 +956,68 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
 #pragma unroll
     for (int q = 0; q < QW; q += 2) {
       *reinterpret_cast<ulonglong2*>(mw0 + q) = make_ulonglong2(w0[q], w0[q + 1]);
-      *reinterpret_cast<ulonglong2*>(mw1 + q) = make_ulonglong2(w1[q], w1[q + 1]);
+      if (with_g) *reinterpret_cast<ulonglong2*>(mw1 + q) = make_ulonglong2(w1[q], w1[q + 1]);
     }
   }
   if (lane == 0) {
     hdr[0] = len;
     hdr[1] = lastpos;
   }
+}
+
+// Helper warp's share of a tile build (first tiles of the ring kernel): the
+// group cuts and gmap, from the staircase the builder published (len, dmin
+// in the slot header).  Same searches and map construction as build_tile.
+template <bool STAGE, int SEGW>
+__device__ __forceinline__ void help_group_map(const RowCtx<STAGE>& c, const GridDev& g,
+                                               const RowLaunch& rl, const TileXY& x, uint8_t* wb,
+                                               int lane) {
+  constexpr int SL = SEGW * 4;
+  const int32_t* hdr = reinterpret_cast<const int32_t*>(wb + rl.w_hdr);
+  const int len = hdr[0];
+  const uint64_t dmin = *reinterpret_cast<const uint64_t*>(hdr + 2);
+  int32_t* cg = reinterpret_cast<int32_t*>(wb + rl.w_cut) + len;
+  const int k0 = x.k0, kc = x.kc, G = c.G;
+  int top = 1;
+  while (top * 2 <= kc) top *= 2;
+  for (int gg = lane; gg < G; gg += 32) {
+    const double lk = c.glk[gg];
+    const int kr = c.krt[x.kcx * G + gg];
+    int lo = 0;
+    for (int step = top; step; step >>= 1) {
+      const int r = k0 + min(lo + step, kc) - 1;
+      const double q = STAGE ? __longlong_as_double(static_cast<long long>(lds_u64(c.kq_s + 8u * uint32_t(r))))
+                             : c.kq[r];
+      const bool keep = r - k0 < kr || abs_bits(__dsub_rn(q, lk)) <= dmin;
+      lo += (lo + step <= kc && keep) ? step : 0;
+    }
+    cg[gg] = lo;
+  }
+  __syncwarp();
+  constexpr int QW = SL / 8;
+  constexpr uint64_t kOnes = 0x0101010101010101ull;
+  const int r0 = lane * SL;
+  int b = 0, h = G;
+  while (b < h) {
+    const int m = (b + h) >> 1;
+    if (cg[m] <= r0) b = m + 1; else h = m;
+  }
+  uint64_t w[QW];
+#pragma unroll
+  for (int q = 0; q < QW; ++q) w[q] = uint64_t(b) * kOnes;
+  for (int s2 = b; s2 < G; ++s2) {
+    const int e = cg[s2] - r0;
+    if (e >= SL) break;
+#pragma unroll
+    for (int q = 0; q < QW; ++q) {
+      const int sh = e - 8 * q;
+      w[q] += sh <= 0 ? kOnes : sh >= 8 ? 0ull : (kOnes << (8 * sh));
+    }
+  }
+  uint64_t* mw = reinterpret_cast<uint64_t*>(wb + rl.w_gmap) + lane * QW;
+#pragma unroll
+  for (int q = 0; q < QW; q += 2)
+    *reinterpret_cast<ulonglong2*>(mw + q) = make_ulonglong2(w[q], w[q + 1]);
 }
 
 // Write one tile's points from its slot: 32-pair blocks b0, b0 + bstep, ...
@@ -1134,9 +1204,6 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t
 // the CTA's tile order; the other warps write the points, each taking every
 // (kRowWarps - kRingProd)-th 32-pair block of a tile.  Writing starts after
 // one tile's build and later builds proceed under the store stream.
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 template <int NB, bool STAGE, int SEGW>
 __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev t, GridDev g,
@@ -1151,6 +1218,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
   // first P positions: writer warp w computes the W table of builder w's
   // first tile while that builder runs its staircase and searches
   uint64_t* wready = empty + S;
+  uint64_t* sready = wready + kRingMaxSlots;  // builder's staircase published (first tiles)
   const int nhelp = min(P, min(NC, S));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const RowCtx<STAGE> c = row_ctx<STAGE>(smem, t, g, rl);
@@ -1164,7 +1232,10 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       mbar_init(full + s, 32);
       mbar_init(empty + s, 32 * NC);
     }
-    for (int s = 0; s < nhelp; ++s) mbar_init(wready + s, 32);
+    for (int s = 0; s < nhelp; ++s) {
+      mbar_init(wready + s, 32);
+      mbar_init(sready + s, 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     row_prologue<STAGE>(smem, c, t, g, rl, bar);
   }
@@ -1189,7 +1260,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       ROW_MARK(tile, 1);
       build_tile<NB, STAGE, SEGW>(c, g, rl, tile_xy(rl, tile, c.nK), cur,
                                   smem + rl.off_warp + slot * rl.warp_bytes, lane, tile,
-                                  /*with_w=*/j >= nhelp);
+                                  /*with_w=*/j >= nhelp, j < nhelp ? sready + j : nullptr);
       __syncwarp();
       ROW_MARK(tile, 2);
       mbar_arrive(full + slot);
@@ -1200,11 +1271,13 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       // W table of builder cw's first tile (position cw, slot cw)
       const int tile0 = blockIdx.x + cw * gridDim.x;
       if (tile0 < rl.tiles) {
+        uint8_t* wb0 = smem + rl.off_warp + cw * rl.warp_bytes;
         const RowIn<NB> r0 = load_row_in<NB>(g, rl, tile0, t.NW, lane);
         mbar_wait(bar, 0);
-        build_w_table<NB, STAGE>(c, g, r0,
-                                 reinterpret_cast<double*>(smem + rl.off_warp + cw * rl.warp_bytes + rl.w_W),
-                                 lane);
+        build_w_table<NB, STAGE>(c, g, r0, reinterpret_cast<double*>(wb0 + rl.w_W), lane);
+        if (STAGE) mbar_wait(bar + 1, 0);
+        mbar_wait(sready + cw, 0);  // the builder's staircase is published
+        help_group_map<STAGE, SEGW>(c, g, rl, tile_xy(rl, tile0, c.nK), wb0, lane);
       }
       __syncwarp();
       mbar_arrive(wready + cw);
