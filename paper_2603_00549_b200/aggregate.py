@@ -20,7 +20,7 @@ from .compute import (CLAMP_ABOVE, CLAMP_BELOW, MATCH_EXACT, MATCH_NEAREST, Conf
                       WaveModel, _check_pair)
 from .core import (COMPUTE_FAMILIES, FAMILY_LINEAR, DType, KernelKey, LayerSpec, ModelGraph,
                    Prediction, TransposeMode, is_utility_family, utility_kernel_name)
-from .errors import InsufficientData, PredictionError, UnresolvedLayer
+from .errors import InsufficientData, PredictionError, UnresolvedLayer, ValidationError
 from .ingest import Dataset
 from .membound import DEFAULT_LAUNCH_FLOOR_US, MemBoundModel, fit
 
@@ -244,3 +244,77 @@ def predict_model(graph: ModelGraph, dataset: Dataset, wm: Optional[WaveModel] =
                   membound_floor_us: float = DEFAULT_LAUNCH_FLOOR_US) -> ModelPrediction:
     """Predict every layer and sum exactly (aggregate.py:173-196)."""
     return predict_models([graph], dataset, wm, membound_floor_us)[0]
+
+
+@dataclass(frozen=True)
+class TemplateLayer:
+    """One layer of a model template (the same kind for every model of a
+    NAS grid): a compute family (shape per model) or a utility kernel
+    (features per model)."""
+    layer_id: str
+    family: str
+    dtype: DType
+    transpose_mode: Optional[TransposeMode] = None
+
+
+def predict_model_grid(template: Sequence[TemplateLayer], shapes, features, dataset: Dataset,
+                       wm: Optional[WaveModel] = None,
+                       membound_floor_us: float = DEFAULT_LAUNCH_FLOOR_US):
+    """predict_models for a NAS grid given as arrays: ``shapes`` [n_models,
+    L, 4] (batch, m, n, k; compute layers), ``features`` [n_models, L, 5]
+    (utility layers; FIELD_ORDER).  Returns (per-layer latency f64[n, L],
+    per-model total f64[n]) with the same values as predict_models on the
+    equivalent graphs (resolution + prediction per compute layer in one
+    device batch per kernel triple, pm2l_points_predict; membound batches;
+    exact per-model totals, pm2l_segment_fsum).  Raises UnresolvedLayer for
+    the first (model, layer) that cannot be predicted."""
+    from . import _device, _native
+    from .compute import _shapes_u32
+    from .membound import predict_membound_batch
+    pred = ModelPredictor(dataset, wm, membound_floor_us)
+    L = len(template)
+    shapes = np.asarray(shapes)
+    n = shapes.shape[0] if shapes.ndim == 3 else np.asarray(features).shape[0]
+    lat = np.full((n, L), np.nan)
+    by_triple: Dict[tuple, List[int]] = {}
+    util: Dict[tuple, List[int]] = {}
+    for l, t in enumerate(template):
+        if is_utility_family(t.family):
+            util.setdefault((utility_kernel_name(t.family), t.dtype), []).append(l)
+        elif t.family in COMPUTE_FAMILIES:
+            tr = t.transpose_mode or default_transpose(t.family)
+            by_triple.setdefault((t.family, t.dtype, tr), []).append(l)
+        else:
+            raise UnresolvedLayer(f"layer {t.layer_id!r}: no predictor for family {t.family!r}")
+    dev = _device.device()
+    for triple, ls in by_triple.items():
+        *_, dt = pred.resolver.triple_tables(*triple)
+        s = _shapes_u32(shapes[:, ls, :].reshape(-1, 4))
+        if s.size and s.max() >= (1 << 22):
+            raise ValidationError("explicit-descriptor coordinates must be < 2^22")
+        d_s = _device.to_device(s, dev)
+        out = _device.empty(len(s), "float64", dev)
+        _native.check(_native.load().pm2l_points_predict(
+            dt.handle, _native.ptr(d_s), len(s), _native.ptr(out), 0, 0, 0, 0, 0,
+            _device.stream()), "pm2l_points_predict")
+        lat[:, ls] = _device.to_numpy(out).reshape(n, len(ls))
+    if util:
+        f = np.asarray(features, dtype=np.float64)
+        models, mids, cols = [], [], []
+        for mi, ((name, dt_), ls) in enumerate(util.items()):
+            models.append(pred.membound_model(name, dt_))
+            for l in ls:
+                cols.append(l)
+                mids.append(mi)
+        feats = np.concatenate([f[:, l, :] for l in cols])
+        ids = np.repeat(np.array(mids, np.int32), n)
+        ulat, _ = predict_membound_batch(models, feats, ids, [membound_floor_us] * len(models))
+        for j, l in enumerate(cols):
+            lat[:, l] = ulat[j * n:(j + 1) * n]
+    bad = np.isnan(lat)
+    if bad.any():
+        i, l = np.argwhere(bad)[0]
+        raise UnresolvedLayer(f"model {int(i)} layer {template[l].layer_id!r}: no usable kernel "
+                              f"configuration")
+    totals = segment_fsum(lat.ravel(), np.arange(0, n * L + 1, L, dtype=np.int64))
+    return lat, totals

@@ -424,3 +424,25 @@ def test_device_table_set_serves_mixed_grids(gpu):
             want = backend.predict_grid(PreparedGrid(ds, grid, WaveModel(ds.device.sm_count)))
             assert np.array_equal(_bits(got), _bits(want))
     assert all(len(v) == 1 for v in handles.values())
+
+
+def test_predict_model_grid_matches_predict_models(gpu):
+    """The array-native NAS-grid path (template + shape/feature arrays) gives
+    the same per-layer latencies and fsum totals as predict_models."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(GOLDEN), "..", "tools"))
+    import c4
+    from paper_2603_00549_b200.aggregate import TemplateLayer, predict_model_grid, predict_models
+    from paper_2603_00549_b200.core import DType
+    ds = dataset("fp32_full")
+    params = [(b, s, h, r) for b in (1, 3, 16) for s in (64, 500, 2048) for h in (256, 768, 1280)
+              for r in (2, 4)]
+    fams = ("linear", "linear", "linear", "batched_matmul", "utility:softmax", "linear", "linear",
+            "linear")
+    template = [TemplateLayer(i, f, DType.FP32) for i, f in zip(c4.TEMPLATE_IDS, fams)]
+    shapes, feats = c4.grid_arrays(params)
+    lat, tot = predict_model_grid(template, shapes, feats, ds)
+    res = predict_models([c4.block(*p) for p in params], ds)
+    for i, r in enumerate(res):
+        assert tot[i].hex() == r.total_latency_us.hex()
+        assert [x.hex() for x in lat[i]] == [lp.prediction.latency_us.hex() for lp in r.per_layer]
