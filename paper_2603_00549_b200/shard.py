@@ -136,3 +136,36 @@ def precompute_sharded(grid, dataset, wm, out_path, group=None, skip_unresolved:
     if res.full is not None:
         write_store(out_path, grid, dataset, res.full)
     return res
+
+
+def topk_global(values: np.ndarray, k: int, offset: int = 0, group=None) -> Tuple[np.ndarray, np.ndarray]:
+    """The k smallest of a value array sharded over the ranks (SURVEY §8e:
+    all-gather of the per-rank top-k, merged by (value, global index)).
+    ``values`` is this rank's slice, ``offset`` its first global index.
+    Returns (global indices i64[k'], values f64[k']), k' = min(k, total),
+    identical on every rank; ties go to the smaller global index and NaN
+    (unresolved) never ranks."""
+    import torch
+    dist = _dist()
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    ok = ~np.isnan(v)
+    idx = np.nonzero(ok)[0]
+    order = np.lexsort((idx, v[idx]))[:k]          # (value, index) ascending
+    loc_i = idx[order] + offset
+    loc_v = v[idx[order]]
+    dev = _tensor_device(group)
+    world = dist.get_world_size(group)
+    pad_i = np.full(k, np.iinfo(np.int64).max, np.int64)
+    pad_v = np.full(k, np.inf)
+    pad_i[:len(loc_i)] = loc_i
+    pad_v[:len(loc_v)] = loc_v
+    mine = torch.from_numpy(np.concatenate([pad_v.view(np.int64), pad_i])).to(dev)
+    allv = torch.empty(2 * k * world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allv, mine, group=group)
+    a = allv.cpu().numpy().reshape(world, 2, k)
+    vals = a[:, 0, :].reshape(-1).view(np.float64)
+    ids = a[:, 1, :].reshape(-1)
+    keep = ids != np.iinfo(np.int64).max
+    vals, ids = vals[keep], ids[keep]
+    sel = np.lexsort((ids, vals))[:k]
+    return ids[sel], vals[sel]

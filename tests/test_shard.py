@@ -149,3 +149,46 @@ def test_global_first_unresolved_lives_on_the_second_rank(tmp_path):
             prep.grid, min(late))
         assert o["raised"] is not None and f"batch={b} m={m} n={n} k={k}" in o["raised"]
     assert np.isnan(outs[0]["full"][list(late)]).all()
+
+
+def _topk_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_00549_b200.shard import shard_bounds, topk_global
+        rng = np.random.default_rng(0)
+        allv = np.round(rng.uniform(1, 50, 1003), 1)    # many exact ties
+        allv[rng.choice(1003, 40, replace=False)] = np.nan
+        lo, hi = shard_bounds(len(allv), world, rank)
+        out = {"rank": rank}
+        for k in (1, 7, 64, 5000):
+            ids, vals = topk_global(allv[lo:hi], k, offset=lo)
+            out[k] = (ids, vals)
+        q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_topk_global_merges_by_value_then_index(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_topk_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(0)
+    allv = np.round(rng.uniform(1, 50, 1003), 1)
+    allv[rng.choice(1003, 40, replace=False)] = np.nan
+    ok = np.nonzero(~np.isnan(allv))[0]
+    ref = ok[np.lexsort((ok, allv[ok]))]
+    for o in outs:
+        for k in (1, 7, 64, 5000):
+            ids, vals = o[k]
+            assert np.array_equal(ids, ref[:k])
+            assert np.array_equal(vals, allv[ref[:k]])
