@@ -107,6 +107,28 @@ __device__ __forceinline__ double wave_scale(const TablesDev& t, int c, uint64_t
   return __ddiv_rn(w, rw);
 }
 
+// ceil(a / d) for a curve's divisor j (0 tile_m, 1 tile_n, 2 blocks per
+// wave) from its parameters held in registers (same result as ceil_div_c)
+__device__ __forceinline__ uint64_t ceil_div_p(const WcParam& p, int j, uint64_t a, uint64_t d) {
+  const uint64_t num = a + d - 1;
+  const uint32_t s = p.ds[j];
+  if ((s >> 16) && num <= 0xFFFFFFFFull) {
+    const uint32_t n32 = uint32_t(num);
+    const uint32_t q = __umulhi(p.dm[j], n32);
+    return uint64_t((q + ((n32 - q) >> (s & 0xFF))) >> ((s >> 8) & 0xFF));
+  }
+  return num / d;
+}
+
+__device__ __forceinline__ WcParam curve_params(const TablesDev& t, int c) {
+  WcParam q;
+  q.tm = t.tile_m[c]; q.tn = t.tile_n[c]; q.sk = t.split_k[c]; q.bpw = t.bpw[c];
+  q.rw = t.ref_waves[c];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) { q.dm[j] = t.dv_m[3 * c + j]; q.ds[j] = t.dv_s[3 * c + j]; }
+  return q;
+}
+
 struct PointResult {
   double lat;
   uint64_t blocks, waves;
@@ -120,6 +142,19 @@ __device__ __forceinline__ PointResult predict_point(const TablesDev& t, int c, 
   r.blocks = blocks_of(t, c, b, m, n, k);
   r.waves = ceil_div_c(t, c, 2, r.blocks, t.bpw[c]);
   r.lat = __dmul_rn(base, wave_scale(t, c, r.waves));
+  return r;
+}
+
+// predict_point from a curve's parameters in registers (rowblock flag apart)
+__device__ __forceinline__ PointResult predict_point_p(const WcParam& p, bool rowblock, uint64_t b,
+                                                       uint64_t m, uint64_t n, uint64_t k,
+                                                       double base) {
+  PointResult r;
+  r.blocks = rowblock ? ceil_div_p(p, 0, b * k, p.tm)
+                      : b * ceil_div_p(p, 0, m, p.tm) * ceil_div_p(p, 1, n, p.tn) * p.sk;
+  r.waves = ceil_div_p(p, 2, r.blocks, p.bpw);
+  const double w = __ull2double_rn(r.waves);
+  r.lat = __dmul_rn(base, p.rw == 1.0 ? w : __ddiv_rn(w, p.rw));
   return r;
 }
 

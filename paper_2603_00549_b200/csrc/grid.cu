@@ -442,6 +442,11 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
       continue;
     }
     const uint64_t k = g.K[ik];
+    // the curve's parameters once per k (registers), then the slab's batch
+    // values in arithmetic only
+    const WcParam cpar = MODE == 2 ? curve_params(t, ci) : WcParam{};
+    const bool crb = MODE == 2 ? t.rowblock[ci] != 0 : false;
+    const uint64_t m_val = MODE == 2 ? g.M[im] : 0, n_val = MODE == 2 ? g.N[jn] : 0;
     for (int ib = 0; ib < nb; ++ib, o += plane) {
       const uint64_t b = g.B[g.b_lo + ib0 + ib];
       double lat;
@@ -451,7 +456,7 @@ __device__ __forceinline__ void consume_tile(const TablesDev& t, const GridDev& 
         waves = ceil_div_c(t, ci, 2, blocks, t.bpw[ci]);
         lat = __dmul_rn(base, wave_scale(t, ci, waves));
       } else {
-        const PointResult r = predict_point(t, ci, b, g.M[im], g.N[jn], k, base);
+        const PointResult r = predict_point_p(cpar, crb, b, m_val, n_val, k, base);
         lat = r.lat;
         blocks = r.blocks;
         waves = r.waves;
@@ -1441,19 +1446,30 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
     gl.mode = (t.all_gemm && 8ll * t.C * (gl.bper + 1) <= 96 * 1024) ? 0 : 2;
     return gl;
   }
-  // warp-specialised grid kernel: (row, batch slab) tiles
+  // warp-specialised grid kernel: (row, batch slab, k tile) tiles.  With few
+  // rows, row-block (general-mode) grids split the k axis first (>= 256 k
+  // per tile): a tile then resolves each k once for its whole batch slab
   const int64_t target_tiles = 148 * 8;
   int64_t nbs = 1;
-  if (rows < target_tiles && nb > 1) nbs = std::min<int64_t>(nb, (target_tiles + rows - 1) / rows);
+  const bool k_first = !t.all_gemm && rows < target_tiles;
+  if (k_first) {
+    const int64_t nkt_max = std::max<int64_t>(1, g.nK / kConsumers);
+    const int64_t per_row = (target_tiles + rows - 1) / rows;
+    if (per_row > nkt_max && nb > 1)
+      nbs = std::min<int64_t>(nb, (per_row + nkt_max - 1) / nkt_max);
+  } else if (rows < target_tiles && nb > 1) {
+    nbs = std::min<int64_t>(nb, (target_tiles + rows - 1) / rows);
+  }
   gl.bper = int((nb + nbs - 1) / nbs);
   gl.nbs = int((nb + gl.bper - 1) / gl.bper);
   // too few (row, slab) tiles (attention grids: one (m, n) row, long k axis):
   // split the k axis too, >= 1024 k values per tile
   gl.nkt = 1;
   gl.kt = int(g.nK);
-  if (rows * gl.nbs < target_tiles && g.nK > 1024)
+  const int64_t min_kt = k_first ? kConsumers : 1024;
+  if (rows * gl.nbs < target_tiles && g.nK > min_kt)
     gl.nkt = int(std::min<int64_t>((target_tiles + rows * gl.nbs - 1) / (rows * gl.nbs),
-                                   (g.nK + 1023) / 1024));
+                                   (g.nK + min_kt - 1) / min_kt));
   if (gl.nkt > 1) {
     gl.kt = int((g.nK + gl.nkt - 1) / gl.nkt);
     gl.nkt = int((g.nK + gl.kt - 1) / gl.kt);
