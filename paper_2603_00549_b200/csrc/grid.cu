@@ -18,6 +18,7 @@
 //                      one coalesced 8-byte store per batch value
 //   fixup_kernel       exact-record hits (take priority over nearest)
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -1495,6 +1496,13 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
                     const LaunchOut& out, int* nb_out) {
   RowLaunch rl{};
   const int64_t nb = g.b_hi - g.b_lo;
+  if (std::getenv("PM2L_DEBUG_PLAN"))  // diagnostics
+    std::fprintf(stderr,
+                 "plan_rows: curve=%d near=%d all_gemm=%d kfast=%d nK=%lld nb=%lld align=%d CM=%d G=%d "
+                 "NW=%d cm_tab=%d\n",
+                 out.curve != nullptr, gl.near, t.all_gemm, g.kfast != nullptr, (long long)g.nK,
+                 (long long)nb, int(reinterpret_cast<uintptr_t>(out.lat) & 15), t.CM, t.G, t.NW,
+                 g.cm_tab != nullptr);
   if (out.curve || gl.near != 2 || !t.all_gemm || !g.kfast || g.nK % 2 != 0 || nb <= 0 ||
       (reinterpret_cast<uintptr_t>(out.lat) & 15) != 0 || t.CM > 254 || t.CM < 1 ||
       g.nM * g.nN > 0x7FFFFFFFll)
@@ -1518,6 +1526,8 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
   const int64_t tiles = g.nM * g.nN * rl.nbs * rl.nkc;
   if (tiles > 0x7FFFFFFFll || t.G + t.CM > 4096) return rl;
   row_layout(t, g, NB, stage_k, rl);
+  if (std::getenv("PM2L_DEBUG_PLAN"))
+    std::fprintf(stderr, "plan_rows: smem=%lld tiles=%lld\n", (long long)rl.smem, (long long)tiles);
   if (rl.smem > 200 * 1024) return rl;
   rl.tiles = int(tiles);
   rl.ctas = int(std::min<int64_t>((tiles + kRowWarps - 1) / kRowWarps, 148 * 3));

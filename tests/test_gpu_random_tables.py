@@ -203,3 +203,50 @@ def test_long_k_axis_few_rows_is_k_tiled(gpu, seed, rowblock, lattice):
     assert st[1] == nan.sum()
     if st[2] == 0:
         assert st[0] == (int(np.argmax(nan)) if nan.any() else -1)
+
+
+@pytest.mark.parametrize("seed,nk", [(31, 6000), (32, 4096), (33, 2050)])
+def test_lookup_path_long_k_chunks(gpu, seed, nk):
+    """k axes longer than one 2048-k chunk: chunk-local ranks, per-k tables
+    read from global memory (not staged), 64-byte map segments."""
+    import torch
+    from paper_2603_00549_b200 import _native
+    rng = np.random.default_rng(seed)
+    t, pm, pn, pk = random_tables(rng, 360, 30, 9, lattice=True)
+    dt = _native.DeviceTables(t, 0)
+    B = np.array([1, 2, 4, 8], np.uint64)
+    M = np.array(sorted(set(rng.choice(pm, 3).tolist()) | set(rng.integers(1, 9000, 3).tolist())), np.uint64)
+    N = np.array(sorted(set(rng.choice(pn, 3).tolist()) | set(rng.integers(1, 9000, 2).tolist())), np.uint64)
+    K = sorted(set(pk.tolist()) | set(rng.integers(1, 60000, 2 * nk).tolist()))
+    K = np.array(K[:nk // 2 * 2], np.uint64)   # even length: pair stores
+    assert len(K) > 2048 and len(K) % 2 == 0
+    plan = _native.GridPlan(dt, (B, M, N, K))
+    lat = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
+    assert plan.kernel_path(lat) == 3
+    stats = torch.tensor([-1, 0, 0], dtype=torch.int64, device="cuda")
+    plan.launch(lat, nan_stats=stats)
+    o_lat, *_ = oracle.grid(t, (B, M, N, K), use_coords=True)
+    assert np.array_equal(lat.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+    assert stats.cpu().numpy()[1] == np.isnan(o_lat).sum()
+
+
+def test_misaligned_output_falls_back_to_general_kernel(gpu):
+    """A latency buffer that is not 16-byte aligned cannot take the lookup
+    kernel's pair stores: the general kernel runs, same bits."""
+    import torch
+    from paper_2603_00549_b200 import _native
+    rng = np.random.default_rng(41)
+    t, pm, pn, pk = random_tables(rng, 120, 12, 6, lattice=True)
+    dt = _native.DeviceTables(t, 0)
+    B = np.array([1, 2, 3, 4], np.uint64)
+    M = np.array(sorted(set(rng.integers(1, 6000, 6).tolist())), np.uint64)
+    N = np.array(sorted(set(rng.integers(1, 6000, 5).tolist())), np.uint64)
+    K = np.array(sorted(set(rng.integers(1, 30000, 400).tolist()))[:300], np.uint64)
+    plan = _native.GridPlan(dt, (B, M, N, K))
+    buf = torch.empty(plan.cardinality + 1, dtype=torch.float64, device="cuda")
+    aligned, shifted = buf[:plan.cardinality], buf[1:]
+    assert plan.kernel_path(aligned) == 3 and plan.kernel_path(shifted) != 3
+    o_lat, *_ = oracle.grid(t, (B, M, N, K), use_coords=True)
+    for out in (aligned, shifted):
+        plan.launch(out)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
