@@ -616,6 +616,7 @@ struct RowLaunch {
   FastDiv d_nkc, d_nbs, d_nN;
   int seg;                   // byte-map bytes per lane (multiple of 16)
   int ring;                  // producer/consumer variant (grid_ring_kernel)
+  int pair;                  // 16-byte pair stores (even k axis, aligned output)
   int prod, slots;           // ring: builder warps, tile-state slots
   int ctas;
   int off_bar, off_gcur, off_glk, off_clm, off_cln, off_wcp, off_kf, off_ms, off_kq, off_kr, off_warp;
@@ -1029,7 +1030,7 @@ __device__ __forceinline__ void help_group_map(const RowCtx<STAGE>& c, const Gri
 // Write one tile's points from its slot: 32-pair blocks b0, b0 + bstep, ...
 // (two adjacent k per lane, one 16-byte store per batch value), then the
 // exact-record hits that fall in those blocks.
-template <int NB, bool STAGE>
+template <int NB, bool STAGE, bool PAIR>
 __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDev& t,
                                           const GridDev& g, const RowLaunch& rl, const TileXY& x,
                                           const uint8_t* wb, const double* __restrict__ base_tab,
@@ -1043,7 +1044,12 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
   const int64_t plane = c.plane;
   double* const obase = out.lat + int64_t(x.slab * NB) * plane + int64_t(x.row) * nK + k0;
   const double* const bbase = base_tab + k0;
-  const int nP = x.kc >> 1, nB = (nP + 31) >> 5;
+  // pairs of adjacent k per lane; an odd chunk's last pair has no second k.
+  // rl.pair: 16-byte pair stores (even k axis, 16-byte aligned output),
+  // else two 8-byte stores
+  const int nP = (x.kc + 1) >> 1, nB = (nP + 31) >> 5;
+  constexpr bool pair = PAIR;
+  auto has_second = [&](int p) { return PAIR || 2 * p + 1 < x.kc; };  // PAIR: kc even
   auto lookup = [&](uint32_t kf, int ikl) -> int2 {
     const uint32_t sb = rmap[kf & 0xFFFFu];
     const bool a = sb == 0xFFu;
@@ -1061,7 +1067,7 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
       const int p = min(pp[u], nP - 1);
       const uint2 kf = *reinterpret_cast<const uint2*>(c.kfs + k0 + 2 * p);
       v[u][0] = lookup(kf.x, 2 * p);
-      v[u][1] = lookup(kf.y, 2 * p + 1);
+      v[u][1] = has_second(p) ? lookup(kf.y, 2 * p + 1) : v[u][0];
     }
     bool all_ok = true;
 #pragma unroll
@@ -1072,7 +1078,7 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
       for (int u = 0; u < U; ++u) {
         const int p = min(pp[u], nP - 1);
         bv[u][0] = bbase[v[u][0].x * nK + 2 * p];
-        bv[u][1] = bbase[v[u][1].x * nK + 2 * p + 1];
+        bv[u][1] = has_second(p) ? bbase[v[u][1].x * nK + 2 * p + 1] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1091,11 +1097,20 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
           } else {
             a0 = w0[ib]; b0v = w1[ib]; a1 = b1v = 0.0;
           }
-          *reinterpret_cast<double2*>(o + ib * plane) =
-              make_double2(__dmul_rn(bv[u][0], a0), __dmul_rn(bv[u][1], b0v));
-          if (NB >= 2)
-            *reinterpret_cast<double2*>(o + (ib + 1) * plane) =
-                make_double2(__dmul_rn(bv[u][0], a1), __dmul_rn(bv[u][1], b1v));
+          const double r00 = __dmul_rn(bv[u][0], a0), r01 = __dmul_rn(bv[u][1], b0v);
+          const double r10 = __dmul_rn(bv[u][0], a1), r11 = __dmul_rn(bv[u][1], b1v);
+          if (pair) {
+            *reinterpret_cast<double2*>(o + ib * plane) = make_double2(r00, r01);
+            if (NB >= 2) *reinterpret_cast<double2*>(o + (ib + 1) * plane) = make_double2(r10, r11);
+          } else {
+            const bool has1 = has_second(p);
+            o[ib * plane] = r00;
+            if (has1) o[ib * plane + 1] = r01;
+            if (NB >= 2) {
+              o[(ib + 1) * plane] = r10;
+              if (has1) o[(ib + 1) * plane + 1] = r11;
+            }
+          }
         }
       }
     } else {
@@ -1105,19 +1120,27 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
         const int p = pp[u];
         if (p >= nP) continue;
         double* o = obase + 2 * p;
-        const bool ok0 = v[u][0].x >= 0, ok1 = v[u][1].x >= 0;
+        const bool has1 = has_second(p);
+        const bool ok0 = v[u][0].x >= 0, ok1 = !has1 || v[u][1].x >= 0;
         const double bb0 = ok0 ? bbase[v[u][0].x * nK + 2 * p] : 0.0;
-        const double bb1 = ok1 ? bbase[v[u][1].x * nK + 2 * p + 1] : 0.0;
+        const double bb1 = ok1 && has1 ? bbase[v[u][1].x * nK + 2 * p + 1] : 0.0;
         if (!(ok0 && ok1) && out.nan_stats) {
           atomicMin(out.nan_stats, (unsigned long long)(o - out.lat + (ok0 ? 1 : 0)));
           atomicAdd(out.nan_stats + 1, (unsigned long long)(NB * (2 - ok0 - ok1)));
         }
         const double* w0 = W + (ok0 ? v[u][0].y : 0) * NB;
-        const double* w1 = W + (ok1 ? v[u][1].y : 0) * NB;
+        const double* w1 = W + (ok1 && has1 ? v[u][1].y : 0) * NB;
 #pragma unroll
-        for (int ib = 0; ib < NB; ++ib)
-          *reinterpret_cast<double2*>(o + ib * plane) =
-              make_double2(ok0 ? __dmul_rn(bb0, w0[ib]) : qnan(), ok1 ? __dmul_rn(bb1, w1[ib]) : qnan());
+        for (int ib = 0; ib < NB; ++ib) {
+          const double a = ok0 ? __dmul_rn(bb0, w0[ib]) : qnan();
+          const double b = ok1 ? __dmul_rn(bb1, w1[ib]) : qnan();
+          if (pair) {
+            *reinterpret_cast<double2*>(o + ib * plane) = make_double2(a, b);
+          } else {
+            o[ib * plane] = a;
+            if (has1) o[ib * plane + 1] = b;
+          }
+        }
       }
     }
   }
@@ -1155,7 +1178,7 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
 }
 
 // Warp-autonomous variant: each warp builds and writes its own tiles.
-template <int NB, bool STAGE, int SEGW>
+template <int NB, bool STAGE, int SEGW, bool PAIR>
 __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t, GridDev g,
                                                                     RowLaunch rl,
                                                                     const double* __restrict__ base_tab,
@@ -1197,7 +1220,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t
       waited = true;
     }
     ROW_MARK(tile, 6);
-    emit_tile<NB, STAGE>(c, t, g, rl, x, wb, base_tab, out, 0, 1, lane);
+    emit_tile<NB, STAGE, PAIR>(c, t, g, rl, x, wb, base_tab, out, 0, 1, lane);
     __syncwarp();  // the warp's state buffers are rewritten by the next tile
     ROW_MARK(tile, 7);
   }
@@ -1211,7 +1234,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t
 // (kRowWarps - kRingProd)-th 32-pair block of a tile.  Writing starts after
 // one tile's build and later builds proceed under the store stream.
 
-template <int NB, bool STAGE, int SEGW>
+template <int NB, bool STAGE, int SEGW, bool PAIR>
 __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev t, GridDev g,
                                                                      RowLaunch rl,
                                                                      const double* __restrict__ base_tab,
@@ -1308,7 +1331,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       if (j == 0 && cw == 0 && lane == 0 && blockIdx.x < 4096) g_pdl_dbg[blockIdx.x * 4 + 3] = clock64();
 #endif
       if (cw == 0) ROW_MARK(tile, 3);
-      emit_tile<NB, STAGE>(c, t, g, rl, tile_xy(rl, tile, c.nK),
+      emit_tile<NB, STAGE, PAIR>(c, t, g, rl, tile_xy(rl, tile, c.nK),
                            smem + rl.off_warp + slot * rl.warp_bytes, base_tab, out, cw, NC,
                            lane);
       __syncwarp();
@@ -1503,10 +1526,10 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
                  out.curve != nullptr, gl.near, t.all_gemm, g.kfast != nullptr, (long long)g.nK,
                  (long long)nb, int(reinterpret_cast<uintptr_t>(out.lat) & 15), t.CM, t.G, t.NW,
                  g.cm_tab != nullptr);
-  if (out.curve || gl.near != 2 || !t.all_gemm || !g.kfast || g.nK % 2 != 0 || nb <= 0 ||
-      (reinterpret_cast<uintptr_t>(out.lat) & 15) != 0 || t.CM > 254 || t.CM < 1 ||
-      g.nM * g.nN > 0x7FFFFFFFll)
+  if (out.curve || gl.near != 2 || !t.all_gemm || !g.kfast || nb <= 0 || t.CM > 254 ||
+      t.CM < 1 || g.nM * g.nN > 0x7FFFFFFFll)
     return rl;
+  rl.pair = g.nK % 2 == 0 && (reinterpret_cast<uintptr_t>(out.lat) & 15) == 0;
   if (!g.cm_tab || t.NW < 1) return rl;
   int NB = 8;
   while (nb % NB) NB >>= 1;
@@ -1543,7 +1566,10 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
 template <int NB, bool STAGE, int SEGW>
 cudaError_t launch_rows_k(const TablesDev& t, const GridDev& g, const RowLaunch& rl,
                           const double* base, const LaunchOut& out, cudaStream_t s) {
-  auto* fn = rl.ring ? grid_ring_kernel<NB, STAGE, SEGW> : grid_row_kernel<NB, STAGE, SEGW>;
+  auto* fn = rl.pair ? (rl.ring ? grid_ring_kernel<NB, STAGE, SEGW, true>
+                                : grid_row_kernel<NB, STAGE, SEGW, true>)
+                     : (rl.ring ? grid_ring_kernel<NB, STAGE, SEGW, false>
+                                : grid_row_kernel<NB, STAGE, SEGW, false>);
   if (rl.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rl.smem));
     if (e != cudaSuccess) return e;

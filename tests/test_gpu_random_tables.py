@@ -230,9 +230,10 @@ def test_lookup_path_long_k_chunks(gpu, seed, nk):
     assert stats.cpu().numpy()[1] == np.isnan(o_lat).sum()
 
 
-def test_misaligned_output_falls_back_to_general_kernel(gpu):
-    """A latency buffer that is not 16-byte aligned cannot take the lookup
-    kernel's pair stores: the general kernel runs, same bits."""
+def test_misaligned_output_and_odd_k_axis(gpu):
+    """A latency buffer that is not 16-byte aligned, or an odd k axis: the
+    lookup kernel writes each pair with two 8-byte stores (and masks the
+    last pair of an odd chunk); same bits as the oracle."""
     import torch
     from paper_2603_00549_b200 import _native
     rng = np.random.default_rng(41)
@@ -241,12 +242,19 @@ def test_misaligned_output_falls_back_to_general_kernel(gpu):
     B = np.array([1, 2, 3, 4], np.uint64)
     M = np.array(sorted(set(rng.integers(1, 6000, 6).tolist())), np.uint64)
     N = np.array(sorted(set(rng.integers(1, 6000, 5).tolist())), np.uint64)
-    K = np.array(sorted(set(rng.integers(1, 30000, 400).tolist()))[:300], np.uint64)
-    plan = _native.GridPlan(dt, (B, M, N, K))
-    buf = torch.empty(plan.cardinality + 1, dtype=torch.float64, device="cuda")
-    aligned, shifted = buf[:plan.cardinality], buf[1:]
-    assert plan.kernel_path(aligned) == 3 and plan.kernel_path(shifted) != 3
-    o_lat, *_ = oracle.grid(t, (B, M, N, K), use_coords=True)
-    for out in (aligned, shifted):
-        plan.launch(out)
-        assert np.array_equal(out.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+    for nk in (300, 301, 2049):
+        K = np.array(sorted(set(rng.integers(1, 30000, 3 * nk).tolist()))[:nk], np.uint64)
+        assert len(K) == nk
+        plan = _native.GridPlan(dt, (B, M, N, K))
+        buf = torch.empty(plan.cardinality + 1, dtype=torch.float64, device="cuda")
+        aligned, shifted = buf[:plan.cardinality], buf[1:]
+        assert plan.kernel_path(aligned) == 3 and plan.kernel_path(shifted) == 3
+        o_lat, *_ = oracle.grid(t, (B, M, N, K), use_coords=True)
+        for out in (aligned, shifted):
+            stats = torch.tensor([-1, 0, 0], dtype=torch.int64, device="cuda")
+            buf.fill_(-1.0)
+            plan.launch(out, nan_stats=stats)
+            assert np.array_equal(out.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+            assert stats.cpu().numpy()[1] == np.isnan(o_lat).sum()
+        # nothing written outside the slice
+        assert buf[-1].item() == -1.0 or buf[0].item() == -1.0
