@@ -617,6 +617,7 @@ struct RowLaunch {
   int seg;                   // byte-map bytes per lane (multiple of 16)
   int ring;                  // producer/consumer variant (grid_ring_kernel)
   int pair;                  // 16-byte pair stores (even k axis, aligned output)
+  int rowblock;              // row-block tables: per-point wave scale (ring kernel, pairs)
   int prod, slots;           // ring: builder warps, tile-state slots
   int ctas;
   int off_bar, off_gcur, off_glk, off_clm, off_cln, off_wcp, off_kf, off_ms, off_kq, off_kr, off_warp;
@@ -686,7 +687,7 @@ struct RowIn {
   uint64_t cm[2], cn[2];  // tile counts of wave classes lane, lane + 32
 };
 
-template <int NB>
+template <int NB, bool RB = false>
 __device__ __forceinline__ RowIn<NB> load_row_in(const GridDev& g, const RowLaunch& rl, int tile,
                                                  int NW, int lane) {
   RowIn<NB> r;
@@ -701,8 +702,8 @@ __device__ __forceinline__ RowIn<NB> load_row_in(const GridDev& g, const RowLaun
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int wc = min(lane + 32 * h, NW - 1);
-    r.cm[h] = g.cm_tab[im * NW + wc];
-    r.cn[h] = g.cn_tab[jn * NW + wc];
+    r.cm[h] = RB ? 0 : g.cm_tab[im * NW + wc];   // row-block waves ignore (m, n)
+    r.cn[h] = RB ? 0 : g.cn_tab[jn * NW + wc];
   }
   return r;
 }
@@ -800,7 +801,7 @@ __device__ __forceinline__ void build_w_table(const RowCtx<STAGE>& c, const Grid
 // One tile's lookup state (one warp): staircase, wave-scale table, cut
 // points, byte maps, written into the slot `wb`; len / lastpos into its
 // header.
-template <int NB, bool STAGE, int SEGW>
+template <int NB, bool STAGE, int SEGW, bool RB = false>
 __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev& g,
                                            const RowLaunch& rl, const TileXY& x,
                                            const RowIn<NB>& cur, uint8_t* wb, int lane,
@@ -877,7 +878,12 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
     mbar_arrive(stair_ready);
   }
   // ---- wave-scale table W[wave class][ib] of this (m, n) and batch slab
-  if (with_w) build_w_table<NB, STAGE>(c, g, cur, W, lane);
+  if (with_w && !RB) build_w_table<NB, STAGE>(c, g, cur, W, lane);
+  if (RB) {  // row-block waves depend on (b, k): the writers need the slab's batch values
+#pragma unroll
+    for (int ib = 0; ib < NB; ++ib)
+      if (lane == ib) W[ib] = __longlong_as_double(static_cast<long long>(cur.b[ib]));
+  }
   __syncwarp();
   ROW_MARK(mark_tile, 6);
   // ---- cut points: fixed-trip branch-free binary searches, one shared
@@ -1027,10 +1033,19 @@ __device__ __forceinline__ void help_group_map(const RowCtx<STAGE>& c, const Gri
     *reinterpret_cast<ulonglong2*>(mw + q) = make_ulonglong2(w[q], w[q + 1]);
 }
 
+// Row-block wave scale (compute.py:78-106, _kernels.pyx:123-132):
+// blocks = ceil(b*k / tile_m), waves = ceil(blocks / blocks_per_wave),
+// scale = waves / ref_waves -- from the wave class's staged parameters.
+__device__ __forceinline__ double rb_scale(const WcParam& p, uint64_t b, uint64_t k) {
+  const uint64_t blocks = ceil_div_w(p, 0, b * k, p.tm);
+  const double w = __ull2double_rn(ceil_div_w(p, 2, blocks, p.bpw));
+  return p.rw == 1.0 ? w : __ddiv_rn(w, p.rw);
+}
+
 // Write one tile's points from its slot: 32-pair blocks b0, b0 + bstep, ...
 // (two adjacent k per lane, one 16-byte store per batch value), then the
 // exact-record hits that fall in those blocks.
-template <int NB, bool STAGE, bool PAIR>
+template <int NB, bool STAGE, bool PAIR, bool RB = false>
 __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDev& t,
                                           const GridDev& g, const RowLaunch& rl, const TileXY& x,
                                           const uint8_t* wb, const double* __restrict__ base_tab,
@@ -1072,7 +1087,41 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
     bool all_ok = true;
 #pragma unroll
     for (int u = 0; u < U; ++u) all_ok = all_ok && v[u][0].x >= 0 && v[u][1].x >= 0;
-    if (__all_sync(0xFFFFFFFFu, all_ok)) {
+    if (RB) {
+      // row-block families: per point scale from (b, k) and the wave class
+      uint64_t bvals[NB];
+#pragma unroll
+      for (int ib = 0; ib < NB; ++ib)
+        bvals[ib] = static_cast<uint64_t>(__double_as_longlong(W[ib]));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = pp[u];
+        if (p >= nP) continue;
+        double* o = obase + 2 * p;
+        const bool has1 = has_second(p);
+        const bool ok0 = v[u][0].x >= 0, ok1 = !has1 || v[u][1].x >= 0;
+        const double bb0 = ok0 ? bbase[v[u][0].x * nK + 2 * p] : 0.0;
+        const double bb1 = ok1 && has1 ? bbase[v[u][1].x * nK + 2 * p + 1] : 0.0;
+        if (!(ok0 && ok1) && out.nan_stats) {
+          atomicMin(out.nan_stats, (unsigned long long)(o - out.lat + (ok0 ? 1 : 0)));
+          atomicAdd(out.nan_stats + 1, (unsigned long long)(NB * (2 - ok0 - ok1)));
+        }
+        const uint64_t ka = g.K[k0 + 2 * p], kb = has1 ? g.K[k0 + 2 * p + 1] : ka;
+        const WcParam q0 = c.wcp[ok0 ? v[u][0].y : 0];
+        const WcParam q1 = c.wcp[ok1 && has1 ? v[u][1].y : 0];
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib) {
+          const double a = ok0 ? __dmul_rn(bb0, rb_scale(q0, bvals[ib], ka)) : qnan();
+          const double b = ok1 ? __dmul_rn(bb1, rb_scale(q1, bvals[ib], kb)) : qnan();
+          if (PAIR) {
+            *reinterpret_cast<double2*>(o + ib * plane) = make_double2(a, b);
+          } else {
+            o[ib * plane] = a;
+            if (has1) o[ib * plane + 1] = b;
+          }
+        }
+      }
+    } else if (__all_sync(0xFFFFFFFFu, all_ok)) {
       double bv[U][2];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1234,7 +1283,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_row_kernel(TablesDev t
 // (kRowWarps - kRingProd)-th 32-pair block of a tile.  Writing starts after
 // one tile's build and later builds proceed under the store stream.
 
-template <int NB, bool STAGE, int SEGW, bool PAIR>
+template <int NB, bool STAGE, int SEGW, bool PAIR, bool RB>
 __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev t, GridDev g,
                                                                      RowLaunch rl,
                                                                      const double* __restrict__ base_tab,
@@ -1272,7 +1321,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
   if (warp < P) {
     int j = warp;
     int tile = blockIdx.x + j * gridDim.x;
-    RowIn<NB> rin = load_row_in<NB>(g, rl, min(tile, rl.tiles - 1), t.NW, lane);
+    RowIn<NB> rin = load_row_in<NB, RB>(g, rl, min(tile, rl.tiles - 1), t.NW, lane);
     mbar_wait(bar, 0);
     if (STAGE) mbar_wait(bar + 1, 0);
     for (; tile < rl.tiles; j += P, tile += P * gridDim.x) {
@@ -1280,14 +1329,14 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       const RowIn<NB> cur = rin;
       {
         const int nt = tile + P * gridDim.x;
-        if (nt < rl.tiles) rin = load_row_in<NB>(g, rl, nt, t.NW, lane);
+        if (nt < rl.tiles) rin = load_row_in<NB, RB>(g, rl, nt, t.NW, lane);
       }
       if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
 #ifdef PM2L_TIMING
       if (lane == 0 && tile < 16384) g_row_dbg[tile * 8] = t_entry;
 #endif
       ROW_MARK(tile, 1);
-      build_tile<NB, STAGE, SEGW>(c, g, rl, tile_xy(rl, tile, c.nK), cur,
+      build_tile<NB, STAGE, SEGW, RB>(c, g, rl, tile_xy(rl, tile, c.nK), cur,
                                   smem + rl.off_warp + slot * rl.warp_bytes, lane, tile,
                                   /*with_w=*/j >= nhelp, j < nhelp ? sready + j : nullptr);
       __syncwarp();
@@ -1301,9 +1350,9 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       const int tile0 = blockIdx.x + cw * gridDim.x;
       if (tile0 < rl.tiles) {
         uint8_t* wb0 = smem + rl.off_warp + cw * rl.warp_bytes;
-        const RowIn<NB> r0 = load_row_in<NB>(g, rl, tile0, t.NW, lane);
+        const RowIn<NB> r0 = load_row_in<NB, RB>(g, rl, tile0, t.NW, lane);
         mbar_wait(bar, 0);
-        build_w_table<NB, STAGE>(c, g, r0, reinterpret_cast<double*>(wb0 + rl.w_W), lane);
+        if (!RB) build_w_table<NB, STAGE>(c, g, r0, reinterpret_cast<double*>(wb0 + rl.w_W), lane);
         if (STAGE) mbar_wait(bar + 1, 0);
         mbar_wait(sready + cw, 0);  // the builder's staircase is published
         help_group_map<STAGE, SEGW>(c, g, rl, tile_xy(rl, tile0, c.nK), wb0, lane);
@@ -1331,7 +1380,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       if (j == 0 && cw == 0 && lane == 0 && blockIdx.x < 4096) g_pdl_dbg[blockIdx.x * 4 + 3] = clock64();
 #endif
       if (cw == 0) ROW_MARK(tile, 3);
-      emit_tile<NB, STAGE, PAIR>(c, t, g, rl, tile_xy(rl, tile, c.nK),
+      emit_tile<NB, STAGE, PAIR, RB>(c, t, g, rl, tile_xy(rl, tile, c.nK),
                            smem + rl.off_warp + slot * rl.warp_bytes, base_tab, out, cw, NC,
                            lane);
       __syncwarp();
@@ -1526,11 +1575,13 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
                  out.curve != nullptr, gl.near, t.all_gemm, g.kfast != nullptr, (long long)g.nK,
                  (long long)nb, int(reinterpret_cast<uintptr_t>(out.lat) & 15), t.CM, t.G, t.NW,
                  g.cm_tab != nullptr);
-  if (out.curve || gl.near != 2 || !t.all_gemm || !g.kfast || nb <= 0 || t.CM > 254 ||
-      t.CM < 1 || g.nM * g.nN > 0x7FFFFFFFll)
+  if (out.curve || gl.near != 2 || !(t.all_gemm || t.all_rowblock) || !g.kfast || nb <= 0 ||
+      t.CM > 254 || t.CM < 1 || g.nM * g.nN > 0x7FFFFFFFll)
     return rl;
   rl.pair = g.nK % 2 == 0 && (reinterpret_cast<uintptr_t>(out.lat) & 15) == 0;
-  if (!g.cm_tab || t.NW < 1) return rl;
+  rl.rowblock = t.all_rowblock;
+  if (rl.rowblock && !rl.pair) return rl;  // row-block variant: pair stores only
+  if ((t.all_gemm && !g.cm_tab) || t.NW < 1) return rl;
   int NB = 8;
   while (nb % NB) NB >>= 1;
   rl.nbs = int(nb / NB);
@@ -1554,6 +1605,7 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
   if (rl.smem > 200 * 1024) return rl;
   rl.tiles = int(tiles);
   rl.ctas = int(std::min<int64_t>((tiles + kRowWarps - 1) / kRowWarps, 148 * 3));
+  if (rl.rowblock && !rl.ring) return RowLaunch{};  // row-block: ring kernel only
   if (rl.ring) rl.ctas = int(std::min<int64_t>(tiles, 148 * 3));
   if (const char* e = std::getenv("PM2L_ROW_CTAS")) {  // tuning experiments only
     const int v = std::atoi(e);
@@ -1566,10 +1618,11 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
 template <int NB, bool STAGE, int SEGW>
 cudaError_t launch_rows_k(const TablesDev& t, const GridDev& g, const RowLaunch& rl,
                           const double* base, const LaunchOut& out, cudaStream_t s) {
-  auto* fn = rl.pair ? (rl.ring ? grid_ring_kernel<NB, STAGE, SEGW, true>
-                                : grid_row_kernel<NB, STAGE, SEGW, true>)
-                     : (rl.ring ? grid_ring_kernel<NB, STAGE, SEGW, false>
-                                : grid_row_kernel<NB, STAGE, SEGW, false>);
+  auto* fn = rl.rowblock ? grid_ring_kernel<NB, STAGE, SEGW, true, true>
+             : rl.pair ? (rl.ring ? grid_ring_kernel<NB, STAGE, SEGW, true, false>
+                                  : grid_row_kernel<NB, STAGE, SEGW, true>)
+                       : (rl.ring ? grid_ring_kernel<NB, STAGE, SEGW, false, false>
+                                  : grid_row_kernel<NB, STAGE, SEGW, false>);
   if (rl.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rl.smem));
     if (e != cudaSuccess) return e;

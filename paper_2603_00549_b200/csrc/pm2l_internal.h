@@ -34,6 +34,7 @@ struct TablesDev {
   int32_t G = 0;        // k-groups
   int32_t n_exact = 0;  // exact records (== R)
   int32_t all_gemm = 1; // no row-block curve referenced
+  int32_t all_rowblock = 0;  // >= 1 curve referenced, all of them row-block
   int32_t lowest_wins = 0;  // equal logs imply equal coordinates (all < 2^44)
   int32_t n_samples = 0;
   // per curve [C]

@@ -83,7 +83,7 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   for (int64_t i = 0; i < R; ++i)
     if (!check_curve(v->cand_curve[i]) || !check_curve(v->exact_curve[i]))
       return "curve index out of range";
-  int32_t all_gemm = 1;
+  int32_t all_gemm = 1, n_ref = 0, n_rowblock = 0;
   for (int64_t c = 0; c < C; ++c) {
     if (!referenced[c]) continue;
     if (v->sample_offsets[c + 1] - v->sample_offsets[c] < 1)
@@ -93,6 +93,8 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
       return "tile_n and split_k must be >= 1";
     if (!(v->ref_dim[c] > 0) || !(v->ref_waves[c] > 0)) return "ref_dim/ref_waves must be > 0";
     if (v->family_rowblock[c]) all_gemm = 0;
+    ++n_ref;
+    n_rowblock += v->family_rowblock[c] ? 1 : 0;
   }
   for (int64_t i = 0; i < R; ++i)
     if (!std::isfinite(v->log_m[i]) || !std::isfinite(v->log_n[i]) || !std::isfinite(v->log_k[i]))
@@ -231,6 +233,7 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t = TablesDev{};
   t.R = int32_t(R); t.C = int32_t(C); t.G = int32_t(grp_lk.size());
   t.n_exact = int32_t(R); t.all_gemm = all_gemm; t.n_samples = int32_t(S);
+  t.all_rowblock = n_ref > 0 && n_rowblock == n_ref ? 1 : 0;
   {
     // log2 is injective on integers below 2^44 at double precision, so equal
     // candidate logs there imply equal coordinates (grid.cu one-class path)

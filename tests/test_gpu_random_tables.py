@@ -258,3 +258,32 @@ def test_misaligned_output_and_odd_k_axis(gpu):
             assert stats.cpu().numpy()[1] == np.isnan(o_lat).sum()
         # nothing written outside the slice
         assert buf[-1].item() == -1.0 or buf[0].item() == -1.0
+
+
+@pytest.mark.parametrize("seed,nk,nb", [(51, 1000, 4), (52, 4096, 8), (53, 2400, 2)])
+def test_lookup_path_row_block_tables(gpu, seed, nk, nb):
+    """Row-block (attention / triton_vec) one-class tables take the lookup
+    kernel with the per-point (b, k) wave model; bit-exact, NaN stats."""
+    import torch
+    from paper_2603_00549_b200 import _native
+    rng = np.random.default_rng(seed)
+    t, pm, pn, pk = random_tables(rng, 80, 6, 8, rowblock=True, lattice=True)
+    dt = _native.DeviceTables(t, 0)
+    B = np.array(sorted(set(rng.integers(1, 9000, 4 * nb).tolist()))[:nb], np.uint64)
+    M = np.array([1], np.uint64)
+    N = np.array([1], np.uint64)
+    K = sorted(set(pk.tolist()) | set(rng.integers(1, 65000, 2 * nk).tolist()))
+    K = np.array(K[:nk], np.uint64)
+    assert len(K) == nk and nk % 2 == 0
+    plan = _native.GridPlan(dt, (B, M, N, K))
+    lat = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
+    assert plan.kernel_path(lat) == 3
+    stats = torch.tensor([-1, 0, 0], dtype=torch.int64, device="cuda")
+    plan.launch(lat, nan_stats=stats)
+    o_lat, *_ = oracle.grid(t, (B, M, N, K), use_coords=True)
+    assert np.array_equal(lat.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+    nan = np.isnan(o_lat)
+    st = stats.cpu().numpy()
+    assert st[1] == nan.sum()
+    if st[2] == 0:
+        assert st[0] == (int(np.argmax(nan)) if nan.any() else -1)
