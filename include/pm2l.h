@@ -241,7 +241,9 @@ int pm2l_store_lookup(const uint8_t* records, int64_t n_records, const uint64_t*
  * synchronous, thread-safe (concurrent calls on disjoint slices, as
  * backend.py:78-87 issues them).  Runs on the current CUDA device; tables
  * are staged per call (cached by content).  Array lengths are the extra
- * n_* arguments the memoryviews carried implicitly. */
+ * n_* arguments the memoryviews carried implicitly.  A page-locked `out`
+ * (cudaHostAlloc / cudaHostRegister) is written by one direct device-to-host
+ * copy; a pageable one through a pinned staging ring. */
 int pm2l_predict_grid_slice(
     const uint64_t* batch_vals, int64_t n_batch,
     const uint64_t* m_vals, int64_t n_m,

@@ -602,6 +602,15 @@ SliceCache g_slice;
 // Device result -> pageable caller buffer: chunked D2H into a ring of pinned
 // buffers on `s`, each chunk copied out by the host pool while the next
 // chunks are in flight over PCIe.
+bool host_page_locked(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 int drain_to_host(SliceDevice& sd, const double* d_out, double* out, size_t bytes) {
   if (!g_slice.pool) {
     // about half the host threads: the copy-out saturates host memory
@@ -715,7 +724,14 @@ int pm2l_predict_grid_slice(
   if (int rc = pm2l_grid_predict(t, batch_vals, n_batch, m_vals, n_m, n_vals, n_n, k_vals, n_k,
                                  b_lo, b_hi, d_out, nullptr, nullptr, nullptr, s))
     return rc;
-  if (int rc = drain_to_host(sd, d_out, out, size_t(count) * sizeof(double))) return rc;
+  // a page-locked caller buffer (cudaHostAlloc / cudaHostRegister, e.g. a
+  // pinned torch tensor's numpy view) takes the result straight from the
+  // copy engine; pageable buffers go through the staged drain
+  if (host_page_locked(out)) {
+    PM2L_CUDA(cudaMemcpyAsync(out, d_out, size_t(count) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  } else if (int rc = drain_to_host(sd, d_out, out, size_t(count) * sizeof(double))) {
+    return rc;
+  }
   PM2L_CUDA(cudaStreamSynchronize(s));
   return PM2L_OK;
 }

@@ -10,6 +10,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 import oracle
 from conftest import GOLDEN, dataset, golden_grid_arrays, golden_meta, golden_npz, prepared
@@ -74,8 +75,11 @@ def test_reference_ffi_dropin_slice(gpu):
         t["log_k"] = np.log2(np.array([r.shape.k for r in recs], np.float64))
         B, M, N, K = prep.axis_arrays()
         nb = len(B)
-        for lo, hi in ((0, nb), (nb - 1, nb)):
-            out = np.empty((hi - lo) * len(M) * len(N) * len(K), np.float64)
+        for lo, hi, pin in ((0, nb, False), (nb - 1, nb, False), (0, nb, True)):
+            n_out = (hi - lo) * len(M) * len(N) * len(K)
+            # pageable output: staged drain; page-locked: one direct D2H copy
+            out = (torch.full((n_out,), -1.0, dtype=torch.float64, pin_memory=True).numpy()
+                   if pin else np.empty(n_out, np.float64))
             P = lambda a: a.ctypes.data  # noqa: E731
             rc = lib.pm2l_predict_grid_slice(
                 P(B), nb, P(M), len(M), P(N), len(N), P(K), len(K), lo, hi,
