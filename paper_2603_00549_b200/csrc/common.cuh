@@ -42,6 +42,12 @@ __device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) {
   return num / b;
 }
 
+// The rare u64 division slow path kept out of line: the fully unrolled
+// emission loops reach it, and inlining one u64 division per call site grows
+// the lookup kernel past the instruction cache (C3 profile: "no instruction"
+// stalls dominated at 130 KB of code).  Same integer result.
+static __device__ __noinline__ uint64_t udiv_slow(uint64_t a, uint64_t b) { return a / b; }
+
 // ceil((a) / d) for the curve's divisor j (0 tile_m, 1 tile_n, 2 blocks per
 // wave) through the host-computed u32 magic when a + d - 1 fits in 32 bits;
 // identical integer result to ceil_div.
@@ -54,7 +60,7 @@ __device__ __forceinline__ uint64_t ceil_div_c(const TablesDev& t, int c, int j,
     const uint32_t q = __umulhi(t.dv_m[3 * c + j], n32);
     return uint64_t((q + ((n32 - q) >> (s & 0xFF))) >> ((s >> 8) & 0xFF));
   }
-  return num / d;
+  return udiv_slow(num, d);
 }
 
 // compute._interpolate_detail / _kernels._interp over samples [lo, hi):
@@ -117,7 +123,7 @@ __device__ __forceinline__ uint64_t ceil_div_p(const WcParam& p, int j, uint64_t
     const uint32_t q = __umulhi(p.dm[j], n32);
     return uint64_t((q + ((n32 - q) >> (s & 0xFF))) >> ((s >> 8) & 0xFF));
   }
-  return num / d;
+  return udiv_slow(num, d);
 }
 
 __device__ __forceinline__ WcParam curve_params(const TablesDev& t, int c) {

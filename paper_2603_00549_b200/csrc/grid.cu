@@ -675,7 +675,7 @@ __device__ __forceinline__ uint64_t ceil_div_w(const WcParam& p, int j, uint64_t
     const uint32_t q = __umulhi(p.dm[j], n32);
     return uint64_t((q + ((n32 - q) >> (s & 0xFF))) >> ((s >> 8) & 0xFF));
   }
-  return num / d;
+  return udiv_slow(num, d);
 }
 
 // Row scalars of one tile (loaded one tile ahead).
@@ -1584,9 +1584,17 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
   if ((t.all_gemm && !g.cm_tab) || t.NW < 1) return rl;
   int NB = 8;
   while (nb % NB) NB >>= 1;
-  rl.nbs = int(nb / NB);
   rl.kc = int(std::min<int64_t>(g.nK, kKChunk));
   rl.nkc = int((g.nK + rl.kc - 1) / rl.kc);
+  // few (m, n) rows (attention grids: one row, long k): narrower batch slabs
+  // until every CTA slot has about two tiles, since a tile's emission is
+  // latency-bound on its 4 writer warps
+  while (NB > 1 && g.nM * g.nN * (nb / NB) * rl.nkc < 2 * 148 * 3) NB >>= 1;
+  if (const char* e = std::getenv("PM2L_ROW_NB")) {  // experiments
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= 8 && (v & (v - 1)) == 0 && nb % v == 0) NB = v;
+  }
+  rl.nbs = int(nb / NB);
   rl.d_nkc = fast_div_for(uint32_t(rl.nkc));
   rl.d_nbs = fast_div_for(uint32_t(rl.nbs));
   rl.d_nN = fast_div_for(uint32_t(g.nN));

@@ -1,3 +1,9 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python bench.py --steps 20 --warmup 5 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value']/1e9, d['ms_per_step']*1e3, json.dumps(d['e2e']))"
-PM2L_E2E_TRACE=1 python bench.py --steps 4 --warmup 3 2>&1 | grep "pm2l drain" | tail -3
+python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+for i in 1 2; do
+for v in prev cur; do
+ if [ $v = prev ]; then export PM2L_LIB_PATH=$PWD/paper_2603_00549_b200/libpm2l_prev.so; else unset PM2L_LIB_PATH; fi
+ echo "$v $(python tools/bench_modes.py 2>&1 | grep 'C3 cut' | cut -c60-120)"
+ python tools/c5.py 2>&1 | grep "cutlass_att\|C5 rank" | cut -c1-130
+done; done
+unset PM2L_LIB_PATH
+python bench.py --steps 50 --warmup 5 2>&1 | tail -1 | cut -c1-250

@@ -37,8 +37,18 @@ def main():
     fn = lib.pm2l_debug_row_timing
     fn.restype = C.c_int
     fn.argtypes = [C.c_void_p, C.c_int]
-    ds = bench.load_bf16()
-    prep = PreparedGrid(ds, bench.grid_for(1), WaveModel(ds.device.sm_count))
+    if os.environ.get("ROW_TIMING_GRID") == "c3":  # attention grid of tools/profile_c3.py
+        from paper_2603_00549_b200 import load_dataset
+        from paper_2603_00549_b200.core import DType, TransposeMode
+        from paper_2603_00549_b200.nascache import GridSpec
+        ds = load_dataset(os.path.join(ROOT, "tests", "golden", "datasets", "generic_bf16.json"))
+        bh = sorted({b * h for b in (1, 2, 4, 8, 16, 32, 64, 128) for h in (8, 12, 16, 20, 32, 40, 64)})
+        grid = GridSpec("cutlass_attention", DType.BF16, TransposeMode.NN,
+                        {"batch": tuple(bh), "m": (1,), "n": (1,), "k": tuple(range(64, 65536))})
+    else:
+        ds = bench.load_bf16()
+        grid = bench.grid_for(1)
+    prep = PreparedGrid(ds, grid, WaveModel(ds.device.sm_count))
     plan = _native.GridPlan(prep.device_tables(0), prep.axis_arrays())
     out = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -54,7 +64,7 @@ def main():
     n = 16384 * 8
     buf = np.zeros(n, np.uint64)
     assert fn(buf.ctypes.data, n) == 0
-    tiles = 2500
+    tiles = int(os.environ.get("ROW_TILES", "2500"))
     t = buf[:tiles * 8].reshape(tiles, 8).astype(np.int64)
     # entry stamp is per (cta, warp) == tile index for a one-tile-per-warp launch
     # SM clock64 stamps: per-tile differences only (clocks differ across SMs)
