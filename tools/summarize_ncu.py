@@ -2,9 +2,11 @@
 """Summaries of ncu output for profiles/ (run here, on the pulled files).
 
     python tools/summarize_ncu.py full  gpurun_out/prof.ncu-rep  profiles/ncu_grid_kernel.json "<capture cmd>"
+      (ALGO_BYTES=<bytes per launch>, default the C2 grid's 80 MB of f64 output)
     python tools/summarize_ncu.py launches gpurun_out/launches.csv profiles/launches_round1.csv
 """
 import csv
+import os
 import io
 import json
 import subprocess
@@ -55,7 +57,7 @@ def full(rep, out, capture):
         "dram_bytes_read": rd,
         "dram_bytes_write": wr,
         "dram_bytes_per_launch": rd + wr,
-        "algorithmic_bytes_per_launch": 80000000,
+        "algorithmic_bytes_per_launch": int(os.environ.get("ALGO_BYTES", 80000000)),
         "warp_instructions": num(d["smsp__inst_executed.sum"]),
         "issue_active_pct": num(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
         "warps_active_pct": num(d["sm__warps_active.avg.pct_of_peak_sustained_active"]),
