@@ -1037,8 +1037,19 @@ __device__ __forceinline__ void help_group_map(const RowCtx<STAGE>& c, const Gri
 // blocks = ceil(b*k / tile_m), waves = ceil(blocks / blocks_per_wave),
 // scale = waves / ref_waves -- from the wave class's staged parameters.
 __device__ __forceinline__ double rb_scale(const WcParam& p, uint64_t b, uint64_t k) {
-  const uint64_t blocks = ceil_div_w(p, 0, b * k, p.tm);
-  const double w = __ull2double_rn(ceil_div_w(p, 2, blocks, p.bpw));
+  // slot 1 of a row-block class = tile_m * blocks_per_wave (tables.cpp):
+  // ceil(ceil(x / tm) / bpw) == ceil(x / (tm * bpw)) for integers, so one
+  // magic division when x + tm*bpw - 1 fits 32 bits; else the two steps
+  const uint64_t x = b * k, num = x + p.tn - 1;
+  uint64_t waves;
+  if ((p.ds[1] >> 16) && num <= 0xFFFFFFFFull) {
+    const uint32_t n32 = uint32_t(num), s = p.ds[1];
+    const uint32_t q = __umulhi(p.dm[1], n32);
+    waves = (q + ((n32 - q) >> (s & 0xFF))) >> ((s >> 8) & 0xFF);
+  } else {
+    waves = ceil_div_w(p, 2, ceil_div_w(p, 0, x, p.tm), p.bpw);
+  }
+  const double w = __ull2double_rn(waves);
   return p.rw == 1.0 ? w : __ddiv_rn(w, p.rw);
 }
 

@@ -222,6 +222,21 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
     q.tm = v->tile_m[c]; q.tn = v->tile_n[c]; q.sk = v->split_k[c]; q.bpw = v->blocks_per_wave[c];
     q.rw = v->ref_waves[c];
     for (int j = 0; j < 3; ++j) { q.dm[j] = dv_m[3 * c + j]; q.ds[j] = dv_s[3 * c + j]; }
+    if (v->family_rowblock[c]) {
+      // row-block classes never divide by tile_n: slot 1 carries
+      // tile_m * blocks_per_wave instead, so the lookup kernel computes
+      // waves = ceil(ceil(b*k / tm) / bpw) = ceil(b*k / (tm * bpw)) with one
+      // magic division (grid.cu rb_scale); ds[1] = 0 when it does not fit
+      q.tn = 0; q.dm[1] = 0; q.ds[1] = 0;
+      const uint64_t d = q.tm * q.bpw;
+      if (q.tm <= 0xFFFFFFFFull && q.bpw <= 0xFFFFFFFFull && d <= 0xFFFFFFFFull) {
+        int l = 0;
+        while ((uint64_t(1) << l) < d) ++l;
+        q.tn = d;
+        q.dm[1] = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1);
+        q.ds[1] = uint32_t(l < 1 ? l : 1) | (uint32_t(l > 1 ? l - 1 : 0) << 8) | (1u << 16);
+      }
+    }
   }
   std::vector<int32_t> s_off(C + 1);
   for (int64_t c = 0; c <= C; ++c) s_off[c] = int32_t(v->sample_offsets[c]);

@@ -260,16 +260,19 @@ def test_misaligned_output_and_odd_k_axis(gpu):
         assert buf[-1].item() == -1.0 or buf[0].item() == -1.0
 
 
-@pytest.mark.parametrize("seed,nk,nb", [(51, 1000, 4), (52, 4096, 8), (53, 2400, 2)])
-def test_lookup_path_row_block_tables(gpu, seed, nk, nb):
+@pytest.mark.parametrize("seed,nk,nb,b_max", [(51, 1000, 4, 9000), (52, 4096, 8, 9000),
+                                              (53, 2400, 2, 9000), (54, 1000, 4, 3_000_000)])
+def test_lookup_path_row_block_tables(gpu, seed, nk, nb, b_max):
     """Row-block (attention / triton_vec) one-class tables take the lookup
-    kernel with the per-point (b, k) wave model; bit-exact, NaN stats."""
+    kernel with the per-point (b, k) wave model; bit-exact, NaN stats.
+    b_max = 3e6 puts b*k past 32 bits: the two-step u64 wave count instead
+    of the single tile_m * blocks_per_wave magic division."""
     import torch
     from paper_2603_00549_b200 import _native
     rng = np.random.default_rng(seed)
     t, pm, pn, pk = random_tables(rng, 80, 6, 8, rowblock=True, lattice=True)
     dt = _native.DeviceTables(t, 0)
-    B = np.array(sorted(set(rng.integers(1, 9000, 4 * nb).tolist()))[:nb], np.uint64)
+    B = np.array(sorted(set(rng.integers(1, b_max, 4 * nb).tolist()))[:nb], np.uint64)
     M = np.array([1], np.uint64)
     N = np.array([1], np.uint64)
     K = sorted(set(pk.tolist()) | set(rng.integers(1, 65000, 2 * nk).tolist()))
