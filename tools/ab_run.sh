@@ -1,5 +1,6 @@
 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-python bench.py 2>&1 | tail -1 > gpurun_out/bench_final.json
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 > /dev/null 2>&1
-ls -la gpurun_out/launches.csv
+b() { python bench.py --steps 50 --warmup 5 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value']/1e9, d['ms_per_step']*1e3, d['roofline']['kernel_ms']*1e3)"; }
+for i in 1 2 3; do
+PM2L_LIB_PATH=$PWD/paper_2603_00549_b200/libpm2l_prev.so b prev
+b cur
+done
