@@ -474,9 +474,19 @@ int pm2l_store_lookup(const uint8_t* records, int64_t n_records, const uint64_t*
 // ------------------------------------------------------------------ drop-in
 namespace {
 
+// FNV-1a style content hash over 8-byte words (one dependent multiply per
+// word instead of per byte: the tables are hashed on every call), then the
+// tail bytes
 uint64_t fnv(uint64_t h, const void* p, size_t n) {
   const uint8_t* b = static_cast<const uint8_t*>(p);
-  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    uint64_t w;
+    std::memcpy(&w, b + i, 8);
+    h = (h ^ w) * 0x100000001b3ull;
+    h ^= h >> 29;
+  }
+  for (; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
   return h;
 }
 
