@@ -205,8 +205,10 @@ int pm2l_membound_predict(const double* features, const int32_t* model_ids, int6
 /* --------------------------------------------------- per-model totals ---
  * Correctly rounded sum (== math.fsum) of values[offsets[s] .. offsets[s+1])
  * for each of n_segments segments (DEVICE arrays; offsets has n_segments+1
- * entries).  Values must be finite and >= 0 (latencies); NaN in a segment
- * gives a NaN total.  Exact warp-segmented fixed-point reduction. */
+ * entries).  Values of either sign (a raw membound layer under a
+ * non-positive floor is negative); NaN, or both infinities, in a segment give
+ * a NaN total (math.fsum raises there), one infinity gives that infinity.
+ * Exact warp-segmented two's-complement fixed-point reduction. */
 int pm2l_segment_fsum(const double* values, const int64_t* offsets, int64_t n_segments,
                       double* out_totals, void* stream);
 

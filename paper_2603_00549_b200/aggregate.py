@@ -316,5 +316,13 @@ def predict_model_grid(template: Sequence[TemplateLayer], shapes, features, data
         i, l = np.argwhere(bad)[0]
         raise UnresolvedLayer(f"model {int(i)} layer {template[l].layer_id!r}: no usable kernel "
                               f"configuration")
+    # every layer is a Prediction in the reference, whose latency must be
+    # finite and > 0 (core.py:383-386): a raw membound layer under a
+    # non-positive floor fails there, so it fails here
+    bad = ~(np.isfinite(lat) & (lat > 0))
+    if bad.any():
+        i, l = np.argwhere(bad)[0]
+        raise ValidationError(f"model {int(i)} layer {template[l].layer_id!r}: latency_us must "
+                              f"be finite and > 0, got {float(lat[i, l])!r}")
     totals = segment_fsum(lat.ravel(), np.arange(0, n * L + 1, L, dtype=np.int64))
     return lat, totals

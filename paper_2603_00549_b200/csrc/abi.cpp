@@ -118,6 +118,22 @@ int get_lut(int device, double** out) {
 
 }  // namespace
 
+namespace pm2l {
+int sm_count() {
+  static std::mutex mu;
+  static std::unordered_map<int, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+  cache[dev] = n;
+  return n;
+}
+}  // namespace pm2l
+
 struct pm2l_tables {
   int device = 0;
   TablesHost host;
@@ -601,9 +617,20 @@ struct SliceDevice {
   cudaStream_t stream = nullptr;
 };
 
+// Staged tables of the drop-in, keyed by a content hash and verified against
+// the full table bytes on every hit (a hash collision never serves another
+// dataset's tables); least recently used entries beyond kSliceCacheMax are
+// destroyed, so a sweep over many triples keeps bounded HBM.
+constexpr size_t kSliceCacheMax = 16;
+struct SliceEntry {
+  std::string bytes;  // the table arrays, concatenated as hashed
+  pm2l_tables* tables = nullptr;
+  uint64_t last_use = 0;
+};
 struct SliceCache {
   std::mutex mu;
-  std::unordered_map<uint64_t, pm2l_tables*> tables;  // (content hash ^ device) -> staged
+  std::unordered_multimap<uint64_t, SliceEntry> tables;  // (content hash ^ device) -> staged
+  uint64_t clock = 0;
   std::unordered_map<int, SliceDevice> dev;
   std::unique_ptr<CopyPool> pool;
 };
@@ -699,28 +726,50 @@ int pm2l_predict_grid_slice(
   const int64_t S = sample_offsets[n_curves];
   uint64_t h = 0xcbf29ce484222325ull ^ uint64_t(device);
   const size_t R = size_t(n_records), C = size_t(n_curves);
-  h = fnv(h, &n_records, 8); h = fnv(h, &n_curves, 8);
+  std::string key;
+  key.reserve(16 + 48 * R + 8 * (C + 1) + 16 * size_t(S > 0 ? S : 0) + 65 * C);
+  auto add = [&](const void* p, size_t n) {
+    h = fnv(h, p, n);
+    key.append(static_cast<const char*>(p), n);
+  };
+  add(&n_records, 8); add(&n_curves, 8);
   if (R) {
-    h = fnv(h, exact_keys, 8 * R); h = fnv(h, exact_curve, 8 * R);
-    h = fnv(h, log_m, 8 * R); h = fnv(h, log_n, 8 * R); h = fnv(h, log_k, 8 * R);
-    h = fnv(h, cand_curve, 8 * R);
+    add(exact_keys, 8 * R); add(exact_curve, 8 * R);
+    add(log_m, 8 * R); add(log_n, 8 * R); add(log_k, 8 * R);
+    add(cand_curve, 8 * R);
   }
-  h = fnv(h, sample_offsets, 8 * (C + 1));
-  if (S > 0) { h = fnv(h, sample_dims, 8 * S); h = fnv(h, sample_thrs, 8 * S); }
+  add(sample_offsets, 8 * (C + 1));
+  if (S > 0) { add(sample_dims, 8 * S); add(sample_thrs, 8 * S); }
   if (C) {
-    h = fnv(h, ref_dim, 8 * C); h = fnv(h, ref_dur, 8 * C); h = fnv(h, ref_thr, 8 * C);
-    h = fnv(h, ref_waves, 8 * C); h = fnv(h, tile_m, 8 * C); h = fnv(h, tile_n, 8 * C);
-    h = fnv(h, split_k, 8 * C); h = fnv(h, blocks_per_wave, 8 * C);
-    h = fnv(h, family_rowblock, C);
+    add(ref_dim, 8 * C); add(ref_dur, 8 * C); add(ref_thr, 8 * C);
+    add(ref_waves, 8 * C); add(tile_m, 8 * C); add(tile_n, 8 * C);
+    add(split_k, 8 * C); add(blocks_per_wave, 8 * C);
+    add(family_rowblock, C);
   }
 
   std::lock_guard<std::mutex> lk(g_slice.mu);
-  pm2l_tables*& t = g_slice.tables[h];
-  if (!t) {
-    if (int rc = pm2l_tables_create(&v, device, &t)) {
-      g_slice.tables.erase(h);
-      return rc;
+  pm2l_tables* t = nullptr;
+  auto range = g_slice.tables.equal_range(h);
+  for (auto it = range.first; it != range.second; ++it)
+    if (it->second.bytes == key) {
+      t = it->second.tables;
+      it->second.last_use = ++g_slice.clock;
+      break;
     }
+  if (!t) {
+    if (int rc = pm2l_tables_create(&v, device, &t)) return rc;
+    while (g_slice.tables.size() >= kSliceCacheMax) {
+      auto lru = g_slice.tables.begin();
+      for (auto it = g_slice.tables.begin(); it != g_slice.tables.end(); ++it)
+        if (it->second.last_use < lru->second.last_use) lru = it;
+      pm2l_tables_destroy(lru->second.tables);
+      g_slice.tables.erase(lru);
+    }
+    SliceEntry e;
+    e.bytes.swap(key);
+    e.tables = t;
+    e.last_use = ++g_slice.clock;
+    g_slice.tables.emplace(h, std::move(e));
   }
   SliceDevice& sd = g_slice.dev[device];
   cudaStream_t& s = sd.stream;

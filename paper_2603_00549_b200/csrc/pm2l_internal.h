@@ -148,6 +148,7 @@ struct GridDev {
   const int32_t* fixr_off = nullptr;
   const FixEntry* fixr = nullptr;
   int32_t max_fix_row = 0;
+  int32_t k_sorted = 0;  // k axis strictly ascending (lookup kernel precondition)
 };
 
 // Host-side image of the staged tables (one contiguous byte blob whose
@@ -168,6 +169,9 @@ struct GridHost {
 std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
                        const int64_t lens[4], int64_t b_lo, int64_t b_hi, GridHost* out);
 GridDev rebase(const GridDev& offsets, const void* base);
+
+// Streaming multiprocessors of the current device (queried once per device).
+int sm_count();
 
 // Kernel launchers (kernels.cu).  Return a CUDA error code (0 = success).
 struct LaunchOut {

@@ -288,7 +288,7 @@ int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const d
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return int(e);
   }
-  const int nb = int(std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 8));
+  const int nb = int(std::min<int64_t>((n + kThreads - 1) / kThreads, int64_t(sm_count()) * 8));
   fn<<<nb, kThreads, smem, s>>>(t, reinterpret_cast<const uint4*>(shapes), n, lut, lut_n, out_lat,
                                 out_curve, out_waves, out_match, out_record, out_dist);
   return int(cudaGetLastError());
@@ -298,7 +298,7 @@ int launch_points_curve(const TablesDev& t, const uint32_t* shapes, const int32_
                         double* out_lat, uint32_t* out_waves, double* out_detail, void* stream) {
   if (n == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int nb = int(std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 16));
+  const int nb = int(std::min<int64_t>((n + kThreads - 1) / kThreads, int64_t(sm_count()) * 16));
   points_curve_kernel<<<nb, kThreads, 0, s>>>(t, reinterpret_cast<const uint4*>(shapes), curves, n,
                                              out_lat, out_waves, out_detail);
   return int(cudaGetLastError());

@@ -42,12 +42,16 @@ __global__ void membound_kernel(const double* __restrict__ f, const int32_t* __r
 }
 
 // ------------------------------------------------------------ exact fsum
-// One warp per segment.  Terms are finite and >= 0.  Pass 1: max exponent E.
+// One warp per segment.  Pass 1: max exponent E (and NaN / inf screening).
 // Pass 2: every term whose bits all lie within a 4x64-bit window anchored at
-// E is added EXACTLY as a fixed-point integer (integer adds are associative,
-// so the warp tree reduction is exact); the 256-bit total is then rounded to
-// nearest-even once.  A segment with a term below the window (dynamic range
-// > ~180 bits) falls back to a sequential exact expansion sum on lane 0.
+// E is added or subtracted EXACTLY as a two's-complement fixed-point integer
+// (integer adds are associative, so the warp tree reduction is exact); the
+// 256-bit total is then rounded to nearest-even once, by magnitude, with its
+// sign.  Terms are < 2^233 in window units, so |sum| < 2^255 for segments
+// below 2^22 terms; longer segments and segments with a term below the
+// window (dynamic range > ~180 bits) take a sequential exact expansion sum
+// (Shewchuk, the algorithm behind math.fsum) on lane 0.  Signed terms are
+// allowed: a raw membound layer below a non-positive floor is negative.
 struct U256 {
   uint64_t w[4];
 };
@@ -59,9 +63,16 @@ __device__ __forceinline__ void add256(U256& a, const U256& b) {
       : "l"(b.w[0]), "l"(b.w[1]), "l"(b.w[2]), "l"(b.w[3]));
 }
 
+__device__ __forceinline__ void sub256(U256& a, const U256& b) {
+  asm("sub.cc.u64 %0, %0, %4;\n\tsubc.cc.u64 %1, %1, %5;\n\t"
+      "subc.cc.u64 %2, %2, %6;\n\tsubc.u64 %3, %3, %7;"
+      : "+l"(a.w[0]), "+l"(a.w[1]), "+l"(a.w[2]), "+l"(a.w[3])
+      : "l"(b.w[0]), "l"(b.w[1]), "l"(b.w[2]), "l"(b.w[3]));
+}
+
 __device__ double two_sum_fsum(const double* v, int64_t lo, int64_t hi) {
   // Shewchuk/msum (the algorithm behind math.fsum), partials kept in a
-  // bounded local array; exact for non-negative finite inputs.
+  // bounded local array; exact for finite inputs of either sign.
   double p[64];
   int np = 0;
   for (int64_t i = lo; i < hi; ++i) {
@@ -94,7 +105,7 @@ __device__ double two_sum_fsum(const double* v, int64_t lo, int64_t hi) {
     const double yr = __dsub_rn(x, hi_);
     if (y == yr) hi_ = x;
   }
-  return hi_;
+  return hi_ == 0.0 ? 0.0 : hi_;  // fsum of zeros is +0.0
 }
 
 __global__ void segment_fsum_kernel(const double* __restrict__ v, const int64_t* __restrict__ off,
@@ -104,24 +115,24 @@ __global__ void segment_fsum_kernel(const double* __restrict__ v, const int64_t*
   if (seg >= nseg) return;
   const int64_t lo = off[seg], hi = off[seg + 1];
   int emax = -2000;
-  bool bad_nan = false, bad_inf = false, bad_neg = false;
+  bool bad_nan = false, pos_inf = false, neg_inf = false;
   for (int64_t i = lo + lane; i < hi; i += 32) {
     const double x = v[i];
     const uint64_t bits = uint64_t(__double_as_longlong(x));
     const int e = int((bits >> 52) & 0x7FF);
     if (x != x) bad_nan = true;
-    else if (e == 0x7FF) bad_inf = true;
-    else if (bits >> 63 && x != 0.0) bad_neg = true;
+    else if (e == 0x7FF) { if (bits >> 63) neg_inf = true; else pos_inf = true; }
     else if (x != 0.0) emax = max(emax, e == 0 ? 1 : e);
   }
   for (int o = 16; o; o >>= 1) emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
   bad_nan = __any_sync(0xFFFFFFFFu, bad_nan);
-  bad_inf = __any_sync(0xFFFFFFFFu, bad_inf);
-  bad_neg = __any_sync(0xFFFFFFFFu, bad_neg);
-  if (bad_nan || bad_neg || bad_inf) {
+  pos_inf = __any_sync(0xFFFFFFFFu, pos_inf);
+  neg_inf = __any_sync(0xFFFFFFFFu, neg_inf);
+  if (bad_nan || pos_inf || neg_inf) {
+    // math.fsum: NaN propagates, -inf + inf raises (NaN here), else the inf
     if (lane == 0)
-      out[seg] = (bad_nan || bad_neg) ? qnan()
-                                      : __longlong_as_double(0x7FF0000000000000ll);
+      out[seg] = (bad_nan || (pos_inf && neg_inf)) ? qnan()
+                 : __longlong_as_double(pos_inf ? 0x7FF0000000000000ll : (long long)0xFFF0000000000000ull);
     return;
   }
   if (emax == -2000) {  // empty or all zeros
@@ -132,10 +143,10 @@ __global__ void segment_fsum_kernel(const double* __restrict__ v, const int64_t*
   // (e==0 -> subnormal, scale as e=1) contributes mant << (e - emax + 180).
   constexpr int kGuard = 180;
   U256 acc = {{0, 0, 0, 0}};
-  bool below = false;
-  for (int64_t i = lo + lane; i < hi; i += 32) {
+  bool below = hi - lo >= (int64_t(1) << 22);
+  for (int64_t i = lo + lane; i < hi && !below; i += 32) {
     const uint64_t bits = uint64_t(__double_as_longlong(v[i]));
-    if (bits == 0) continue;
+    if ((bits << 1) == 0) continue;  // +-0
     const int be = int((bits >> 52) & 0x7FF);
     const uint64_t mant = (bits & 0xFFFFFFFFFFFFFull) | (be ? (1ull << 52) : 0ull);
     const int e = be ? be : 1;
@@ -145,7 +156,8 @@ __global__ void segment_fsum_kernel(const double* __restrict__ v, const int64_t*
     const int limb = sh >> 6, bit = sh & 63;
     term.w[limb] = mant << bit;
     if (bit && limb + 1 < 4) term.w[limb + 1] = mant >> (64 - bit);
-    add256(acc, term);
+    if (bits >> 63) sub256(acc, term);
+    else add256(acc, term);
   }
   below = __any_sync(0xFFFFFFFFu, below);
   if (below) {
@@ -158,9 +170,20 @@ __global__ void segment_fsum_kernel(const double* __restrict__ v, const int64_t*
     add256(acc, other);
   }
   if (lane != 0) return;
-  // round the exact 256-bit integer to 53 bits, nearest-even
+  // sign and magnitude of the exact two's-complement total
+  const bool negative = (acc.w[3] >> 63) != 0;
+  if (negative) {
+    U256 zero = {{0, 0, 0, 0}};
+    sub256(zero, acc);
+    acc = zero;
+  }
+  // round the exact 256-bit magnitude to 53 bits, nearest-even
   int top = 255;
   while (top >= 0 && !((acc.w[top >> 6] >> (top & 63)) & 1ull)) --top;
+  if (top < 0) {  // exact cancellation: fsum returns +0.0
+    out[seg] = 0.0;
+    return;
+  }
   auto bit_at = [&](int p) -> uint64_t { return p < 0 ? 0 : (acc.w[p >> 6] >> (p & 63)) & 1ull; };
   uint64_t mant = 0;
   int shift = 0;  // value = mant * 2^shift * LSB
@@ -186,7 +209,8 @@ __global__ void segment_fsum_kernel(const double* __restrict__ v, const int64_t*
   // LSB weight exponent: (emax - 1075) - kGuard  (unbiased exponent of 1 ulp
   // at biased exponent emax is emax - 1075)
   const int exp2 = shift + (emax - 1075) - kGuard;
-  out[seg] = scalbn(double(mant), exp2);
+  const double mag = scalbn(double(mant), exp2);
+  out[seg] = negative ? -mag : mag;
 }
 
 }  // namespace
@@ -196,7 +220,7 @@ int launch_membound(const double* f, const int32_t* mid, int64_t n, const double
                     uint8_t* floored, void* stream) {
   if (n == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int nb = int(std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 16));
+  const int nb = int(std::min<int64_t>((n + kThreads - 1) / kThreads, int64_t(sm_count()) * 16));
   membound_kernel<<<nb, kThreads, 0, s>>>(f, mid, n, w, b, floors, n_models, out, floored);
   return int(cudaGetLastError());
 }

@@ -220,7 +220,7 @@ int launch_store_lookup(const uint8_t* records, int64_t n_rec, const uint64_t* c
   la.dense = axes != nullptr;
   if (la.dense)
     for (int a = 0; a < 4; ++a) { la.ax[a] = axes[a]; la.len[a] = lens[a]; }
-  const int nb = int(std::min<int64_t>((nq + 255) / 256, 148 * 16));
+  const int nb = int(std::min<int64_t>((nq + 255) / 256, int64_t(sm_count()) * 16));
   store_lookup_kernel<<<nb, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const uint64_t*>(records), n_rec, la, queries, nq, out, first_missing);
   return int(cudaGetLastError());

@@ -506,6 +506,9 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   g.fixr_off = blob.add(fixr_off);
   g.fixr = blob.add(fixr);
   g.max_fix_row = max_fix_row;
+  g.k_sorted = 1;
+  for (int64_t i = 1; i < nK; ++i)
+    if (!(axes[3][i - 1] < axes[3][i])) g.k_sorted = 0;
   out->blob.swap(blob.bytes());
   return "";
 }

@@ -9,11 +9,13 @@ git archive "$REV" paper_2603_00549_b200 include | tar -x -C "$TMP"
 python - "$TMP" "$TAG" <<'PY'
 import os, subprocess, sys
 tmp, tag = sys.argv[1], sys.argv[2]
-sys.path.insert(0, os.getcwd())
-from paper_2603_00549_b200 import _build
-pkg = os.path.join(tmp, "paper_2603_00549_b200")
 out = os.path.join(os.getcwd(), "paper_2603_00549_b200", f"libpm2l_{tag}.so")
-subprocess.run([_build.nvcc(), *_build.NVCC_FLAGS, *_build.SOURCES, "-o", out], cwd=pkg, check=True)
+sys.path.insert(0, tmp)  # the revision's own build script and source list
+from paper_2603_00549_b200 import _build
+if "out_path" in _build.build.__code__.co_varnames:
+    _build.build(force=True, out_path=out)
+else:
+    subprocess.run([_build.nvcc(), *_build.NVCC_FLAGS, *_build.SOURCES, "-o", out], cwd=_build.PKG, check=True)
 print(out)
 PY
 rm -rf "$TMP"

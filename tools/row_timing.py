@@ -19,10 +19,7 @@ LIB = os.path.join(ROOT, "paper_2603_00549_b200", "libpm2l_timing.so")
 
 def build():
     from paper_2603_00549_b200 import _build
-    cmd = [_build.nvcc(), *_build.NVCC_FLAGS, "-DPM2L_TIMING",
-           f"-DPM2L_SOURCE_HASH=\"{_build.source_hash()}\"", *_build.SOURCES, "-o", LIB]
-    subprocess.run(cmd, cwd=_build.PKG, check=True)
-    print(LIB)
+    print(_build.build(extra_flags=["-DPM2L_TIMING"], out_path=LIB))
 
 
 def main():
