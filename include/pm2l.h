@@ -17,6 +17,8 @@
  *   pm2l_tables_create         <- nascache.py:174-241  PreparedGrid.tables()
  *                                 (stages those arrays in HBM once per grid triple)
  *   pm2l_grid_predict          <- backend.py:49-88     predict_grid/_predict_grid_compiled
+ *   pm2l_grid_dplan_*          <- nascache.py:140-245 + backend.py:58-76: the per-grid
+ *                                 planning (PreparedGrid / tables() / axis logs) on the GPU
  *   pm2l_points_predict        <- compute.py:251-268 + 150-193
  *                                 ConfigResolver.resolve + predict_generic, batched
  *   pm2l_points_predict_curve  <- compute.py:150-193   predict_generic with an explicit
@@ -151,6 +153,38 @@ int pm2l_grid_plan_info(const pm2l_grid_plan* p, int64_t* info);
  * form, 3 one-class lookup path; negative on error. */
 int pm2l_grid_plan_kernel(const pm2l_grid_plan* p, const double* out_lat, int verify);
 int pm2l_grid_plan_destroy(pm2l_grid_plan* p);
+/* Device-planned grid slices.  The per-slice planning of pm2l_grid_plan_create
+ * (host libm log2 of the axes, the k-only half of the nearest-config argmin,
+ * the exact-record join of _kernels.pyx:107-110, the per-(curve, k) base
+ * table) runs as one GPU kernel in the launch's stream, so a sweep over many
+ * grids never returns to the host between slices (and a launch is CUDA-graph
+ * capturable).  Axes are DEVICE arrays in canonical GridSpec order (strictly
+ * ascending, every m/n/k value in [1, 2^22)); a violation sets a sticky bit
+ * read by pm2l_grid_dplan_status (1: value out of range, 2: not ascending) and
+ * the slice's outputs are then undefined.  Capacities bound the axis lengths
+ * of every launch.  Outputs, nan_stats and stages as pm2l_grid_plan_launch
+ * (stage 1 = the planner kernel, which also builds the base table).
+ * pm2l_grid_predict plans on the device by itself whenever the host axes are
+ * canonical. */
+typedef struct pm2l_grid_dplan pm2l_grid_dplan;
+int pm2l_grid_dplan_create(pm2l_tables* t, int64_t max_batch, int64_t max_m, int64_t max_n,
+                           int64_t max_k, pm2l_grid_dplan** out);
+int pm2l_grid_dplan_launch(pm2l_grid_dplan* p,
+                           const uint64_t* batch_vals, int64_t n_batch,
+                           const uint64_t* m_vals, int64_t n_m,
+                           const uint64_t* n_vals, int64_t n_n,
+                           const uint64_t* k_vals, int64_t n_k,
+                           int64_t b_lo, int64_t b_hi,
+                           double* out_lat, int32_t* out_curve, uint64_t* out_blocks,
+                           uint64_t* out_waves, uint64_t* nan_stats, int stages, void* stream);
+/* Synchronises the device; returns and clears the sticky status bits. */
+int pm2l_grid_dplan_status(pm2l_grid_dplan* p, uint32_t* status);
+/* Grid kernel of the last launch (codes as pm2l_grid_plan_kernel). */
+int pm2l_grid_dplan_kernel(const pm2l_grid_dplan* p);
+/* Exact-record fix-ups planned for the last launch (synchronises). */
+int pm2l_grid_dplan_fixups(pm2l_grid_dplan* p, int64_t* count);
+int pm2l_grid_dplan_destroy(pm2l_grid_dplan* p);
+
 /* first NaN index of lat[0..n) -> atomicMin into *first (DEVICE u64). */
 int pm2l_nan_scan(const double* lat, int64_t n, uint64_t* first, void* stream);
 

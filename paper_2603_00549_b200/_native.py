@@ -56,6 +56,13 @@ SIGNATURES = {
     "pm2l_grid_plan_info": (_i32, [_p, C.POINTER(_i64)]),
     "pm2l_grid_plan_kernel": (_i32, [_p, _p, _i32]),
     "pm2l_grid_plan_destroy": (_i32, [_p]),
+    "pm2l_grid_dplan_create": (_i32, [_p, _i64, _i64, _i64, _i64, C.POINTER(_p)]),
+    "pm2l_grid_dplan_launch": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
+                                      _p, _p, _p, _p, _p, _i32, _p]),
+    "pm2l_grid_dplan_status": (_i32, [_p, C.POINTER(C.c_uint32)]),
+    "pm2l_grid_dplan_kernel": (_i32, [_p]),
+    "pm2l_grid_dplan_fixups": (_i32, [_p, C.POINTER(_i64)]),
+    "pm2l_grid_dplan_destroy": (_i32, [_p]),
     "pm2l_nan_scan": (_i32, [_p, _i64, _p, _p]),
     "pm2l_grid_predict_all_curves": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64,
                                             _i64, _i64, _p, _p]),
@@ -247,6 +254,56 @@ class GridPlan:
     def close(self):
         if self.handle:
             self._lib.pm2l_grid_plan_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceGridPlanner:
+    """Owning wrapper of pm2l_grid_dplan: per-slice planning on the GPU.
+    ``launch`` takes DEVICE axis tensors (canonical GridSpec order) and runs
+    the planner kernel + grid kernel in the stream; nothing returns to the
+    host between slices (CUDA-graph capturable)."""
+
+    def __init__(self, tables: DeviceTables, max_batch: int, max_m: int, max_n: int, max_k: int):
+        lib = require_gpu()
+        handle = C.c_void_p()
+        check(lib.pm2l_grid_dplan_create(tables.handle, max_batch, max_m, max_n, max_k,
+                                         C.byref(handle)), "pm2l_grid_dplan_create")
+        self._lib = lib
+        self._tables = tables
+        self.handle = handle
+
+    def launch(self, axes, out_lat, b_lo: int = 0, b_hi=None, curve=None, blocks=None,
+               waves=None, nan_stats=None, stages: int = 7, stream=None):
+        B, M, N, K = axes
+        b_hi = len(B) if b_hi is None else b_hi
+        check(self._lib.pm2l_grid_dplan_launch(
+            self.handle, ptr(B), len(B), ptr(M), len(M), ptr(N), len(N), ptr(K), len(K),
+            b_lo, b_hi, ptr(out_lat), ptr(curve), ptr(blocks), ptr(waves), ptr(nan_stats),
+            stages, stream_handle(stream)), "pm2l_grid_dplan_launch")
+
+    def status(self) -> int:
+        """Sticky axis-contract violations since the last call (0: none)."""
+        v = C.c_uint32()
+        check(self._lib.pm2l_grid_dplan_status(self.handle, C.byref(v)), "pm2l_grid_dplan_status")
+        return int(v.value)
+
+    def kernel_path(self) -> int:
+        return int(self._lib.pm2l_grid_dplan_kernel(self.handle))
+
+    def fixups(self) -> int:
+        n = _i64()
+        check(self._lib.pm2l_grid_dplan_fixups(self.handle, C.byref(n)), "pm2l_grid_dplan_fixups")
+        return int(n.value)
+
+    def close(self):
+        if self.handle:
+            self._lib.pm2l_grid_dplan_destroy(self.handle)
             self.handle = C.c_void_p()
 
     def __del__(self):

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -134,11 +135,23 @@ int sm_count() {
 }
 }  // namespace pm2l
 
+struct pm2l_grid_dplan {
+  pm2l_tables* tables = nullptr;
+  DPlanCaps caps;
+  DeviceBuf buf;        // plan arrays + axis slots
+  DeviceBuf workspace;  // base table [C x max_k]
+  GridDev last{};       // the last launched slice (diagnostics)
+  int path = -1;        // grid kernel of the last launch
+};
+
 struct pm2l_tables {
   int device = 0;
   TablesHost host;
   TablesDev dev;
   DeviceBuf blob;
+  // host-axis calls on canonical axes plan on the device (grown on demand)
+  std::unique_ptr<pm2l_grid_dplan> hplan;
+  PinnedBuf axes_pinned;
   // per-call staging (guarded by mu; reused once the previous call's work
   // has drained, tracked by `done`)
   std::mutex mu;
@@ -151,15 +164,84 @@ struct pm2l_tables {
 
 namespace {
 
+// Axes the device planner takes: strictly ascending, values in [1, kLutN).
+bool canonical_axes(const uint64_t* const axes[4], const int64_t lens[4]) {
+  for (int a = 0; a < 4; ++a) {
+    if (lens[a] < 1 || !axes[a]) return false;
+    for (int64_t i = 0; i < lens[a]; ++i) {
+      const uint64_t v = axes[a][i];
+      if (v == 0 || (a > 0 && v >= uint64_t(kLutN)) || (i > 0 && !(axes[a][i - 1] < v)))
+        return false;
+    }
+  }
+  return true;
+}
+
+int dplan_reserve(pm2l_grid_dplan* p, const DPlanCaps& need) {
+  DPlanCaps c = p->caps;
+  if (need.nB <= c.nB && need.nM <= c.nM && need.nN <= c.nN && need.nK <= c.nK && p->buf.ptr)
+    return PM2L_OK;
+  c.nB = std::max(c.nB, need.nB); c.nM = std::max(c.nM, need.nM);
+  c.nN = std::max(c.nN, need.nN); c.nK = std::max(c.nK, need.nK);
+  const TablesDev& t = p->tables->dev;
+  if (!dplan_supported(t, c)) return fail(PM2L_ERR_INVALID, "slice too large for the device planner");
+  p->buf.release();
+  PM2L_CUDA(p->buf.reserve(size_t(dplan_bytes(t, c))));
+  PM2L_CUDA(cudaMemset(p->buf.ptr, 0, size_t(dplan_bytes(t, c))));
+  PM2L_CUDA(p->workspace.reserve(size_t(std::max<int64_t>(int64_t(t.C) * c.nK, 1)) * sizeof(double)));
+  p->caps = c;
+  return PM2L_OK;
+}
+
+// GridDev of a device-planned slice (device axis pointers, or the plan's own
+// axis slots when axes[a] is null).
+int dplan_grid_for(pm2l_grid_dplan* p, const uint64_t* const axes[4], const int64_t lens[4],
+                   int64_t b_lo, int64_t b_hi, GridDev* g) {
+  for (int a = 0; a < 4; ++a)
+    if (lens[a] < 1) return fail(PM2L_ERR_INVALID, "device-planned axes must be non-empty");
+  if (b_lo < 0 || b_hi < b_lo || b_hi > lens[0]) return fail(PM2L_ERR_INVALID, "batch slice out of range");
+  if (lens[0] > p->caps.nB || lens[1] > p->caps.nM || lens[2] > p->caps.nN || lens[3] > p->caps.nK)
+    return fail(PM2L_ERR_INVALID, "axes exceed the device plan's capacity");
+  double* lut = nullptr;
+  if (int rc = get_lut(p->tables->device, &lut)) return rc;
+  *g = dplan_grid(p->tables->dev, p->caps, p->buf.ptr, axes, lens, b_lo, b_hi);
+  g->lut = lut;
+  g->lut_n = kLutN;
+  return PM2L_OK;
+}
+
 int stage_grid(pm2l_tables* t, const uint64_t* const axes[4], const int64_t lens[4],
                int64_t b_lo, int64_t b_hi, cudaStream_t s, GridDev* g) {
-  GridHost gh;
-  std::string err = build_grid(t->host, axes, lens, b_lo, b_hi, &gh);
-  if (!err.empty()) return fail(PM2L_ERR_INVALID, err);
   if (t->pending) {
     PM2L_CUDA(cudaEventSynchronize(t->done));
     t->pending = false;
   }
+  const DPlanCaps need{lens[0], lens[1], lens[2], lens[3]};
+  if (b_lo >= 0 && b_hi >= b_lo && b_hi <= lens[0] && dplan_supported(t->dev, need) &&
+      canonical_axes(axes, lens)) {
+    // canonical axes: upload them (a few KB) and plan on the device
+    if (!t->hplan) {
+      t->hplan.reset(new pm2l_grid_dplan());
+      t->hplan->tables = t;
+    }
+    pm2l_grid_dplan* p = t->hplan.get();
+    if (int rc = dplan_reserve(p, need)) return rc;
+    size_t bytes = 0;
+    for (int a = 0; a < 4; ++a) bytes += size_t(lens[a]) * 8;
+    PM2L_CUDA(t->axes_pinned.reserve(bytes));
+    uint8_t* hp = static_cast<uint8_t*>(t->axes_pinned.ptr);
+    for (int a = 0; a < 4; ++a) {
+      std::memcpy(hp, axes[a], size_t(lens[a]) * 8);
+      PM2L_CUDA(cudaMemcpyAsync(dplan_axis_slot(t->dev, p->caps, p->buf.ptr, a), hp,
+                                size_t(lens[a]) * 8, cudaMemcpyHostToDevice, s));
+      hp += size_t(lens[a]) * 8;
+    }
+    const uint64_t* none[4] = {nullptr, nullptr, nullptr, nullptr};
+    return dplan_grid_for(p, none, lens, b_lo, b_hi, g);
+  }
+  GridHost gh;
+  std::string err = build_grid(t->host, axes, lens, b_lo, b_hi, &gh);
+  if (!err.empty()) return fail(PM2L_ERR_INVALID, err);
   PM2L_CUDA(t->grid_pinned.reserve(gh.blob.size()));
   PM2L_CUDA(t->grid_dev.reserve(gh.blob.size()));
   std::memcpy(t->grid_pinned.ptr, gh.blob.data(), gh.blob.size());
@@ -238,6 +320,11 @@ int pm2l_tables_destroy(pm2l_tables* t) {
     t->grid_dev.release();
     t->workspace.release();
     t->grid_pinned.release();
+    t->axes_pinned.release();
+    if (t->hplan) {
+      t->hplan->buf.release();
+      t->hplan->workspace.release();
+    }
   }
   delete t;
   return PM2L_OK;
@@ -268,6 +355,7 @@ int pm2l_grid_predict(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_batc
   LaunchOut o{out_lat, out_curve, out_blocks, out_waves};
   const int rc = launch_grid(t->dev, g, t->host.max_group,
                              ws > 0 ? static_cast<double*>(t->workspace.ptr) : nullptr, ws, o, s);
+  if (g.dev_planned) t->hplan->path = grid_kernel_path(t->dev, g, o);
   if (rc) return cuda_fail(cudaError_t(rc), "grid kernel launch");
   return finish_call(t, s);
 }
@@ -354,6 +442,93 @@ int pm2l_grid_plan_destroy(pm2l_grid_plan* p) {
     DeviceGuard guard(p->tables->device);
     cudaDeviceSynchronize();
     p->blob.release();
+    p->workspace.release();
+  }
+  delete p;
+  return PM2L_OK;
+}
+
+int pm2l_grid_dplan_create(pm2l_tables* t, int64_t max_batch, int64_t max_m, int64_t max_n,
+                           int64_t max_k, pm2l_grid_dplan** out) {
+  if (!t || !out) return fail(PM2L_ERR_INVALID, "null tables/output handle");
+  *out = nullptr;
+  if (max_batch < 1 || max_m < 1 || max_n < 1 || max_k < 1)
+    return fail(PM2L_ERR_INVALID, "device plan capacities must be >= 1");
+  DeviceGuard guard(t->device);
+  std::unique_ptr<pm2l_grid_dplan> p(new pm2l_grid_dplan());
+  p->tables = t;
+  if (!dplan_supported(t->dev, DPlanCaps{max_batch, max_m, max_n, max_k}))
+    return fail(PM2L_ERR_INVALID, "tables or capacities outside the device planner's range");
+  if (int rc = dplan_reserve(p.get(), DPlanCaps{max_batch, max_m, max_n, max_k})) return rc;
+  double* lut = nullptr;
+  if (int rc = get_lut(t->device, &lut)) return rc;  // built once per device, before any capture
+  *out = p.release();
+  return PM2L_OK;
+}
+
+int pm2l_grid_dplan_launch(pm2l_grid_dplan* p, const uint64_t* batch_vals, int64_t n_batch,
+                           const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals,
+                           int64_t n_n, const uint64_t* k_vals, int64_t n_k, int64_t b_lo,
+                           int64_t b_hi, double* out_lat, int32_t* out_curve,
+                           uint64_t* out_blocks, uint64_t* out_waves, uint64_t* nan_stats,
+                           int stages, void* stream) {
+  if (!p) return fail(PM2L_ERR_INVALID, "null device plan");
+  const bool any_v = out_curve || out_blocks || out_waves;
+  if (any_v && !(out_curve && out_blocks && out_waves))
+    return fail(PM2L_ERR_INVALID, "out_curve/out_blocks/out_waves must be all set or all NULL");
+  if (!batch_vals || !m_vals || !n_vals || !k_vals) return fail(PM2L_ERR_INVALID, "null axis");
+  if (!out_lat) return fail(PM2L_ERR_INVALID, "null out_lat");
+  DeviceGuard guard(p->tables->device);
+  const uint64_t* axes[4] = {batch_vals, m_vals, n_vals, k_vals};
+  const int64_t lens[4] = {n_batch, n_m, n_n, n_k};
+  GridDev g;
+  if (int rc = dplan_grid_for(p, axes, lens, b_lo, b_hi, &g)) return rc;
+  LaunchOut o{out_lat, out_curve, out_blocks, out_waves,
+              reinterpret_cast<unsigned long long*>(nan_stats)};
+  const int64_t ws = grid_workspace_elems(p->tables->dev, g);
+  const int rc = launch_grid(p->tables->dev, g, p->tables->host.max_group,
+                             static_cast<double*>(p->workspace.ptr),
+                             std::max<int64_t>(ws, int64_t(p->tables->dev.C) * p->caps.nK), o,
+                             stream, stages ? stages : kStageAll);
+  if (rc) return cuda_fail(cudaError_t(rc), "device-planned grid launch");
+  p->last = g;
+  p->path = grid_kernel_path(p->tables->dev, g, o);
+  return PM2L_OK;
+}
+
+int pm2l_grid_dplan_status(pm2l_grid_dplan* p, uint32_t* status) {
+  if (!p || !status) return fail(PM2L_ERR_INVALID, "null device plan/status");
+  DeviceGuard guard(p->tables->device);
+  const GridDev g = dplan_grid(p->tables->dev, p->caps, p->buf.ptr, nullptr,
+                               std::array<int64_t, 4>{1, 1, 1, 1}.data(), 0, 1);
+  PM2L_CUDA(cudaDeviceSynchronize());
+  PM2L_CUDA(cudaMemcpy(status, g.status, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  PM2L_CUDA(cudaMemset(g.status, 0, sizeof(uint32_t)));
+  return PM2L_OK;
+}
+
+int pm2l_grid_dplan_kernel(const pm2l_grid_dplan* p) {
+  if (!p) return fail(PM2L_ERR_INVALID, "null device plan");
+  return p->path;
+}
+
+int pm2l_grid_dplan_fixups(pm2l_grid_dplan* p, int64_t* count) {
+  if (!p || !count) return fail(PM2L_ERR_INVALID, "null device plan/count");
+  DeviceGuard guard(p->tables->device);
+  int32_t n = 0;
+  PM2L_CUDA(cudaDeviceSynchronize());
+  if (p->last.n_fix_dev)
+    PM2L_CUDA(cudaMemcpy(&n, p->last.n_fix_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  *count = n;
+  return PM2L_OK;
+}
+
+int pm2l_grid_dplan_destroy(pm2l_grid_dplan* p) {
+  if (!p) return PM2L_OK;
+  {
+    DeviceGuard guard(p->tables->device);
+    cudaDeviceSynchronize();
+    p->buf.release();
     p->workspace.release();
   }
   delete p;

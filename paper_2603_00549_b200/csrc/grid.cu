@@ -108,7 +108,7 @@ void smem_layout(const TablesDev& t, GridLaunch& gl) {
 template <bool VERIFY>
 __global__ void fixup_kernel(TablesDev t, GridDev g, LaunchOut out, const double* fixval) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= g.n_fix) return;
+  if (i >= (g.n_fix_dev ? int64_t(*g.n_fix_dev) : g.n_fix)) return;
   const int64_t p = g.fix_pos[i];
   const uint64_t* c4 = g.fix_coord + 4 * i;
   const int ci = g.fix_curve[i];
@@ -406,9 +406,16 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
     return int(cudaErrorInvalidValue);
   const double* base = t.C > 0 ? ws : nullptr;
   // exact-hit values are precomputed with the base table whenever it runs in
-  // the same launch sequence (stage masks that skip it recompute in fixup_kernel)
-  double* fixval = (g.n_fix > 0 && (stages & kStageBase)) ? ws + nbase : nullptr;
-  if (stages & kStageBase) launch_base_table(t, g, ws, fixval, out.nan_stats, s);
+  // the same launch sequence (stage masks that skip it, and device-planned
+  // slices, recompute them in fixup_kernel)
+  double* fixval = (g.n_fix > 0 && (stages & kStageBase) && !g.dev_planned) ? ws + nbase : nullptr;
+  if (stages & kStageBase) {
+    if (g.dev_planned) {
+      if (const int rc = launch_dplan(t, g, ws, out.nan_stats, s)) return rc;
+    } else {
+      launch_base_table(t, g, ws, fixval, out.nan_stats, s);
+    }
+  }
   const bool v = out.curve != nullptr;
   cudaError_t e = cudaSuccess;
   int row_nb = 0;

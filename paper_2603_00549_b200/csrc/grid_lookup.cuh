@@ -168,6 +168,8 @@ __device__ __forceinline__ void row_prologue(uint8_t* smem, const RowCtx<STAGE>&
   bulk_g2s(c.glk, t.grp_lk, r16(8ll * c.G), bar);
   bulk_g2s(c.gcur, t.g_cw, r16(8ll * t.R), bar);
   if (STAGE) {
+    // device-planned slices: the per-k tables come from the planner kernel
+    if (g.dev_planned) pdl_wait();
     mbar_expect_tx(bar + 1, r16(4ll * c.nK) + 2 * r16(8ll * c.nK) + r16(4ll * rl.nkc * c.G));
     bulk_g2s(smem + rl.off_ms, g.mn_sorted, r16(8ll * c.nK), bar + 1);
     bulk_g2s(smem + rl.off_kq, g.logK, r16(8ll * c.nK), bar + 1);
@@ -693,6 +695,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
   if (warp < P) {
     int j = warp;
     int tile = blockIdx.x + j * gridDim.x;
+    if (g.dev_planned) pdl_wait();  // row inputs (logs, tile counts) come from the planner
     RowIn<NB> rin = load_row_in<NB, RB>(g, rl, min(tile, rl.tiles - 1), t.NW, lane);
     mbar_wait(bar, 0);
     if (STAGE) mbar_wait(bar + 1, 0);
@@ -722,6 +725,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       const int tile0 = blockIdx.x + cw * gridDim.x;
       if (tile0 < rl.tiles) {
         uint8_t* wb0 = smem + rl.off_warp + cw * rl.warp_bytes;
+        if (g.dev_planned) pdl_wait();
         const RowIn<NB> r0 = load_row_in<NB, RB>(g, rl, tile0, t.NW, lane);
         mbar_wait(bar, 0);
         if (!RB) build_w_table<NB, STAGE>(c, g, r0, reinterpret_cast<double*>(wb0 + rl.w_W), lane);

@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(kWsThreads) grid_kernel(TablesDev t, GridDev g
   }
   __syncthreads();
   if (warp < kProducerWarps) {
+    if (g.dev_planned) pdl_wait();  // row logs come from the planner kernel
     int it = 0;
     int tile = blockIdx.x;
     // tile = (row * nbs + slab) * nkt + k tile

@@ -149,7 +149,37 @@ struct GridDev {
   const FixEntry* fixr = nullptr;
   int32_t max_fix_row = 0;
   int32_t k_sorted = 0;  // k axis strictly ascending (lookup kernel precondition)
+  // device-planned slices (plan.cu): every array above is written on the GPU
+  // by plan_kernel, in the same stream as the grid kernel.  n_fix is then the
+  // capacity (the triple's exact records) and n_fix_dev the planned count;
+  // status collects axis violations (kPlanBad*), 0 for a valid plan.
+  int32_t dev_planned = 0;
+  const int32_t* n_fix_dev = nullptr;
+  uint32_t* status = nullptr;
+  const double* lut = nullptr;  // per-device libm log2 table of [0, lut_n)
+  int64_t lut_n = 0;
 };
+
+// Device planner (plan.cu): the per-slice work of build_grid on the GPU for
+// canonical axes (strictly ascending, every value in [1, lut_n)).
+enum : uint32_t { kPlanBadValue = 1, kPlanUnsorted = 2 };
+struct DPlanCaps {
+  int64_t nB = 0, nM = 0, nN = 0, nK = 0;  // axis capacities (batch: the whole axis)
+};
+// Whether a slice of these sizes can be device-planned with these tables.
+bool dplan_supported(const struct TablesDev& t, const DPlanCaps& c);
+// Bytes of the device buffer holding a plan of capacity c (incl. axes).
+int64_t dplan_bytes(const struct TablesDev& t, const DPlanCaps& c);
+// GridDev over a plan buffer for axes of the given lengths (axes: DEVICE
+// arrays; nullptr -> the buffer's own axis copies, filled by the caller).
+struct GridDev dplan_grid(const struct TablesDev& t, const DPlanCaps& c, void* buf,
+                          const uint64_t* const axes[4], const int64_t lens[4], int64_t b_lo,
+                          int64_t b_hi);
+// Device axis copies inside a plan buffer (for host-side axes uploads).
+uint64_t* dplan_axis_slot(const struct TablesDev& t, const DPlanCaps& c, void* buf, int axis);
+// plan_kernel: logs, per-k tables, exact-hit join, base table, stats reset.
+int launch_dplan(const struct TablesDev& t, const struct GridDev& g, double* base,
+                 unsigned long long* nan_stats, void* stream);
 
 // Host-side image of the staged tables (one contiguous byte blob whose
 // internal pointers are rebased onto the device copy).
