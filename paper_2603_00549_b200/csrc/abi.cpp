@@ -434,6 +434,11 @@ int pm2l_grid_plan_kernel(const pm2l_grid_plan* p, const double* out_lat, int ve
 int pm2l_debug_row_timing(unsigned long long* host, int n) {
   return pm2l::row_timing_copy(host, n);
 }
+int pm2l_debug_plan_timing(unsigned long long* host, int n) {
+  if (!pm2l::plan_timing_buffer()) return -1;
+  return int(cudaMemcpy(host, pm2l::plan_timing_buffer(), sizeof(unsigned long long) * size_t(n),
+                        cudaMemcpyDeviceToHost));
+}
 #endif
 
 int pm2l_grid_plan_destroy(pm2l_grid_plan* p) {
@@ -515,11 +520,12 @@ int pm2l_grid_dplan_kernel(const pm2l_grid_dplan* p) {
 int pm2l_grid_dplan_fixups(pm2l_grid_dplan* p, int64_t* count) {
   if (!p || !count) return fail(PM2L_ERR_INVALID, "null device plan/count");
   DeviceGuard guard(p->tables->device);
-  int32_t n = 0;
   PM2L_CUDA(cudaDeviceSynchronize());
-  if (p->last.n_fix_dev)
-    PM2L_CUDA(cudaMemcpy(&n, p->last.n_fix_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
-  *count = n;
+  std::vector<int64_t> pos(size_t(std::max<int64_t>(p->last.n_fix, 0)));
+  if (!pos.empty())
+    PM2L_CUDA(cudaMemcpy(pos.data(), p->last.fix_pos, pos.size() * sizeof(int64_t),
+                         cudaMemcpyDeviceToHost));
+  *count = std::count_if(pos.begin(), pos.end(), [](int64_t v) { return v >= 0; });
   return PM2L_OK;
 }
 

@@ -108,8 +108,9 @@ void smem_layout(const TablesDev& t, GridLaunch& gl) {
 template <bool VERIFY>
 __global__ void fixup_kernel(TablesDev t, GridDev g, LaunchOut out, const double* fixval) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= (g.n_fix_dev ? int64_t(*g.n_fix_dev) : g.n_fix)) return;
+  if (i >= g.n_fix) return;
   const int64_t p = g.fix_pos[i];
+  if (p < 0) return;  // device plans: a record off this slice
   const uint64_t* c4 = g.fix_coord + 4 * i;
   const int ci = g.fix_curve[i];
   if (out.nan_stats) {
@@ -320,10 +321,10 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
   if (tu.debug)
     std::fprintf(stderr,
                  "plan_rows: curve=%d near=%d all_gemm=%d kfast=%d nK=%lld nb=%lld align=%d CM=%d G=%d "
-                 "NW=%d cm_tab=%d k_sorted=%d\n",
+                 "NW=%d k_sorted=%d\n",
                  out.curve != nullptr, gl.near, t.all_gemm, g.kfast != nullptr, (long long)g.nK,
                  (long long)nb, int(reinterpret_cast<uintptr_t>(out.lat) & 15), t.CM, t.G, t.NW,
-                 g.cm_tab != nullptr, g.k_sorted);
+                 g.k_sorted);
   // the byte maps and per-chunk group cuts assume an ascending k axis (the
   // canonical GridSpec order); the raw FFI accepts any order, which takes
   // the order-independent sweep kernel
@@ -333,7 +334,7 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
   rl.pair = g.nK % 2 == 0 && (reinterpret_cast<uintptr_t>(out.lat) & 15) == 0;
   rl.rowblock = t.all_rowblock;
   if (rl.rowblock && !rl.pair) return rl;  // row-block variant: pair stores only
-  if ((t.all_gemm && !g.cm_tab) || t.NW < 1) return rl;
+  if (t.NW < 1) return rl;
   int NB = 8;
   while (nb % NB) NB >>= 1;
   rl.kc = int(std::min<int64_t>(g.nK, kKChunk));

@@ -95,7 +95,7 @@ struct RowIn {
   double qm, qn;
   int im, jn;
   uint64_t b[NB];
-  uint64_t cm[2], cn[2];  // tile counts of wave classes lane, lane + 32
+  uint64_t m, n;  // the row's shape (W table: tile counts per wave class)
 };
 
 template <int NB, bool RB = false>
@@ -104,18 +104,22 @@ __device__ __forceinline__ RowIn<NB> load_row_in(const GridDev& g, const RowLaun
   RowIn<NB> r;
   const int rs = fdiv(tile, rl.d_nkc), row = fdiv(rs, rl.d_nbs), slab = rs - row * rl.nbs;
   const int im = fdiv(row, rl.d_nN), jn = row - im * int(g.nN);
-  r.qm = g.logM[im];
-  r.qn = g.logN[jn];
   r.im = im;
   r.jn = jn;
+  r.m = g.M[im];
+  r.n = g.N[jn];
+  if (g.lut) {
+    // device plans: the row's log2 straight from the per-device libm table,
+    // so a tile's staircase and W table never wait for the planner kernel
+    // (an out-of-range value is the planner's reported contract violation)
+    r.qm = r.m < uint64_t(g.lut_n) ? g.lut[r.m] : 0.0;
+    r.qn = r.n < uint64_t(g.lut_n) ? g.lut[r.n] : 0.0;
+  } else {
+    r.qm = g.logM[im];
+    r.qn = g.logN[jn];
+  }
 #pragma unroll
   for (int ib = 0; ib < NB; ++ib) r.b[ib] = g.B[g.b_lo + slab * NB + ib];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int wc = min(lane + 32 * h, NW - 1);
-    r.cm[h] = RB ? 0 : g.cm_tab[im * NW + wc];   // row-block waves ignore (m, n)
-    r.cn[h] = RB ? 0 : g.cn_tab[jn * NW + wc];
-  }
   return r;
 }
 
@@ -167,15 +171,19 @@ __device__ __forceinline__ void row_prologue(uint8_t* smem, const RowCtx<STAGE>&
   bulk_g2s(c.wcp, t.wcp, r16(int64_t(sizeof(WcParam)) * c.NW), bar);
   bulk_g2s(c.glk, t.grp_lk, r16(8ll * c.G), bar);
   bulk_g2s(c.gcur, t.g_cw, r16(8ll * t.R), bar);
-  if (STAGE) {
-    // device-planned slices: the per-k tables come from the planner kernel
-    if (g.dev_planned) pdl_wait();
-    mbar_expect_tx(bar + 1, r16(4ll * c.nK) + 2 * r16(8ll * c.nK) + r16(4ll * rl.nkc * c.G));
-    bulk_g2s(smem + rl.off_ms, g.mn_sorted, r16(8ll * c.nK), bar + 1);
-    bulk_g2s(smem + rl.off_kq, g.logK, r16(8ll * c.nK), bar + 1);
-    bulk_g2s(smem + rl.off_kr, g.kright, r16(4ll * rl.nkc * c.G), bar + 1);
-    bulk_g2s(smem + rl.off_kf, g.kfast, r16(4ll * c.nK), bar + 1);
-  }
+}
+
+// The per-k tables of the slice (STAGE): on bar + 1.  A device-planned
+// slice's come from the planner kernel, so the issuing thread has passed
+// griddepcontrol.wait first.
+template <bool STAGE>
+__device__ __forceinline__ void row_prologue_k(uint8_t* smem, const RowCtx<STAGE>& c,
+                                               const GridDev& g, const RowLaunch& rl, uint64_t* bar) {
+  mbar_expect_tx(bar + 1, r16(4ll * c.nK) + 2 * r16(8ll * c.nK) + r16(4ll * rl.nkc * c.G));
+  bulk_g2s(smem + rl.off_ms, g.mn_sorted, r16(8ll * c.nK), bar + 1);
+  bulk_g2s(smem + rl.off_kq, g.logK, r16(8ll * c.nK), bar + 1);
+  bulk_g2s(smem + rl.off_kr, g.kright, r16(4ll * rl.nkc * c.G), bar + 1);
+  bulk_g2s(smem + rl.off_kf, g.kfast, r16(4ll * c.nK), bar + 1);
 }
 
 // Tile coordinates: tile = (row * nbs + slab) * nkc + k chunk.
@@ -200,8 +208,9 @@ __device__ __forceinline__ void build_w_table(const RowCtx<STAGE>& c, const Grid
   const int NW = c.NW;
   for (int wc = lane; wc < NW; wc += 32) {
     const WcParam& p = c.wcp[wc];
-    const uint64_t tmn = wc < 64 ? cur.cm[wc >> 5] * cur.cn[wc >> 5]
-                                 : g.cm_tab[cur.im * NW + wc] * g.cn_tab[cur.jn * NW + wc];
+    // ceil(m / tile_m) * ceil(n / tile_n) * split_k in u64 (the reference's
+    // block product, _kernels.pyx:126; wrapping like the host planner's)
+    const uint64_t tmn = ceil_div_w(p, 0, cur.m, p.tm) * (ceil_div_w(p, 1, cur.n, p.tn) * p.sk);
     const double rw = p.rw;
 #pragma unroll
     for (int ib = 0; ib < NB; ++ib) {
@@ -219,7 +228,11 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
                                            const RowLaunch& rl, const TileXY& x,
                                            const RowIn<NB>& cur, uint8_t* wb, int lane,
                                            int mark_tile = 1 << 30, bool with_w = true,
-                                           uint64_t* stair_ready = nullptr) {
+                                           uint64_t* stair_ready = nullptr,
+                                           uint64_t* k_ready = nullptr, bool plan_wait = false) {
+  // k_ready / plan_wait (a builder's first tile): the staircase and W table
+  // need only the CTA tables; the cut searches below also need the slice's
+  // per-k tables (bar k_ready) and, for device plans, the planner kernel
   // stair_ready != nullptr: a helper warp builds the group cuts and gmap of
   // this tile (help_group_map) once the staircase is published
   uint64_t* sD = reinterpret_cast<uint64_t*>(wb + rl.w_sD);
@@ -298,6 +311,8 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
       if (lane == ib) W[ib] = __longlong_as_double(static_cast<long long>(cur.b[ib]));
   }
   __syncwarp();
+  if (plan_wait) pdl_wait();
+  if (STAGE && k_ready) mbar_wait(k_ready, 0);
   ROW_MARK(mark_tile, 6);
   // ---- cut points: fixed-trip branch-free binary searches, one shared
   // load per step, both kinds in one loop (lanes never diverge)
@@ -619,7 +634,15 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
   }
   // exact-record hits in these blocks take priority over the nearest result
   // (_kernels.pyx:107-110): re-count them by their exact result
-  const int f0 = g.fixr_off[x.row], f1 = g.fixr_off[x.row + 1];
+  int f0, f1;
+  if (g.fixr_rng) {  // device plan: the row's record range (off-slice entries skip below)
+    const int2 fr = g.fixr_rng[x.row];
+    f0 = fr.x;
+    f1 = fr.y;
+  } else {
+    f0 = g.fixr_off[x.row];
+    f1 = g.fixr_off[x.row + 1];
+  }
   if (f1 > f0) {
     __syncwarp();  // this warp's stores above are visible to every lane
     for (int f = f0 + lane; f < f1; f += 32) {
@@ -690,15 +713,18 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     row_prologue<STAGE>(smem, c, t, g, rl, bar);
+    // host plans: the per-k tables are ready now; device plans: the first
+    // writer warp issues them after the planner kernel (below)
+    if (STAGE && !g.dev_planned) row_prologue_k<STAGE>(smem, c, g, rl, bar);
   }
   __syncthreads();  // mbarriers initialised before anyone waits on them
   if (warp < P) {
     int j = warp;
     int tile = blockIdx.x + j * gridDim.x;
-    if (g.dev_planned) pdl_wait();  // row inputs (logs, tile counts) come from the planner
+    // row inputs (axis values, libm log2) are plan-independent: the first
+    // tile's staircase and W table overlap the planner kernel
     RowIn<NB> rin = load_row_in<NB, RB>(g, rl, min(tile, rl.tiles - 1), t.NW, lane);
     mbar_wait(bar, 0);
-    if (STAGE) mbar_wait(bar + 1, 0);
     for (; tile < rl.tiles; j += P, tile += P * gridDim.x) {
       const int slot = j % S, use = j / S;
       const RowIn<NB> cur = rin;
@@ -711,9 +737,11 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       if (lane == 0 && tile < 16384) rl.dbg_row[tile * 8] = t_entry;
 #endif
       ROW_MARK(tile, 1);
+      const bool first = j < P;
       build_tile<NB, STAGE, SEGW, RB>(c, g, rl, tile_xy(rl, tile, c.nK), cur,
                                   smem + rl.off_warp + slot * rl.warp_bytes, lane, tile,
-                                  /*with_w=*/j >= nhelp, j < nhelp ? sready + j : nullptr);
+                                  /*with_w=*/j >= nhelp, j < nhelp ? sready + j : nullptr,
+                                  first ? bar + 1 : nullptr, first && g.dev_planned);
       __syncwarp();
       ROW_MARK(tile, 2);
       mbar_arrive(full + slot);
@@ -723,12 +751,17 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
     if (cw < nhelp) {
       // W table of builder cw's first tile (position cw, slot cw)
       const int tile0 = blockIdx.x + cw * gridDim.x;
+      uint8_t* wb0 = smem + rl.off_warp + cw * rl.warp_bytes;
+      RowIn<NB> r0;
+      if (tile0 < rl.tiles) r0 = load_row_in<NB, RB>(g, rl, tile0, t.NW, lane);
+      mbar_wait(bar, 0);
+      if (tile0 < rl.tiles && !RB)
+        build_w_table<NB, STAGE>(c, g, r0, reinterpret_cast<double*>(wb0 + rl.w_W), lane);
+      if (g.dev_planned) {
+        pdl_wait();  // the planner kernel's per-k tables are complete and visible
+        if (STAGE && cw == 0 && lane == 0) row_prologue_k<STAGE>(smem, c, g, rl, bar);
+      }
       if (tile0 < rl.tiles) {
-        uint8_t* wb0 = smem + rl.off_warp + cw * rl.warp_bytes;
-        if (g.dev_planned) pdl_wait();
-        const RowIn<NB> r0 = load_row_in<NB, RB>(g, rl, tile0, t.NW, lane);
-        mbar_wait(bar, 0);
-        if (!RB) build_w_table<NB, STAGE>(c, g, r0, reinterpret_cast<double*>(wb0 + rl.w_W), lane);
         if (STAGE) mbar_wait(bar + 1, 0);
         mbar_wait(sready + cw, 0);  // the builder's staircase is published
         help_group_map<STAGE, SEGW>(c, g, rl, tile_xy(rl, tile0, c.nK), wb0, lane);

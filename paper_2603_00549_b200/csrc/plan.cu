@@ -32,14 +32,24 @@ namespace {
 
 using namespace dev;
 
-constexpr int kPlanThreads = 1024;
+constexpr int kPlanThreads = 256;
 constexpr int kBaseBlock = 1024;           // k values per base-table block
 constexpr int kMaxBaseSamples = 256;       // samples staged per base block
-constexpr int64_t kMaxJoinRows = 32768;    // (m, n) rows of a device-planned slice
-constexpr int kMaxJoinRecords = 1 << 16;
-constexpr int64_t kJoinStageBytes = 96 * 1024;
 
 __device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+#ifdef PM2L_TIMING
+#define PLAN_MARK(a, slot)                                                   \
+  do {                                                                       \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {                             \
+      unsigned long long t_;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+      (a).dbg[8 * blockIdx.x + (slot)] = t_;                                 \
+    }                                                                        \
+  } while (0)
+#else
+#define PLAN_MARK(a, slot) do {} while (0)
+#endif
 
 __device__ __forceinline__ void flag(uint32_t* status, uint32_t bit) {
   if (status) atomicOr(status, bit);
@@ -57,41 +67,64 @@ __device__ __forceinline__ int64_t find_sorted(const uint64_t* a, int64_t n, uin
 
 struct PlanArgs {
   int nkc;           // k chunks
+  int kparts;        // rank CTAs per k chunk
+  int nrec;          // record CTAs
+  int nrow;          // row-range CTAs
   int kblocks;       // base-table k blocks per curve
-  int stage_axes;    // join stages the axes in shared memory
+  int stage_axes;    // record / row CTAs stage the axes in shared memory
+  int stage_keys;    // row CTAs stage the records' (m, n) keys
   const double* lut;
   int64_t lut_n;
   double* base;
   unsigned long long* stats;
+#ifdef PM2L_TIMING
+  unsigned long long* dbg;  // diagnostic build: per-CTA globaltimer at entry / exit
+#endif
 };
 
-// ---------------------------------------------------------------- k chunk
-__device__ void plan_k_chunk(const TablesDev& t, const GridDev& g, const PlanArgs& a, int chunk,
-                             uint8_t* smem) {
+// ----------------------------------------------------------------- k ranks
+// One chunk of kKChunk k values is served by several CTAs; each computes the
+// k-only quantities of the whole chunk in shared memory (a few dependent
+// loads per k) and the rank of its own kRankPerCta k values by counting:
+// rank(i) = #{j : mn_j > mn_i} + #{j < i : mn_j == mn_i}, the position in the
+// stable descending order of mn (std::stable_sort in the host planner).  A
+// warp counts for kRankPerWarp values at a time over lane-strided j.
+constexpr int kRankPerWarp = 2;
+constexpr int kRankPerCta = kRankPerWarp * (kPlanThreads / 32);
+
+__device__ void plan_k_rank(const TablesDev& t, const GridDev& g, const PlanArgs& a, int chunk,
+                            int part, uint8_t* smem) {
   const int64_t k0 = int64_t(chunk) * kKChunk;
   const int kc = int(::min((int64_t)kKChunk, g.nK - k0));
-  int P = 1;
-  while (P < kc) P <<= 1;
   uint64_t* mn_s = reinterpret_cast<uint64_t*>(smem);                 // [kKChunk]
   double* glk = reinterpret_cast<double*>(mn_s + kKChunk);            // [256]
-  uint16_t* idx_s = reinterpret_cast<uint16_t*>(glk + 256);           // [kKChunk]
-  uint8_t* st_s = reinterpret_cast<uint8_t*>(idx_s + kKChunk);        // [kKChunk]
+  uint8_t* st_s = reinterpret_cast<uint8_t*>(glk + 256);              // [kKChunk]
   uint8_t* gb_s = st_s + kKChunk;                                     // [kKChunk]
-  const int G = t.G;
-  for (int i = threadIdx.x; i < G; i += blockDim.x) glk[i] = t.grp_lk[i];
+  const int G = t.G, tid = threadIdx.x;
+  constexpr int kPer = kKChunk / kPlanThreads;
+  uint64_t kv[kPer];
+#pragma unroll
+  for (int h = 0; h < kPer; ++h) {
+    const int i = tid + h * kPlanThreads;
+    kv[h] = i < kc ? g.K[k0 + i] : 0;
+  }
+  for (int i = tid; i < G; i += kPlanThreads) glk[i] = t.grp_lk[i];
   __syncthreads();
+  PLAN_MARK(a, 1);
   auto dk = [&](int gg, double qk) { return abs_bits(__dsub_rn(glk[gg], qk)); };
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    if (i >= kc) {
-      mn_s[i] = 0;
-      idx_s[i] = 0xFFFF;  // after every real entry (equal mn: larger index)
-      continue;
-    }
-    const int64_t ik = k0 + i;
-    const uint64_t k = g.K[ik];
-    if (k == 0 || int64_t(k) >= a.lut_n || k >= (uint64_t(1) << 62)) flag(g.status, kPlanBadValue);
-    if (ik > 0 && !(g.K[ik - 1] < k)) flag(g.status, kPlanUnsorted);
-    const double qk = (k >= 1 && int64_t(k) < a.lut_n) ? a.lut[k] : 0.0;
+  double qv[kPer];  // every log2 gather in flight at once
+#pragma unroll
+  for (int h = 0; h < kPer; ++h) {
+    const uint64_t k = kv[h];
+    qv[h] = (k >= 1 && int64_t(k) < a.lut_n) ? __ldg(a.lut + k) : 0.0;
+  }
+#pragma unroll
+  for (int h = 0; h < kPer; ++h) {
+    const int i = tid + h * kPlanThreads;
+    if (i >= kc) continue;
+    const uint64_t k = kv[h];
+    const bool ok = k >= 1 && int64_t(k) < a.lut_n;
+    const double qk = qv[h];
     // #groups with grp_lk < qk (std::lower_bound)
     int lo = 0, hi = G;
     while (lo < hi) {
@@ -107,136 +140,144 @@ __device__ void plan_k_chunk(const TablesDev& t, const GridDev& g, const PlanArg
       gb = start - 1;
       while (gb > 0 && dk(gb - 1, qk) == mn) --gb;
     }
-    const_cast<KInfo*>(g.kinfo)[ik] = KInfo{qk, start, 0};
-    const_cast<double*>(g.logK)[ik] = qk;
     mn_s[i] = mn;
-    idx_s[i] = uint16_t(i);
     st_s[i] = uint8_t(start);
     gb_s[i] = uint8_t(gb);
-  }
-  __syncthreads();
-  // bitonic sort, "a before b" = mn_a > mn_b || (mn_a == mn_b && idx_a < idx_b):
-  // the stable descending order of mn (ties keep ascending k index)
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < (P >> 1); i += blockDim.x) {
-        const int lo_i = 2 * i - (i & (stride - 1));
-        const int hi_i = lo_i + stride;
-        const bool up = (lo_i & size) == 0;  // this run ascends in "before" order
-        const uint64_t ma = mn_s[lo_i], mb = mn_s[hi_i];
-        const uint16_t ia = idx_s[lo_i], ib = idx_s[hi_i];
-        const bool b_first = mb > ma || (mb == ma && ib < ia);
-        if (b_first == up) {
-          mn_s[lo_i] = mb; mn_s[hi_i] = ma;
-          idx_s[lo_i] = ib; idx_s[hi_i] = ia;
-        }
-      }
-      __syncthreads();
+    if (part == 0) {  // one CTA per chunk writes the per-k arrays and checks the axis
+      const int64_t ik = k0 + i;
+      const_cast<KInfo*>(g.kinfo)[ik] = KInfo{qk, start, 0};
+      const_cast<double*>(g.logK)[ik] = qk;
+      if (!ok || k >= (uint64_t(1) << 62)) flag(g.status, kPlanBadValue);
+      if (ik > 0 && !(g.K[ik - 1] < k)) flag(g.status, kPlanUnsorted);
     }
   }
-  uint32_t* kfast = const_cast<uint32_t*>(g.kfast);
-  uint64_t* mn_sorted = const_cast<uint64_t*>(g.mn_sorted);
-  for (int r = threadIdx.x; r < kc; r += blockDim.x) {
-    const int i = idx_s[r];
-    mn_sorted[k0 + r] = mn_s[r];
-    kfast[k0 + i] = uint32_t(r) | (uint32_t(gb_s[i]) << 16) | (uint32_t(st_s[i]) << 24);
+  __syncthreads();
+  PLAN_MARK(a, 2);
+  const int lane = tid & 31, warp = tid >> 5;
+  const int i0 = part * kRankPerCta + warp * kRankPerWarp;
+  uint64_t mi[kRankPerWarp];
+  int cnt[kRankPerWarp];
+#pragma unroll
+  for (int u = 0; u < kRankPerWarp; ++u) {
+    mi[u] = i0 + u < kc ? mn_s[i0 + u] : 0;
+    cnt[u] = 0;
+  }
+  if (i0 < kc) {
+#pragma unroll 4
+    for (int j = lane; j < kc; j += 32) {
+      const uint64_t mj = mn_s[j];
+#pragma unroll
+      for (int u = 0; u < kRankPerWarp; ++u)
+        cnt[u] += (mj > mi[u] || (mj == mi[u] && j < i0 + u)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kRankPerWarp; ++u)
+      for (int o = 16; o; o >>= 1) cnt[u] += __shfl_xor_sync(0xFFFFFFFFu, cnt[u], o);
+    if (lane < kRankPerWarp) {
+      int r = 0;
+#pragma unroll
+      for (int u = 0; u < kRankPerWarp; ++u) r = lane == u ? cnt[u] : r;
+      const int i = i0 + lane;
+      if (i < kc) {
+        const_cast<uint64_t*>(g.mn_sorted)[k0 + r] = mn_s[i];
+        const_cast<uint32_t*>(g.kfast)[k0 + i] =
+            uint32_t(r) | (uint32_t(gb_s[i]) << 16) | (uint32_t(st_s[i]) << 24);
+      }
+    }
   }
   // kright[chunk][g]: first chunk-local index whose insertion point exceeds
   // g (start is non-decreasing along an ascending k axis)
-  int32_t* kright = const_cast<int32_t*>(g.kright);
-  for (int gg = threadIdx.x; gg < G; gg += blockDim.x) {
-    int l = 0, h = kc;
-    while (l < h) {
-      const int mid = (l + h) >> 1;
-      if (st_s[mid] <= gg) l = mid + 1; else h = mid;
+  if (part == 0) {
+    int32_t* kright = const_cast<int32_t*>(g.kright);
+    for (int gg = tid; gg < G; gg += kPlanThreads) {
+      int l = 0, h = kc;
+      while (l < h) {
+        const int mid = (l + h) >> 1;
+        if (st_s[mid] <= gg) l = mid + 1; else h = mid;
+      }
+      kright[int64_t(chunk) * G + gg] = l;
     }
-    kright[int64_t(chunk) * G + gg] = l;
   }
 }
 
 // ------------------------------------------------------- exact-record join
-__device__ void plan_join(const TablesDev& t, const GridDev& g, const PlanArgs& a,
-                          uint8_t* smem) {
-  const int64_t nbs = g.b_hi - g.b_lo, rows = g.nM * g.nN;
-  int32_t* cnt = reinterpret_cast<int32_t*>(smem);  // [rows + 1]
-  uint64_t* ax = reinterpret_cast<uint64_t*>(smem + ((4 * (rows + 1) + 15) & ~int64_t(15)));
-  const uint64_t* Bs = g.B + g.b_lo;
-  const uint64_t* Ms = g.M;
-  const uint64_t* Ns = g.N;
-  const uint64_t* Ks = g.K;
-  if (a.stage_axes) {
-    uint64_t* p = ax;
-    for (int64_t i = threadIdx.x; i < nbs; i += blockDim.x) p[i] = Bs[i];
-    Bs = p; p += nbs;
-    for (int64_t i = threadIdx.x; i < g.nM; i += blockDim.x) p[i] = Ms[i];
-    Ms = p; p += g.nM;
-    for (int64_t i = threadIdx.x; i < g.nN; i += blockDim.x) p[i] = Ns[i];
-    Ns = p; p += g.nN;
-    for (int64_t i = threadIdx.x; i < g.nK; i += blockDim.x) p[i] = Ks[i];
-    Ks = p;
-  }
-  for (int64_t r = threadIdx.x; r <= rows; r += blockDim.x) cnt[r] = 0;
+// Records are the tables' unique exact shapes sorted by (m, n, b, k), so one
+// (m, n) row owns a contiguous range of them.  Record CTAs locate each
+// record on the slice (fix-up entry, or ib = -1 when it is off the slice);
+// row CTAs find each row's range.  Both are independent of each other.
+__device__ void stage_axes(const GridDev& g, const PlanArgs& a, uint64_t* ax,
+                           const uint64_t** Bs, const uint64_t** Ms, const uint64_t** Ns,
+                           const uint64_t** Ks, bool with_bk) {
+  const int64_t nbs = g.b_hi - g.b_lo;
+  *Bs = g.B + g.b_lo; *Ms = g.M; *Ns = g.N; *Ks = g.K;
+  if (!a.stage_axes) return;
+  uint64_t* p = ax;
+  for (int64_t i = threadIdx.x; i < g.nM; i += blockDim.x) p[i] = g.M[i];
+  *Ms = p; p += g.nM;
+  for (int64_t i = threadIdx.x; i < g.nN; i += blockDim.x) p[i] = g.N[i];
+  *Ns = p; p += g.nN;
+  if (!with_bk) return;
+  for (int64_t i = threadIdx.x; i < nbs; i += blockDim.x) p[i] = g.B[g.b_lo + i];
+  *Bs = p; p += nbs;
+  for (int64_t i = threadIdx.x; i < g.nK; i += blockDim.x) p[i] = g.K[i];
+  *Ks = p;
+}
+
+__device__ void plan_records(const TablesDev& t, const GridDev& g, const PlanArgs& a, int blk,
+                             uint8_t* smem) {
+  const int r = blk * kPlanThreads + threadIdx.x;
+  const bool mine = r < t.n_mn;
+  uint64_t c4[4] = {0, 0, 0, 0};
+  if (mine)
+    for (int j = 0; j < 4; ++j) c4[j] = t.ex_mn_coord[4 * int64_t(r) + j];
+  const uint64_t *Bs, *Ms, *Ns, *Ks;
+  stage_axes(g, a, reinterpret_cast<uint64_t*>(smem), &Bs, &Ms, &Ns, &Ks, true);
   __syncthreads();
-  const int R = t.n_exact;
-  struct Hit {
-    int64_t ib, im, jn, ik;
+  if (!mine) return;
+  const int64_t ib = find_sorted(Bs, g.b_hi - g.b_lo, c4[0]);
+  const int64_t im = ib < 0 ? -1 : find_sorted(Ms, g.nM, c4[1]);
+  const int64_t jn = im < 0 ? -1 : find_sorted(Ns, g.nN, c4[2]);
+  const int64_t ik = jn < 0 ? -1 : find_sorted(Ks, g.nK, c4[3]);
+  const bool on = ik >= 0;
+  const int32_t ci = t.ex_mn_curve[r];
+  const_cast<FixEntry*>(g.fixr)[r] = FixEntry{on ? int32_t(ik) : -1, on ? int32_t(ib) : -1, ci, r};
+  const_cast<int64_t*>(g.fix_pos)[r] = on ? ((ib * g.nM + im) * g.nN + jn) * g.nK + ik : -1;
+}
+
+__device__ void plan_rows_rng(const TablesDev& t, const GridDev& g, const PlanArgs& a, int blk,
+                              uint8_t* smem) {
+  const uint64_t *Bs, *Ms, *Ns, *Ks;
+  stage_axes(g, a, reinterpret_cast<uint64_t*>(smem), &Bs, &Ms, &Ns, &Ks, false);
+  // the records' (m, n) keys, for the range searches
+  uint64_t* km = reinterpret_cast<uint64_t*>(smem) + (a.stage_axes ? g.nM + g.nN : 0);
+  const int R = t.n_mn;
+  const bool stage_keys = a.stage_keys != 0;
+  if (stage_keys)
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+      km[2 * i] = t.ex_mn_coord[4 * int64_t(i) + 1];
+      km[2 * i + 1] = t.ex_mn_coord[4 * int64_t(i) + 2];
+    }
+  __syncthreads();
+  const int64_t row = int64_t(blk) * kPlanThreads + threadIdx.x;
+  if (row >= g.nM * g.nN) return;
+  const int64_t im = row / g.nN, jn = row - im * g.nN;
+  const uint64_t m = Ms[im], n = Ns[jn];
+  auto key_less = [&](int i, uint64_t qm, uint64_t qn, bool upper) {
+    const uint64_t rm = stage_keys ? km[2 * i] : t.ex_mn_coord[4 * int64_t(i) + 1];
+    const uint64_t rn = stage_keys ? km[2 * i + 1] : t.ex_mn_coord[4 * int64_t(i) + 2];
+    return upper ? (rm < qm || (rm == qm && rn <= qn)) : (rm < qm || (rm == qm && rn < qn));
   };
-  auto locate = [&](int r) -> Hit {
-    const uint64_t* c4 = t.ex_coord + 4 * int64_t(r);
-    Hit h;
-    h.ib = find_sorted(Bs, nbs, c4[0]);
-    h.im = h.ib < 0 ? -1 : find_sorted(Ms, g.nM, c4[1]);
-    h.jn = h.im < 0 ? -1 : find_sorted(Ns, g.nN, c4[2]);
-    h.ik = h.jn < 0 ? -1 : find_sorted(Ks, g.nK, c4[3]);
-    return h;
-  };
-  for (int r = threadIdx.x; r < R; r += blockDim.x) {
-    const Hit h = locate(r);
-    if (h.ik >= 0) atomicAdd(&cnt[h.im * g.nN + h.jn], 1);
+  int lo = 0, hi = R;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (key_less(mid, m, n, false)) lo = mid + 1; else hi = mid;
   }
-  __syncthreads();
-  // exclusive scan of the row counts -> fixr_off[0..rows] (one contiguous
-  // segment per thread, then a block scan of the segment sums)
-  __shared__ int32_t part[kPlanThreads];
-  const int64_t n = rows + 1;
-  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
-  const int64_t s0 = ::min((int64_t)n, threadIdx.x * per), s1 = ::min((int64_t)n, s0 + per);
-  int32_t sum = 0;
-  for (int64_t i = s0; i < s1; ++i) sum += cnt[i];
-  part[threadIdx.x] = sum;
-  __syncthreads();
-  for (int off = 1; off < int(blockDim.x); off <<= 1) {
-    const int32_t v = threadIdx.x >= unsigned(off) ? part[threadIdx.x - off] : 0;
-    __syncthreads();
-    part[threadIdx.x] += v;
-    __syncthreads();
+  int lo2 = lo, hi2 = R;
+  while (lo2 < hi2) {
+    const int mid = (lo2 + hi2) >> 1;
+    if (key_less(mid, m, n, true)) lo2 = mid + 1; else hi2 = mid;
   }
-  int32_t run = part[threadIdx.x] - sum;  // exclusive prefix of this segment
-  int32_t* fixr_off = const_cast<int32_t*>(g.fixr_off);
-  for (int64_t i = s0; i < s1; ++i) {
-    const int32_t c = cnt[i];
-    cnt[i] = run;  // becomes the scatter cursor
-    fixr_off[i] = run;
-    run += c;
-  }
-  if (threadIdx.x == blockDim.x - 1) *const_cast<int32_t*>(g.n_fix_dev) = part[blockDim.x - 1];
-  __syncthreads();
-  FixEntry* fixr = const_cast<FixEntry*>(g.fixr);
-  int64_t* fix_pos = const_cast<int64_t*>(g.fix_pos);
-  uint64_t* fix_coord = const_cast<uint64_t*>(g.fix_coord);
-  int32_t* fix_curve = const_cast<int32_t*>(g.fix_curve);
-  for (int r = threadIdx.x; r < R; r += blockDim.x) {
-    const Hit h = locate(r);
-    if (h.ik < 0) continue;
-    const int64_t row = h.im * g.nN + h.jn;
-    const int slot = atomicAdd(&cnt[row], 1);
-    const int32_t ci = t.ex_curve[r];
-    fixr[slot] = FixEntry{int32_t(h.ik), int32_t(h.ib), ci, slot};
-    fix_pos[slot] = ((h.ib * g.nM + h.im) * g.nN + h.jn) * g.nK + h.ik;
-    const uint64_t* c4 = t.ex_coord + 4 * int64_t(r);
-    for (int j = 0; j < 4; ++j) fix_coord[4 * int64_t(slot) + j] = c4[j];
-    fix_curve[slot] = ci;
-  }
+  const_cast<int2*>(g.fixr_rng)[row] = make_int2(lo, lo2);
 }
 
 // ---------------------------------------------------- m / n axes, W inputs
@@ -260,21 +301,6 @@ __device__ void plan_mn(const TablesDev& t, const GridDev& g, const PlanArgs& a)
       if (v == 0 || int64_t(v) >= a.lut_n || v >= (uint64_t(1) << 62)) flag(g.status, kPlanBadValue);
       if (i > 0 && !(V[i - 1] < v)) flag(g.status, kPlanUnsorted);
       L[i] = (v >= 1 && int64_t(v) < a.lut_n) ? a.lut[v] : 0.0;
-    }
-  }
-  if (g.cm_tab) {
-    // ceil(m / tile_m) and ceil(n / tile_n) * split_k per wave class, in u64
-    // exactly like the host planner (and the reference's block product)
-    uint64_t* cm = const_cast<uint64_t*>(g.cm_tab);
-    uint64_t* cn = const_cast<uint64_t*>(g.cn_tab);
-    const int NW = t.NW;
-    for (int64_t e = threadIdx.x; e < g.nM * NW; e += blockDim.x) {
-      const WcParam& p = t.wcp[e % NW];
-      cm[e] = (g.M[e / NW] + p.tm - 1) / p.tm;
-    }
-    for (int64_t e = threadIdx.x; e < g.nN * NW; e += blockDim.x) {
-      const WcParam& p = t.wcp[e % NW];
-      cn[e] = ((g.N[e / NW] + p.tn - 1) / p.tn) * p.sk;
     }
   }
 }
@@ -309,16 +335,31 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(TablesDev t, GridDev
   pdl_release();  // the grid kernel may launch and run its table prologue now
   extern __shared__ __align__(16) uint8_t smem[];
   const int b = blockIdx.x;
-  if (b < a.nkc) plan_k_chunk(t, g, a, b, smem);
-  else if (b == a.nkc) plan_join(t, g, a, smem);
-  else if (b == a.nkc + 1) plan_mn(t, g, a);
-  else plan_base(t, g, a, b - a.nkc - 2);
+#ifdef PM2L_TIMING
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
+  const int nk = a.nkc * a.kparts;
+  if (b < nk) plan_k_rank(t, g, a, b / a.kparts, b % a.kparts, smem);
+  else if (b < nk + a.nrec) plan_records(t, g, a, b - nk, smem);
+  else if (b < nk + a.nrec + a.nrow) plan_rows_rng(t, g, a, b - nk - a.nrec, smem);
+  else if (b == nk + a.nrec + a.nrow) plan_mn(t, g, a);
+  else plan_base(t, g, a, b - nk - a.nrec - a.nrow - 1);
+#ifdef PM2L_TIMING
+  __syncthreads();
+  if (threadIdx.x == 0 && b < 1024) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    a.dbg[8 * b] = t0;
+    a.dbg[8 * b + 7] = t1;
+  }
+#endif
 }
 
 // Plan buffer layout (256-byte aligned sections).
 struct Layout {
-  int64_t B, M, N, K, logM, logN, logK, kinfo, kfast, mn_sorted, kright, cm, cn, fix_pos,
-      fix_coord, fix_curve, fixr, fixr_off, n_fix, status, total;
+  int64_t B, M, N, K, logM, logN, logK, kinfo, kfast, mn_sorted, kright, fix_pos, fixr,
+      fixr_rng, status, total;
 };
 
 Layout layout(const TablesDev& t, const DPlanCaps& c) {
@@ -329,32 +370,36 @@ Layout layout(const TablesDev& t, const DPlanCaps& c) {
     o = (o + std::max<int64_t>(bytes, 16) + 255) & ~int64_t(255);
     return at;
   };
-  const int64_t nkc = (c.nK + kKChunk - 1) / kKChunk, R = t.n_exact;
+  const int64_t nkc = (c.nK + kKChunk - 1) / kKChunk, R = t.n_mn;
   L.B = take(8 * c.nB); L.M = take(8 * c.nM); L.N = take(8 * c.nN); L.K = take(8 * c.nK);
   L.logM = take(8 * c.nM); L.logN = take(8 * c.nN); L.logK = take(8 * c.nK);
   L.kinfo = take(int64_t(sizeof(KInfo)) * c.nK);
   L.kfast = take(4 * c.nK); L.mn_sorted = take(8 * c.nK); L.kright = take(4 * nkc * t.G);
-  L.cm = take(8 * c.nM * t.NW); L.cn = take(8 * c.nN * t.NW);
-  L.fix_pos = take(8 * R); L.fix_coord = take(32 * R); L.fix_curve = take(4 * R);
+  L.fix_pos = take(8 * R);
   L.fixr = take(int64_t(sizeof(FixEntry)) * R);
-  L.fixr_off = take(4 * (c.nM * c.nN + 1));
-  L.n_fix = take(4); L.status = take(4);
+  L.fixr_rng = take(8 * c.nM * c.nN);
+  L.status = take(4);
   L.total = o + 256;
   return L;
 }
 
-int64_t join_smem(const GridDev& g, bool stage) {
-  const int64_t rows = g.nM * g.nN;
-  int64_t s = (4 * (rows + 1) + 15) & ~int64_t(15);
-  if (stage) s += 8 * ((g.b_hi - g.b_lo) + g.nM + g.nN + g.nK);
-  return s;
-}
+constexpr int64_t kStageAxesBytes = 64 * 1024;
+constexpr int64_t kStageKeysBytes = 48 * 1024;
 
 }  // namespace
 
+#ifdef PM2L_TIMING
+unsigned long long*& plan_timing_buffer() {
+  static unsigned long long* p = nullptr;
+  return p;
+}
+#endif
+
 bool dplan_supported(const TablesDev& t, const DPlanCaps& c) {
-  return t.G >= 0 && t.G <= 255 && c.nK >= 1 && c.nK <= 65535 && c.nM * c.nN + 1 <= kMaxJoinRows &&
-         t.n_exact <= kMaxJoinRecords && c.nM >= 1 && c.nN >= 1 && c.nB >= 1;
+  // G < 256 and k chunks of kKChunk: the kfast packing; rows and axes fit
+  // 31-bit launch indices
+  return t.G >= 0 && t.G <= 255 && c.nK >= 1 && c.nK <= 65535 && c.nM >= 1 && c.nN >= 1 &&
+         c.nB >= 1 && c.nM * c.nN <= (int64_t(1) << 30) && c.nB <= (int64_t(1) << 30);
 }
 
 int64_t dplan_bytes(const TablesDev& t, const DPlanCaps& c) { return layout(t, c).total; }
@@ -384,40 +429,48 @@ GridDev dplan_grid(const TablesDev& t, const DPlanCaps& c, void* buf, const uint
   g.kfast = reinterpret_cast<const uint32_t*>(p + L.kfast);
   g.mn_sorted = reinterpret_cast<const uint64_t*>(p + L.mn_sorted);
   g.kright = reinterpret_cast<const int32_t*>(p + L.kright);
-  if (t.all_gemm && t.NW > 0) {
-    g.cm_tab = reinterpret_cast<const uint64_t*>(p + L.cm);
-    g.cn_tab = reinterpret_cast<const uint64_t*>(p + L.cn);
-  }
-  g.n_fix = t.n_exact;  // capacity; the planned count is n_fix_dev
+  // one fix-up entry per unique exact record (ib == -1, fix_pos == -1 when
+  // it is off the slice); coordinates and curves are the tables' own
+  g.n_fix = t.n_mn;
   g.fix_pos = reinterpret_cast<const int64_t*>(p + L.fix_pos);
-  g.fix_coord = reinterpret_cast<const uint64_t*>(p + L.fix_coord);
-  g.fix_curve = reinterpret_cast<const int32_t*>(p + L.fix_curve);
-  g.fixr_off = reinterpret_cast<const int32_t*>(p + L.fixr_off);
+  g.fix_coord = t.ex_mn_coord;
+  g.fix_curve = t.ex_mn_curve;
   g.fixr = reinterpret_cast<const FixEntry*>(p + L.fixr);
-  g.max_fix_row = t.n_exact;
+  g.fixr_rng = reinterpret_cast<const int2*>(p + L.fixr_rng);
+  g.max_fix_row = t.n_mn;
   g.k_sorted = 1;  // canonical axes (a violation is reported in status)
   g.dev_planned = 1;
-  g.n_fix_dev = reinterpret_cast<const int32_t*>(p + L.n_fix);
   g.status = reinterpret_cast<uint32_t*>(p + L.status);
   return g;
 }
 
 int launch_dplan(const TablesDev& t, const GridDev& g, double* base,
                  unsigned long long* nan_stats, void* stream) {
-  const double* lut = g.lut;
-  const int64_t lut_n = g.lut_n;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PlanArgs a{};
   a.nkc = int((g.nK + kKChunk - 1) / kKChunk);
+  a.kparts = int((std::min<int64_t>(g.nK, kKChunk) + kRankPerCta - 1) / kRankPerCta);
+  a.nrec = (t.n_mn + kPlanThreads - 1) / kPlanThreads;
+  a.nrow = int((g.nM * g.nN + kPlanThreads - 1) / kPlanThreads);
   a.kblocks = int((g.nK + kBaseBlock - 1) / kBaseBlock);
-  a.lut = lut;
-  a.lut_n = lut_n;
+  a.lut = g.lut;
+  a.lut_n = g.lut_n;
   a.base = base;
   a.stats = nan_stats;
-  const int64_t chunk_smem = 8 * kKChunk + 8 * 256 + 2 * kKChunk + 2 * kKChunk;
-  a.stage_axes = join_smem(g, true) <= kJoinStageBytes + 4 * (g.nM * g.nN + 1) ? 1 : 0;
-  const int64_t smem = std::max(chunk_smem, join_smem(g, a.stage_axes != 0));
-  const int blocks = a.nkc + 2 + t.C * a.kblocks;
+#ifdef PM2L_TIMING
+  static unsigned long long* dbg = nullptr;
+  if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 8192);
+  a.dbg = dbg;
+  plan_timing_buffer() = dbg;
+#endif
+  const int64_t axes_bytes = 8 * ((g.b_hi - g.b_lo) + g.nM + g.nN + g.nK);
+  a.stage_axes = axes_bytes <= kStageAxesBytes ? 1 : 0;
+  a.stage_keys = 16ll * t.n_mn <= kStageKeysBytes ? 1 : 0;
+  const int64_t rank_smem = 8 * kKChunk + 8 * 256 + 2 * kKChunk;
+  const int64_t rec_smem = a.stage_axes ? axes_bytes : 0;
+  const int64_t row_smem = (a.stage_axes ? 8 * (g.nM + g.nN) : 0) + (a.stage_keys ? 16ll * t.n_mn : 0);
+  const int64_t smem = std::max(rank_smem, std::max(rec_smem, row_smem));
+  const int blocks = a.nkc * a.kparts + a.nrec + a.nrow + 1 + t.C * a.kblocks;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));

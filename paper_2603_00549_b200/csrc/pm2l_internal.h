@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include <vector_types.h>
+
 #include "../../include/pm2l.h"
 #include <string>
 #include <vector>
@@ -86,6 +88,10 @@ struct TablesDev {
   const uint64_t* ex_coord = nullptr; // 4 per record
   const int32_t* ex_curve = nullptr;
   const int32_t* ex_rec = nullptr;    // position in the caller's exact arrays
+  // the same records, unique, sorted by (m, n, b, k) (device planner)
+  int32_t n_mn = 0;
+  const uint64_t* ex_mn_coord = nullptr;  // 4 per record
+  const int32_t* ex_mn_curve = nullptr;
 };
 
 // k chunk of the one-class lookup kernel: ranks of the per-k distance are
@@ -135,9 +141,6 @@ struct GridDev {
   const uint64_t* mn_sorted = nullptr;
   // [chunks x G]: first chunk-local k index with start(ik) > g
   const int32_t* kright = nullptr;
-  // all-GEMM tables: [nM x NW] ceil(m / tile_m), [nN x NW] ceil(n / tile_n) * split_k
-  const uint64_t* cm_tab = nullptr;
-  const uint64_t* cn_tab = nullptr;
   // exact-hit fix-ups: slice-relative flat index + coordinates + curve
   int64_t n_fix = 0;
   const int64_t* fix_pos = nullptr;
@@ -151,10 +154,14 @@ struct GridDev {
   int32_t k_sorted = 0;  // k axis strictly ascending (lookup kernel precondition)
   // device-planned slices (plan.cu): every array above is written on the GPU
   // by plan_kernel, in the same stream as the grid kernel.  n_fix is then the
-  // capacity (the triple's exact records) and n_fix_dev the planned count;
-  // status collects axis violations (kPlanBad*), 0 for a valid plan.
+  // triple's unique exact records, one fix-up entry each (fix_pos == -1 and
+  // ib == -1 for records off the slice); status collects axis violations
+  // (kPlanBad*), 0 for a valid plan.
   int32_t dev_planned = 0;
-  const int32_t* n_fix_dev = nullptr;
+  // device plans: per (m, n) row the [lo, hi) range of its records in the
+  // fix-up list (entries of records off the slice have ib == -1 and
+  // fix_pos == -1); null for host plans (fixr_off)
+  const int2* fixr_rng = nullptr;
   uint32_t* status = nullptr;
   const double* lut = nullptr;  // per-device libm log2 table of [0, lut_n)
   int64_t lut_n = 0;
@@ -223,6 +230,7 @@ int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g);
 int grid_kernel_path(const TablesDev& t, const GridDev& g, const LaunchOut& out);
 #ifdef PM2L_TIMING
 int row_timing_copy(unsigned long long* host, int n);  // diagnostic build only
+unsigned long long*& plan_timing_buffer();              // plan.cu: per-CTA entry/exit
 #endif
 int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* workspace,
                            double* out, void* stream);

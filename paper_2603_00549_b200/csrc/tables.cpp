@@ -175,6 +175,27 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
     ex_curve[i] = int32_t(int64_t(ex[i][4]));
     ex_rec[i] = int32_t(ex[i][5]);
   }
+  // two exact records of one shape naming different kernels are the
+  // reference resolver's AmbiguousConfig (compute.py:227-234); the same
+  // kernel twice is kept once in the device planner's copy below
+  for (int64_t i = 1; i < R; ++i)
+    if (std::equal(ex[i].begin(), ex[i].begin() + 4, ex[i - 1].begin()) && ex[i][4] != ex[i - 1][4])
+      return "ambiguous exact records: one shape, two kernels";
+  // the device planner's copy: unique shapes sorted by (m, n, b, k), so the
+  // records of one (m, n) row are one contiguous range
+  std::vector<std::array<uint64_t, 6>> exm;
+  for (int64_t i = 0; i < R; ++i)
+    if (i == 0 || !std::equal(ex[i].begin(), ex[i].begin() + 4, ex[i - 1].begin())) exm.push_back(ex[i]);
+  std::stable_sort(exm.begin(), exm.end(), [](const auto& a, const auto& b) {
+    const std::array<uint64_t, 4> ka = {a[1], a[2], a[0], a[3]}, kb = {b[1], b[2], b[0], b[3]};
+    return ka < kb;
+  });
+  std::vector<uint64_t> exm_coord(4 * exm.size());
+  std::vector<int32_t> exm_curve(exm.size());
+  for (size_t i = 0; i < exm.size(); ++i) {
+    for (int j = 0; j < 4; ++j) exm_coord[4 * i + j] = exm[i][j];
+    exm_curve[i] = int32_t(int64_t(exm[i][4]));
+  }
 
   // u32 division magic (Granlund & Montgomery, PLDI'94, fig. 4.1): for every
   // 32-bit n, n / d == (t + ((n - t) >> sh1)) >> sh2 with t = umulhi(m, n)
@@ -294,6 +315,9 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.ex_coord = blob.add(ex_coord);
   t.ex_curve = blob.add(ex_curve);
   t.ex_rec = blob.add(ex_rec);
+  t.n_mn = int32_t(exm.size());
+  t.ex_mn_coord = blob.add(exm_coord);
+  t.ex_mn_curve = blob.add(exm_curve);
   out->blob.swap(blob.bytes());
   out->max_group = max_group;
   return "";
@@ -319,6 +343,8 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.cls_lm = shift(o.cls_lm, base); t.cls_ln = shift(o.cls_ln, base);
   t.ex_coord = shift(o.ex_coord, base); t.ex_curve = shift(o.ex_curve, base);
   t.ex_rec = shift(o.ex_rec, base);
+  t.ex_mn_coord = shift(o.ex_mn_coord, base);
+  t.ex_mn_curve = shift(o.ex_mn_curve, base);
   return t;
 }
 
@@ -351,22 +377,6 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   // group attaining it (gB), and rank(k) in the stable descending order of
   // mn.  A row's cut points are thresholds on that order.  Same IEEE
   // subtraction and |.| as the device (host double, no contraction).
-  // per (m value, wave class): ceil(m / tile_m); per (n value, wave class):
-  // ceil(n / tile_n) * split_k -- the row kernel's W table inputs (u64,
-  // wrapping exactly like the reference's block product, _kernels.pyx:126)
-  std::vector<uint64_t> cm_tab, cn_tab;
-  if (tt.all_gemm && tt.NW > 0) {
-    const WcParam* wcp = reinterpret_cast<const WcParam*>(
-        th.blob.data() + reinterpret_cast<uintptr_t>(tt.wcp));
-    cm_tab.resize(size_t(nM) * tt.NW);
-    cn_tab.resize(size_t(nN) * tt.NW);
-    for (int64_t i = 0; i < nM; ++i)
-      for (int w = 0; w < tt.NW; ++w)
-        cm_tab[i * tt.NW + w] = (axes[1][i] + wcp[w].tm - 1) / wcp[w].tm;
-    for (int64_t j = 0; j < nN; ++j)
-      for (int w = 0; w < tt.NW; ++w)
-        cn_tab[j * tt.NW + w] = ((axes[2][j] + wcp[w].tn - 1) / wcp[w].tn) * wcp[w].sk;
-  }
   std::vector<uint32_t> kfast;
   std::vector<uint64_t> mn_sorted;
   std::vector<int32_t> kright;
@@ -497,8 +507,6 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   g.kfast = fast_ok ? blob.add(kfast) : nullptr;
   g.mn_sorted = fast_ok ? blob.add(mn_sorted) : nullptr;
   g.kright = fast_ok ? blob.add(kright) : nullptr;
-  g.cm_tab = cm_tab.empty() ? nullptr : blob.add(cm_tab);
-  g.cn_tab = cn_tab.empty() ? nullptr : blob.add(cn_tab);
   g.n_fix = int64_t(fix_pos.size());
   g.fix_pos = blob.add(fix_pos);
   g.fix_coord = blob.add(fix_coord);
@@ -522,10 +530,6 @@ GridDev rebase(const GridDev& o, const void* base) {
     g.kfast = shift(o.kfast, base);
     g.mn_sorted = shift(o.mn_sorted, base);
     g.kright = shift(o.kright, base);
-  }
-  if (o.cm_tab) {
-    g.cm_tab = shift(o.cm_tab, base);
-    g.cn_tab = shift(o.cn_tab, base);
   }
   g.fix_pos = shift(o.fix_pos, base);
   g.fix_coord = shift(o.fix_coord, base); g.fix_curve = shift(o.fix_curve, base);
