@@ -288,7 +288,7 @@ unsigned long long** timing_buffers() {
 // Launch-shape overrides for tuning experiments (tools/ab_*.sh), read once
 // per process -- never on the launch path.  PM2L_DEBUG_PLAN prints the plan.
 struct Tuning {
-  int nb = 0, prod = 0, slots = 0, ctas = 0;
+  int nb = 0, prod = 0, slots = 0, ctas = 0, direct = -1;
   bool debug = false;
 };
 const Tuning& tuning() {
@@ -302,6 +302,7 @@ const Tuning& tuning() {
     t.prod = geti("PM2L_RING_PROD");
     t.slots = geti("PM2L_RING_SLOTS");
     t.ctas = geti("PM2L_ROW_CTAS");
+    if (const char* e = std::getenv("PM2L_ROW_DIRECT")) t.direct = std::atoi(e);
     t.debug = std::getenv("PM2L_DEBUG_PLAN") != nullptr;
     return t;
   }();
@@ -349,6 +350,11 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
   rl.d_nbs = fast_div_for(uint32_t(rl.nbs));
   rl.d_nN = fast_div_for(uint32_t(g.nN));
   const bool stage_k = g.nK <= kKChunk;
+  // rank/group byte maps per tile (GEMM grids: many rows share the k
+  // ranks, a map serves NB batch values) or the per-k closed-form resolve
+  // (row-block grids: one (m, n) row and a long k axis, where the planner's
+  // k ranks would dominate a plan-inclusive launch)
+  rl.direct = tu.direct >= 0 ? (tu.direct != 0) : (t.all_rowblock ? 1 : 0);
   rl.prod = tu.prod > 0 ? std::min(tu.prod, kRowWarps - 1) : kRingProd;
   rl.slots = tu.slots > 0 ? std::min(tu.slots, kRingMaxSlots) : kRingSlots;
   const int64_t tiles = g.nM * g.nN * rl.nbs * rl.nkc;
@@ -410,17 +416,19 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   // the same launch sequence (stage masks that skip it, and device-planned
   // slices, recompute them in fixup_kernel)
   double* fixval = (g.n_fix > 0 && (stages & kStageBase) && !g.dev_planned) ? ws + nbase : nullptr;
+  int row_nb = 0;
+  const RowLaunch rl = plan_rows(t, g, gl, out, &row_nb);
   if (stages & kStageBase) {
     if (g.dev_planned) {
-      if (const int rc = launch_dplan(t, g, ws, out.nan_stats, s)) return rc;
+      // the k ranks only feed the lookup kernel's byte maps
+      const bool ranks = rl.tiles > 0 && !rl.direct;
+      if (const int rc = launch_dplan(t, g, ws, out.nan_stats, ranks, s)) return rc;
     } else {
       launch_base_table(t, g, ws, fixval, out.nan_stats, s);
     }
   }
   const bool v = out.curve != nullptr;
   cudaError_t e = cudaSuccess;
-  int row_nb = 0;
-  const RowLaunch rl = plan_rows(t, g, gl, out, &row_nb);
   if ((stages & kStageGrid) && rl.tiles > 0) {
     e = row_nb == 8   ? launch_rows_t<8>(t, g, rl, base, out, s)
         : row_nb == 4 ? launch_rows_t<4>(t, g, rl, base, out, s)

@@ -73,8 +73,10 @@ struct RowLaunch {
   int pair;                  // 16-byte pair stores (even k axis, aligned output)
   int rowblock;              // row-block tables: per-point wave scale (ring kernel, pairs)
   int prod, slots;           // ring: builder warps, tile-state slots
+  int direct;                // per-k closed-form resolve (no byte maps, no k ranks)
   int ctas;
-  int off_bar, off_gcur, off_glk, off_clm, off_cln, off_wcp, off_kf, off_ms, off_kq, off_kr, off_warp;
+  int off_bar, off_gcur, off_glk, off_clm, off_cln, off_wcp, off_kf, off_ms, off_kq, off_kr, off_ki,
+      off_warp;
   int w_hdr, w_sD, w_sP, w_cut, w_W, w_rmap, w_gmap, warp_bytes;
   int64_t smem;
 #ifdef PM2L_TIMING
@@ -97,10 +99,12 @@ inline void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_
   rl.off_cln = take(8ll * t.CM);
   rl.off_wcp = take(int64_t(sizeof(WcParam)) * t.NW);
   rl.seg = int(kmap_lane_bytes(g.nK));
-  rl.off_kf = take(stage_k ? 4ll * g.nK : 0);
-  rl.off_ms = take(stage_k ? 8ll * g.nK : 0);
-  rl.off_kq = take(stage_k ? 8ll * g.nK : 0);
-  rl.off_kr = take(stage_k ? 4ll * rl.nkc * t.G : 0);
+  const bool maps = !rl.direct;
+  rl.off_kf = take(stage_k && maps ? 4ll * g.nK : 0);
+  rl.off_ms = take(stage_k && maps ? 8ll * g.nK : 0);
+  rl.off_kq = take(stage_k && maps ? 8ll * g.nK : 0);
+  rl.off_kr = take(stage_k && maps ? 4ll * rl.nkc * t.G : 0);
+  rl.off_ki = take(stage_k && !maps ? int64_t(sizeof(KInfo)) * g.nK : 0);
   rl.off_warp = int(o);
   int64_t w = 0;
   auto wtake = [&](int64_t bytes) {
@@ -111,10 +115,10 @@ inline void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_
   rl.w_hdr = wtake(16);
   rl.w_sD = wtake(8ll * t.CM);
   rl.w_sP = wtake(4ll * t.CM);
-  rl.w_cut = wtake(4ll * (t.CM + t.G + 1));
+  rl.w_cut = wtake(maps ? 4ll * (t.CM + t.G + 1) : 0);
   rl.w_W = wtake(8ll * t.NW * nb);
-  rl.w_rmap = wtake(32ll * rl.seg);
-  rl.w_gmap = wtake(32ll * rl.seg);
+  rl.w_rmap = wtake(maps ? 32ll * rl.seg : 0);
+  rl.w_gmap = wtake(maps ? 32ll * rl.seg : 0);
   rl.warp_bytes = int(w);
   rl.smem = o + int64_t(rl.slots) * w;
 }

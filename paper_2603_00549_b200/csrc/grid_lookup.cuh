@@ -133,6 +133,7 @@ struct RowCtx {
   const uint64_t* ms;    // per-k tables (shared when STAGE)
   const double* kq;
   const int32_t* krt;    // [chunk x G] kright
+  const KInfo* ki;       // direct resolve: {log2 k, k-group insertion point} per k
   uint32_t ms_s, kq_s;   // shared addresses of ms / kq (STAGE)
   int G, CM, NW, nK;
   int64_t plane;
@@ -151,6 +152,7 @@ __device__ __forceinline__ RowCtx<STAGE> row_ctx(uint8_t* smem, const TablesDev&
   c.ms = STAGE ? reinterpret_cast<const uint64_t*>(smem + rl.off_ms) : g.mn_sorted;
   c.kq = STAGE ? reinterpret_cast<const double*>(smem + rl.off_kq) : g.logK;
   c.krt = STAGE ? reinterpret_cast<const int32_t*>(smem + rl.off_kr) : g.kright;
+  c.ki = STAGE ? reinterpret_cast<const KInfo*>(smem + rl.off_ki) : g.kinfo;
   c.ms_s = smem_u32(smem + rl.off_ms);
   c.kq_s = smem_u32(smem + rl.off_kq);
   c.G = t.G; c.CM = t.CM; c.NW = t.NW; c.nK = int(g.nK);
@@ -179,6 +181,11 @@ __device__ __forceinline__ void row_prologue(uint8_t* smem, const RowCtx<STAGE>&
 template <bool STAGE>
 __device__ __forceinline__ void row_prologue_k(uint8_t* smem, const RowCtx<STAGE>& c,
                                                const GridDev& g, const RowLaunch& rl, uint64_t* bar) {
+  if (rl.direct) {
+    mbar_expect_tx(bar + 1, r16(int64_t(sizeof(KInfo)) * c.nK));
+    bulk_g2s(smem + rl.off_ki, g.kinfo, r16(int64_t(sizeof(KInfo)) * c.nK), bar + 1);
+    return;
+  }
   mbar_expect_tx(bar + 1, r16(4ll * c.nK) + 2 * r16(8ll * c.nK) + r16(4ll * rl.nkc * c.G));
   bulk_g2s(smem + rl.off_ms, g.mn_sorted, r16(8ll * c.nK), bar + 1);
   bulk_g2s(smem + rl.off_kq, g.logK, r16(8ll * c.nK), bar + 1);
@@ -311,6 +318,16 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
       if (lane == ib) W[ib] = __longlong_as_double(static_cast<long long>(cur.b[ib]));
   }
   __syncwarp();
+  if (rl.direct) {
+    // per-k closed form at emission: the tile state is the staircase, its
+    // minimum and first minimiser, and the W table
+    if (lane == 0) {
+      hdr[0] = len;
+      hdr[1] = lastpos;
+      *reinterpret_cast<uint64_t*>(hdr + 2) = dmin;
+    }
+    return;
+  }
   if (plan_wait) pdl_wait();
   if (STAGE && k_ready) mbar_wait(k_ready, 0);
   ROW_MARK(mark_tile, 6);
@@ -511,6 +528,38 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
     const int pos = a ? lastpos : sP[sb];
     return c.gcur[gg * CM + pos];  // one class: group g's members at g * CM
   };
+  // direct: nearest_one_class (grid_sweep.cu) per k from {log2 k, insertion
+  // point}: the nearest k-groups' distance mn decides case A (mn <= dmin:
+  // leftmost group within dmin, member lastpos) or case B (leftmost group
+  // at mn, member = first staircase step <= mn); same comparisons, same bits
+  const uint64_t* sD = reinterpret_cast<const uint64_t*>(wb + rl.w_sD);
+  const uint64_t dmin = *reinterpret_cast<const uint64_t*>(hdr + 2);
+  const int len = hdr[0];
+  int top = 1;
+  while (top * 2 <= len) top *= 2;
+  auto resolve = [&](const KInfo& q) -> int2 {
+    const double qk = q.qk;
+    const int start = q.start, G = c.G;
+    auto dk = [&](int gg) { return abs_bits(__dsub_rn(c.glk[gg], qk)); };
+    const uint64_t dkL = start > 0 ? dk(start - 1) : ~0ull;
+    const uint64_t dkR = start < G ? dk(start) : ~0ull;
+    const uint64_t mn = dkL < dkR ? dkL : dkR;
+    const bool case_a = mn <= dmin;
+    const uint64_t lim = case_a ? dmin : mn;  // walk left while within it (A) / tied (B)
+    int gg = start;
+    if (case_a ? dkL <= dmin : dkL == mn) {
+      gg = start - 1;
+      while (gg > 0 && (case_a ? dk(gg - 1) <= lim : dk(gg - 1) == lim)) --gg;
+    }
+    int pos = lastpos;
+    if (!case_a) {  // #{steps with sD > mn} (sD strictly descends; sD[len-1] = dmin < mn)
+      int s = 0;
+      for (int step = top; step; step >>= 1)
+        if (s + step <= len && sD[s + step - 1] > mn) s += step;
+      pos = sP[s];
+    }
+    return c.gcur[gg * CM + pos];
+  };
   constexpr int U = 4;
   for (int bq = b0; bq < nB; bq += U * bstep) {  // warp-uniform trip count (__all_sync)
     int2 v[U][2];
@@ -519,9 +568,14 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
     for (int u = 0; u < U; ++u) {
       pp[u] = (bq + u * bstep) * 32 + lane;
       const int p = min(pp[u], nP - 1);
-      const uint2 kf = *reinterpret_cast<const uint2*>(c.kfs + k0 + 2 * p);
-      v[u][0] = lookup(kf.x, 2 * p);
-      v[u][1] = has_second(p) ? lookup(kf.y, 2 * p + 1) : v[u][0];
+      if (rl.direct) {
+        v[u][0] = resolve(c.ki[k0 + 2 * p]);
+        v[u][1] = has_second(p) ? resolve(c.ki[k0 + 2 * p + 1]) : v[u][0];
+      } else {
+        const uint2 kf = *reinterpret_cast<const uint2*>(c.kfs + k0 + 2 * p);
+        v[u][0] = lookup(kf.x, 2 * p);
+        v[u][1] = has_second(p) ? lookup(kf.y, 2 * p + 1) : v[u][0];
+      }
     }
     bool all_ok = true;
 #pragma unroll
@@ -740,7 +794,8 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       const bool first = j < P;
       build_tile<NB, STAGE, SEGW, RB>(c, g, rl, tile_xy(rl, tile, c.nK), cur,
                                   smem + rl.off_warp + slot * rl.warp_bytes, lane, tile,
-                                  /*with_w=*/j >= nhelp, j < nhelp ? sready + j : nullptr,
+                                  /*with_w=*/j >= nhelp,
+                                  j < nhelp && !rl.direct ? sready + j : nullptr,
                                   first ? bar + 1 : nullptr, first && g.dev_planned);
       __syncwarp();
       ROW_MARK(tile, 2);
@@ -761,7 +816,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
         pdl_wait();  // the planner kernel's per-k tables are complete and visible
         if (STAGE && cw == 0 && lane == 0) row_prologue_k<STAGE>(smem, c, g, rl, bar);
       }
-      if (tile0 < rl.tiles) {
+      if (tile0 < rl.tiles && !rl.direct) {
         if (STAGE) mbar_wait(bar + 1, 0);
         mbar_wait(sready + cw, 0);  // the builder's staircase is published
         help_group_map<STAGE, SEGW>(c, g, rl, tile_xy(rl, tile0, c.nK), wb0, lane);

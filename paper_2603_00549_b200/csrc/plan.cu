@@ -68,6 +68,7 @@ __device__ __forceinline__ int64_t find_sorted(const uint64_t* a, int64_t n, uin
 struct PlanArgs {
   int nkc;           // k chunks
   int kparts;        // rank CTAs per k chunk
+  int ranks;         // k ranks / kright needed (lookup kernel's byte maps)
   int nrec;          // record CTAs
   int nrow;          // row-range CTAs
   int kblocks;       // base-table k blocks per curve
@@ -151,6 +152,7 @@ __device__ void plan_k_rank(const TablesDev& t, const GridDev& g, const PlanArgs
       if (ik > 0 && !(g.K[ik - 1] < k)) flag(g.status, kPlanUnsorted);
     }
   }
+  if (!a.ranks) return;  // kinfo / logK only (direct resolve, sweep kernel)
   __syncthreads();
   PLAN_MARK(a, 2);
   const int lane = tid & 31, warp = tid >> 5;
@@ -445,11 +447,12 @@ GridDev dplan_grid(const TablesDev& t, const DPlanCaps& c, void* buf, const uint
 }
 
 int launch_dplan(const TablesDev& t, const GridDev& g, double* base,
-                 unsigned long long* nan_stats, void* stream) {
+                 unsigned long long* nan_stats, bool ranks, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PlanArgs a{};
   a.nkc = int((g.nK + kKChunk - 1) / kKChunk);
-  a.kparts = int((std::min<int64_t>(g.nK, kKChunk) + kRankPerCta - 1) / kRankPerCta);
+  a.kparts = ranks ? int((std::min<int64_t>(g.nK, kKChunk) + kRankPerCta - 1) / kRankPerCta) : 1;
+  a.ranks = ranks ? 1 : 0;
   a.nrec = (t.n_mn + kPlanThreads - 1) / kPlanThreads;
   a.nrow = int((g.nM * g.nN + kPlanThreads - 1) / kPlanThreads);
   a.kblocks = int((g.nK + kBaseBlock - 1) / kBaseBlock);

@@ -186,7 +186,7 @@ struct GridDev dplan_grid(const struct TablesDev& t, const DPlanCaps& c, void* b
 uint64_t* dplan_axis_slot(const struct TablesDev& t, const DPlanCaps& c, void* buf, int axis);
 // plan_kernel: logs, per-k tables, exact-hit join, base table, stats reset.
 int launch_dplan(const struct TablesDev& t, const struct GridDev& g, double* base,
-                 unsigned long long* nan_stats, void* stream);
+                 unsigned long long* nan_stats, bool ranks, void* stream);
 
 // Host-side image of the staged tables (one contiguous byte blob whose
 // internal pointers are rebased onto the device copy).
