@@ -1,0 +1,241 @@
+"""Parity at the benchmarked configurations, at full size.
+
+Every grid here is the one bench.py / tools/bench_modes.py / tools/c5.py
+time, launched whole on the B200 and compared bit for bit against the
+reference's own compiled kernel (oracle/_ref: the unmodified
+_kernels.pyx:76-133, given the reference's np.log2 candidate tables as
+nascache.py:189-191 builds them) over every host core — or, where the
+reference kernel would take minutes, on a seeded >= 1 M-point sub-grid of
+the full launch (sub-grids are exact: a point's result depends only on its
+own coordinates, _kernels.pyx:97-133).  The C oracle covers what the
+reference has no batch kernel for (explicit descriptors, mode X)."""
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import dataset
+
+pytestmark = pytest.mark.gpu
+
+THREADS = max(1, len(os.sched_getaffinity(0)))
+B8 = (1, 2, 4, 8, 16, 32, 64, 128)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def _ref_tables(prep):
+    """PreparedGrid.tables() with the reference's np.log2 candidate logs."""
+    t = dict(prep.tables())
+    recs = prep.records
+    for ax in ("m", "n", "k"):
+        t[f"log_{ax}"] = np.log2(np.array([getattr(r.shape, ax) for r in recs], np.float64))
+    return t
+
+
+def _reference(prep, axes=None):
+    """Reference Cython kernel (all host cores) or, if it was not built, the
+    C oracle threaded the same way."""
+    axes = prep.axis_arrays() if axes is None else axes
+    t = _ref_tables(prep)
+    mod = oracle.reference_kernels()
+    if mod is not None:
+        return oracle.reference_predict_grid_tiles(mod, t, axes, THREADS)
+    B, M, N, K = (np.ascontiguousarray(a, np.uint64) for a in axes)
+    inner = len(M) * len(N) * len(K)
+    out = np.empty(len(B) * inner, np.float64)
+    cuts = np.linspace(0, len(M), min(len(M), THREADS) + 1, dtype=int)
+
+    def run(b, m0, m1):
+        o = oracle.grid(t, (B, M[m0:m1], N, K), b, b + 1, verify=False)
+        out[b * inner + m0 * len(N) * len(K):b * inner + m1 * len(N) * len(K)] = o
+
+    with ThreadPoolExecutor(THREADS) as pool:
+        list(pool.map(lambda a: run(*a), [(b, int(m0), int(m1)) for b in range(len(B))
+                                          for m0, m1 in zip(cuts[:-1], cuts[1:]) if m1 > m0]))
+    return out
+
+
+def _prep(ds_name, family, dtype, tmode, axes):
+    from paper_2603_00549_b200.compute import WaveModel
+    from paper_2603_00549_b200.core import DType, TransposeMode
+    from paper_2603_00549_b200.nascache import GridSpec, PreparedGrid
+    ds = dataset(ds_name)
+    grid = GridSpec(family, DType.parse(dtype), TransposeMode.parse(tmode), axes)
+    return PreparedGrid(ds, grid, WaveModel(ds.device.sm_count))
+
+
+def _c2_axes():
+    return {"batch": (1, 2, 4, 8), "m": tuple(range(64, 64 + 61 * 50, 61)),
+            "n": tuple(range(96, 96 + 53 * 50, 53)), "k": tuple(range(32, 32 + 17 * 1000, 17))}
+
+
+def _sub_index(shape, picks):
+    """Flat indices (canonical order) of the sub-grid picks[a] ⊂ axis a."""
+    grids = np.meshgrid(*[np.asarray(p, np.int64) for p in picks], indexing="ij")
+    return np.ravel_multi_index([g.ravel() for g in grids], shape)
+
+
+def test_c2_full_grid_equals_reference_kernel(gpu):
+    """bench.py's workload, all 10 M points: the device planner path (what
+    the bench times), the host-planned path and the reference FFI drop-in
+    all equal the reference's compiled kernel."""
+    import torch
+    from paper_2603_00549_b200 import _native, backend
+    from conftest import ffi_slice
+    prep = _prep("bf16", "matmul", "bf16", "nn", _c2_axes())
+    ref = _reference(prep)
+    got = backend.predict_grid(prep)
+    assert np.array_equal(_bits(got), _bits(ref))
+    # bench.py's plan-inclusive path: device-resident axes, planner kernel
+    axes = [torch.from_numpy(np.ascontiguousarray(a, np.uint64).view(np.int64)).cuda()
+            for a in prep.axis_arrays()]
+    dp = _native.DeviceGridPlanner(prep.device_tables(0), *(len(a) for a in axes))
+    out = torch.full((prep.grid.cardinality,), -1.0, dtype=torch.float64, device="cuda")
+    dp.launch(axes, out)
+    assert dp.kernel_path() == 3, "C2 must take the lookup kernel"
+    assert np.array_equal(_bits(out.cpu().numpy()), _bits(ref))
+    # the reference's own FFI signature with its own (np.log2) tables
+    t = _ref_tables(prep)
+    B, M, N, K = prep.axis_arrays()
+    ffi = ffi_slice(t, (B, M, N, K), 0, len(B), np.empty(prep.grid.cardinality, np.float64))
+    assert np.array_equal(_bits(ffi), _bits(ref))
+
+
+@pytest.mark.parametrize("family", ["cutlass_attention", "flash_attention"])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_c3_attention_full_grid_equals_reference_kernel(gpu, family, dtype):
+    """C3: 28 B*H batch values x seq 64..65535 (1.83 M points per family),
+    row-block wave model, lookup ring kernel."""
+    bh = sorted({b * h for b in B8 for h in (8, 12, 16, 20, 32, 40, 64)})
+    assert len(bh) == 28
+    prep = _prep("generic_bf16" if dtype == "bf16" else "generic", family, dtype, "nn",
+                 {"batch": tuple(bh), "m": (1,), "n": (1,), "k": tuple(range(64, 65536))})
+    from paper_2603_00549_b200 import backend
+    got = backend.predict_grid(prep)
+    assert np.array_equal(_bits(got), _bits(_reference(prep)))
+    lat, cur, blk, wav = (x.cpu().numpy() for x in backend.predict_grid_device(prep, verify=True))
+    assert np.array_equal(_bits(lat), _bits(got))
+
+
+C5_GEMM = [
+    ("matmul", "nn", 100, 100, 8, 7500),
+    ("linear", "tn", 50, 100, 12, 5000),
+    ("batched_matmul", "nn", 50, 50, 12, 5000),
+]
+
+
+@pytest.mark.parametrize("family,tmode,nm,nn,kstep,nk", C5_GEMM)
+def test_c5_gemm_component_shard0(gpu, family, tmode, nm, nn, kstep, nk):
+    """C5 GEMM components at tools/c5.py's size: rank 0's shard (batch
+    value 1 of 8) launched whole (k chunked by the kernel), checked on a
+    seeded 12 x 12 x all-k sub-grid (>= 0.72 M points) against the
+    reference kernel, plus every point of the shard finite and > 0."""
+    from paper_2603_00549_b200 import backend
+    axes = {"batch": B8, "m": tuple(range(64, 64 + 61 * nm, 61)),
+            "n": tuple(range(96, 96 + 53 * nn, 53)), "k": tuple(range(32, 32 + kstep * nk, kstep))}
+    prep = _prep("bf16", family, "bf16", tmode, axes)
+    lat = backend.predict_grid_device(prep, b_lo=0, b_hi=1)
+    rng = np.random.default_rng(hash(family) % 2**32)
+    mi = np.sort(rng.choice(nm, 12, replace=False))
+    ni = np.sort(rng.choice(nn, 12, replace=False))
+    idx = _sub_index((1, nm, nn, nk), [[0], mi, ni, np.arange(nk)])
+    import torch
+    got = lat[torch.from_numpy(idx).cuda()].cpu().numpy()
+    B, M, N, K = prep.axis_arrays()
+    want = _reference(prep, (B[:1], M[mi], N[ni], K))
+    assert np.array_equal(_bits(got), _bits(want))
+    assert bool(torch.isfinite(lat).all()) and bool((lat > 0).all())
+
+
+@pytest.mark.parametrize("family", ["flash_attention", "cutlass_attention"])
+def test_c5_attention_component_shard0(gpu, family):
+    """C5 attention components: batch' 8..4800 step 8 x seq 64..62563 —
+    rank 0's 75-value slab (4.69 M points) compared whole."""
+    from paper_2603_00549_b200 import backend
+    axes = {"batch": tuple(range(8, 8 + 8 * 600, 8)), "m": (1,), "n": (1,),
+            "k": tuple(range(64, 64 + 62500))}
+    prep = _prep("generic_bf16", family, "bf16", "nn", axes)
+    got = backend.predict_grid_device(prep, b_lo=0, b_hi=75).cpu().numpy()
+    B, M, N, K = prep.axis_arrays()
+    assert np.array_equal(_bits(got), _bits(_reference(prep, (B[:75], M, N, K))))
+
+
+def _c2_shapes(n, seed):
+    axes = _c2_axes()
+    rng = np.random.default_rng(seed)
+    pick = [rng.integers(0, len(axes[a]), n) for a in ("batch", "m", "n", "k")]
+    return np.stack([np.asarray(axes[a], np.uint32)[p]
+                     for a, p in zip(("batch", "m", "n", "k"), pick)], 1)
+
+
+def _oracle_points_threaded(t, shapes):
+    parts = np.array_split(np.arange(len(shapes)), THREADS)
+    with ThreadPoolExecutor(THREADS) as pool:
+        res = list(pool.map(lambda p: oracle.points(t, shapes[p]), parts))
+    return [np.concatenate([r[i] for r in res]) for i in range(6)]
+
+
+def test_points_mode_c2_shapes_match_oracle(gpu):
+    """tools/bench_modes.py 'points': explicit 16-byte descriptors over the
+    C2 shapes (2 M seeded ops, exact + nearest + tile/wave + interpolation)
+    against the oracle's ConfigResolver restatement: latency, curve, waves,
+    match kind, record and distance."""
+    import torch
+    from paper_2603_00549_b200 import _native
+    prep = _prep("bf16", "matmul", "bf16", "nn", _c2_axes())
+    shapes = _c2_shapes(2_000_000, 5)
+    # mix in every recorded shape so exact hits are exercised
+    rec = np.array([r.shape.as_tuple() for r in prep.records], np.uint32)
+    shapes[:len(rec)] = rec
+    n = len(shapes)
+    s = torch.from_numpy(shapes).cuda()
+    lat = torch.empty(n, dtype=torch.float64, device="cuda")
+    cur = torch.empty(n, dtype=torch.int32, device="cuda")
+    wav = torch.empty(n, dtype=torch.int32, device="cuda")
+    mat = torch.empty(n, dtype=torch.int8, device="cuda")
+    rid = torch.empty(n, dtype=torch.int32, device="cuda")
+    dist = torch.empty(n, dtype=torch.float64, device="cuda")
+    dt = prep.device_tables(0)
+    _native.check(_native.load().pm2l_points_predict(
+        dt.handle, s.data_ptr(), n, lat.data_ptr(), cur.data_ptr(), wav.data_ptr(),
+        mat.data_ptr(), rid.data_ptr(), dist.data_ptr(), _native.stream_handle()), "points")
+    o_lat, o_cur, o_wav, o_mat, o_rec, o_dist = _oracle_points_threaded(prep.tables(), shapes)
+    assert np.array_equal(_bits(lat.cpu().numpy()), _bits(o_lat))
+    assert np.array_equal(cur.cpu().numpy(), o_cur)
+    assert np.array_equal(wav.cpu().numpy().view(np.uint32), o_wav)
+    assert np.array_equal(mat.cpu().numpy(), o_mat)
+    assert np.array_equal(rid.cpu().numpy(), o_rec)
+    assert np.array_equal(_bits(dist.cpu().numpy()), _bits(o_dist))
+    assert (o_mat[:len(rec)] == 0).all()
+
+
+def test_mode_x_full_c2_grid_sample_matches_oracle(gpu):
+    """Mode X on the full C2 grid: 10 M shapes x 60 kernels = 600 M pairs on
+    the device, 1 M seeded pairs checked against the oracle's predict_generic
+    restatement (compute.py:150-193)."""
+    import torch
+    from paper_2603_00549_b200 import backend
+    prep = _prep("bf16", "matmul", "bf16", "nn", _c2_axes())
+    allc = backend.predict_grid_all_curves(prep)
+    C, P = allc.shape
+    assert C == len(prep.curve_list) == 60 and P == 10_000_000
+    rng = np.random.default_rng(3)
+    ci = rng.integers(0, C, 1_000_000)
+    pi = rng.integers(0, P, 1_000_000)
+    got = allc[torch.from_numpy(ci).cuda(), torch.from_numpy(pi).cuda()].cpu().numpy()
+    axes = _c2_axes()
+    coords = np.unravel_index(pi, prep.grid.shape())
+    shapes = np.stack([np.asarray(axes[a], np.uint32)[c]
+                       for a, c in zip(("batch", "m", "n", "k"), coords)], 1)
+    t = prep.tables()
+    parts = np.array_split(np.arange(len(ci)), THREADS)
+    with ThreadPoolExecutor(THREADS) as pool:
+        res = list(pool.map(lambda p: oracle.points_curve(t, shapes[p], ci[p])[0], parts))
+    assert np.array_equal(_bits(got), _bits(np.concatenate(res)))
+    assert bool(torch.isfinite(allc).all())
