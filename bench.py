@@ -18,8 +18,11 @@ N > 1 the all-gather of the statistics.  Steps alternate between two
 distinct slices (k axis shifted by one), so no step reuses a plan.
 Inputs (tables, axes) are resident in HBM before timing; L2 is flushed
 (256 MiB write) between steps, outside the per-step CUDA-event window.
-N GPUs: weak scaling, rank r owns the contiguous batch slab [4r, 4r+4) of a
-global grid whose batch axis has 4N values (the first four are C2's 1,2,4,8).
+N GPUs: weak scaling, rank r owns the contiguous k-row-aligned flat range
+shard.flat_bounds(shape, N, r) of a global grid whose batch axis has 4N
+values (the first four are C2's 1,2,4,8) -- the batch slab [4r, 4r+4).
+For N > 1 `gather_inclusive` times the same step plus the NCCL gather of
+every rank's results into rank 0's HBM.
 
 `e2e` is the same metric through the reference-facing C-ABI drop-in
 (pm2l_predict_grid_slice: HOST tables/axes in, HOST output written), copies
@@ -63,8 +66,9 @@ def c2_config(world: int, n_pts: int = 10_000_000):
     return {"workload": "C2: BF16 matmul NN grid 4x50x50x1000 = 10M (b,m,n,k) points "
                         "per GPU vs bf16 seed-11 tables (540 recorded configs, 60 kernels)",
             "points_per_gpu": n_pts, "global_points": world * n_pts,
-            "parallelism": f"dp{world}: contiguous batch-slab shards, "
-                           f"all-gather of first-NaN/count stats",
+            "parallelism": f"dp{world}: contiguous k-row-aligned flat ranges (4 batch values "
+                           f"per rank), all-gather of first-NaN/count stats; results stay "
+                           f"sharded (gather_inclusive: + NCCL gather to rank 0)",
             "l2": "flushed between steps (256 MiB write, outside event window)",
             "output": "f64 latency per point, canonical order, HBM-resident"}
 
@@ -233,7 +237,7 @@ def slice_axes(world: int, variant: int):
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
-    from paper_2603_00549_b200 import _native
+    from paper_2603_00549_b200 import _native, shard
     from paper_2603_00549_b200.compute import WaveModel
     from paper_2603_00549_b200.nascache import PreparedGrid
 
@@ -244,7 +248,12 @@ def run_ours(args, rank, world, local_rank):
     ds = load_bf16()
     grid = grid_for(world)
     prep = PreparedGrid(ds, grid, WaveModel(ds.device.sm_count))
-    b_lo, b_hi = 4 * rank, 4 * rank + 4
+    # the rank's k-row-aligned flat range (shard.flat_bounds);
+    # with 4 batch values per rank it is the batch slab [4r, 4r + 4)
+    f_lo, f_hi = shard.flat_bounds(grid.shape(), world, rank)
+    inner = grid.cardinality // len(grid.axes["batch"])
+    assert f_lo % inner == 0 and f_hi % inner == 0
+    b_lo, b_hi = f_lo // inner, f_hi // inner
     dt = prep.device_tables(local_rank)
     # device-resident axes of two distinct slices; the planner kernel turns
     # them into the launch plan inside every step (pm2l_grid_dplan)
@@ -316,6 +325,30 @@ def run_ours(args, rank, world, local_rank):
                 g_step[j & 1].replay()
             torch.cuda.synchronize()
     step_ms = [e[0].elapsed_time(e[1]) for e in events]
+    # gather-inclusive (N > 1): the same step followed by the results of
+    # every rank to rank 0's HBM (one grouped NCCL send/recv), max over ranks
+    gather = None
+    if world > 1:
+        gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps + 2):
+            flush.zero_()
+            if k >= 2:
+                gev[k - 2][0].record(stream)
+            g_step[k & 1].replay()
+            shard.gather_to_root(out, f_lo, f_hi, grid.shape())
+            if k >= 2:
+                gev[k - 2][1].record(stream)
+        torch.cuda.synchronize()
+        g_tot = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in gev)], dtype=torch.float64,
+                             device=dev)
+        dist.all_reduce(g_tot, op=dist.ReduceOp.MAX)
+        g_ms = float(g_tot.item()) / args.steps
+        gather = {"value": world * n_pts / (g_ms * 1e-3), "ms_per_step": g_ms,
+                  "bytes_to_rank0_per_step": 8 * n_pts * (world - 1),
+                  "how": "step + grouped NCCL send/recv of every rank's f64 range into rank 0's "
+                         "HBM (shard.gather_to_root), CUDA events, max over ranks"}
     # the dominant kernel alone: L2 flushed, the slice planned (planner
     # kernel), then events around the grid kernel
     kev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
@@ -370,6 +403,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": args.steps * launches_per_step,
         "unresolved_points": nan_count,
         "clocks": clk.summary(),
+        "gather_inclusive": gather,
     }
     if rank == 0 and world == 1:
         rates, base = time_reference(3, 1)

@@ -202,23 +202,37 @@ int pm2l_grid_predict_all_curves(pm2l_tables* t,
 /* -------------------------------------------- explicit-descriptor mode ---
  * n ops, DEVICE array `shapes` of n x uint4-like records {b, m, n, k} (u32
  * each, 16 B per op), resolved against the staged triple `t`
- * (ConfigResolver.resolve semantics: exact match first, else nearest by
- * Chebyshev distance in log2 space, first index on ties) and predicted.
- * Coordinates must be >= 1 and < 2^22 (query log2 comes from a per-device
- * table of host-libm log2 values; the grid mode has no such limit).
- * Nullable outputs: out_curve (curve id, -1 unresolved), out_waves,
- * out_match (0 exact, 1 nearest, -1 no candidates, -2 invalid coordinate),
- * out_record (matched record: scan index for nearest; position in the
- * exact arrays given at pm2l_tables_create for exact hits), out_dist
- * (ResolvedConfig.distance: 0 for exact, Chebyshev log2 distance otherwise). */
+ * (ConfigResolver.resolve semantics, pm2lat/compute.py:251-268: exact match
+ * first, else nearest by Chebyshev distance in log2 space, first index on
+ * ties) and predicted (compute.py:163-193).
+ * Query log2 values are host-libm log2 (math.log2, as the reference's
+ * resolver takes them): a per-device table covers coordinates below
+ * pm2l_points_log2_table_size() (2^22); larger coordinates need an entry in
+ * the caller's extension -- DEVICE arrays ext_coords (ascending, unique u32)
+ * and ext_log2 (libm log2 of each), n_ext entries (pm2l_points_predict has
+ * none).  Nullable outputs: out_curve (curve id, -1 unresolved), out_waves
+ * (saturated at 2^32-1), out_match (0 exact, 1 nearest, -1 no candidates,
+ * -2 invalid coordinate (0, or no log2 for it), -3 block count >= 2^64,
+ * which the reference's unbounded-integer Python path would still answer),
+ * out_record (matched record: scan index for nearest; position in the exact
+ * arrays given at pm2l_tables_create for exact hits -- the first record of
+ * that shape), out_dist (ResolvedConfig.distance: 0 exact, Chebyshev log2
+ * distance otherwise). */
+int pm2l_points_predict_ext(pm2l_tables* t, const uint32_t* shapes, int64_t n,
+                            const uint32_t* ext_coords, const double* ext_log2, int64_t n_ext,
+                            double* out_lat, int32_t* out_curve, uint32_t* out_waves,
+                            int8_t* out_match, int32_t* out_record, double* out_dist,
+                            void* stream);
 int pm2l_points_predict(pm2l_tables* t, const uint32_t* shapes, int64_t n,
                         double* out_lat, int32_t* out_curve, uint32_t* out_waves,
                         int8_t* out_match, int32_t* out_record, double* out_dist,
                         void* stream);
+int64_t pm2l_points_log2_table_size(void);
 
 /* n ops with an explicit curve each (DEVICE int32 curve ids; no resolution;
  * predict_generic, compute.py:150-193).  out_detail (nullable) receives 4
- * doubles per op: base_us, new_throughput_gflops, wave_scale, blocks. */
+ * doubles per op: base_us, new_throughput_gflops, wave_scale, waves.  A block
+ * count >= 2^64 gives NaN everywhere (see pm2l_points_predict_ext). */
 int pm2l_points_predict_curve(pm2l_tables* t, const uint32_t* shapes,
                               const int32_t* curve_ids, int64_t n,
                               double* out_lat, uint32_t* out_waves, double* out_detail,
@@ -270,6 +284,16 @@ int pm2l_store_encode(const double* lat, int64_t n, const uint64_t* batch_vals,
 int pm2l_store_lookup(const uint8_t* records, int64_t n_records, const uint64_t* const* axes,
                       const int64_t* axis_lens, const uint64_t* queries, int64_t n, double* out,
                       uint64_t* first_missing, void* stream);
+
+/* backend.predict_grid's host-output form (pm2lat/backend.py:49-88 returns a
+ * numpy array): the slice [b_lo, b_hi) of the staged triple's grid (HOST
+ * axis arrays) into the HOST buffer `out` -- one D2H copy when `out` is
+ * page-locked, else chunked D2H through a pinned ring drained by a host
+ * copy pool (the same path as pm2l_predict_grid_slice).  Synchronous. */
+int pm2l_grid_predict_host(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_batch,
+                           const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals,
+                           int64_t n_n, const uint64_t* k_vals, int64_t n_k, int64_t b_lo,
+                           int64_t b_hi, double* out);
 
 /* ------------------------------------------------ reference FFI drop-in ---
  * Exactly pm2lat._kernels.predict_grid_slice (_kernels.pyx:76-133): HOST

@@ -64,9 +64,13 @@ SIGNATURES = {
     "pm2l_grid_dplan_fixups": (_i32, [_p, C.POINTER(_i64)]),
     "pm2l_grid_dplan_destroy": (_i32, [_p]),
     "pm2l_nan_scan": (_i32, [_p, _i64, _p, _p]),
+    "pm2l_grid_predict_host": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
+                                      _p]),
     "pm2l_grid_predict_all_curves": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64,
                                             _i64, _i64, _p, _p]),
     "pm2l_points_predict": (_i32, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
+    "pm2l_points_predict_ext": (_i32, [_p, _p, _i64, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
+    "pm2l_points_log2_table_size": (_i64, []),
     "pm2l_points_predict_curve": (_i32, [_p, _p, _p, _i64, _p, _p, _p, _p]),
     "pm2l_membound_predict": (_i32, [_p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "pm2l_segment_fsum": (_i32, [_p, _p, _i64, _p, _p]),

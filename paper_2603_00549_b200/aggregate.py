@@ -20,9 +20,21 @@ from .compute import (CLAMP_ABOVE, CLAMP_BELOW, MATCH_EXACT, MATCH_NEAREST, Conf
                       WaveModel, _check_pair)
 from .core import (COMPUTE_FAMILIES, FAMILY_LINEAR, DType, KernelKey, LayerSpec, ModelGraph,
                    Prediction, TransposeMode, is_utility_family, utility_kernel_name)
-from .errors import InsufficientData, PredictionError, UnresolvedLayer, ValidationError
+from .errors import (InsufficientData, NoConfigAvailable, PredictionError, UnresolvedLayer,
+                     ValidationError)
 from .ingest import Dataset
 from .membound import DEFAULT_LAUNCH_FLOOR_US, MemBoundModel, fit
+
+_NP_OF: Dict[object, np.dtype] = {}
+
+
+def _np_dtype(tdtype):
+    """numpy dtype of a torch dtype (cached)."""
+    d = _NP_OF.get(tdtype)
+    if d is None:
+        import torch
+        d = _NP_OF[tdtype] = torch.empty(0, dtype=tdtype).numpy().dtype
+    return d
 
 PREDICTOR_COMPUTE = "compute"
 PREDICTOR_MEMBOUND = "membound"
@@ -68,6 +80,7 @@ class ModelPredictor:
         self._membound: Dict[Tuple[str, DType], MemBoundModel] = {
             (m.kernel_name, m.dtype): m for m in dataset.membound_models}
         self._curves = None
+        self._dev = None
 
     def membound_model(self, kernel_name: str, dtype: DType) -> MemBoundModel:
         got = self._membound.get((kernel_name, dtype))
@@ -91,11 +104,36 @@ class ModelPredictor:
             self._curve_pos = {c.kernel: i for i, c in enumerate(self._curves)}
         return self._curves
 
+    def _device_state(self):
+        """Per-predictor device state, built once: the curve set of every
+        curve of the dataset (explicit-curve prediction) and, per triple, the
+        map record (scan index) -> curve-set id (-1: kernel without curve)."""
+        if self._dev is None:
+            from .compute import _CurveSet
+            curves = self.all_curves()
+            self._dev = {"cs": _CurveSet.get(tuple(curves), self.wm), "maps": {}}
+        return self._dev
+
+    def _rec_map(self, triple):
+        from . import _device
+        st = self._device_state()
+        m = st["maps"].get(triple)
+        if m is None:
+            recs = self.resolver.triple_tables(*triple)[0]
+            host = np.array([self._curve_pos.get(r.chosen_key, -1) for r in recs], np.int64)
+            m = st["maps"][triple] = _device.to_device(host, _device.device())
+        return m
+
     def predict_layers(self, layers: Sequence[LayerSpec]):
         """Device batch over layers: [(Prediction, kind, flags)] in order.
-        Raises like the reference on the first unresolvable layer."""
-        from .compute import predict_curve_batch
-        from .membound import predict_membound_batch
+        Raises like the reference on the first unresolvable layer.
+
+        One host->device copy per input kind, then every kernel back to back
+        on the stream (resolution per triple, record -> curve map, explicit-
+        curve prediction, membound with and without the floor) and ONE
+        device->host copy of every output."""
+        from . import _device, _native
+        from .compute import _log2_extension, _shapes_u32
         n = len(layers)
         out: List[Optional[tuple]] = [None] * n
         errors: Dict[int, Exception] = {}   # the reference raises at the FIRST bad layer
@@ -122,37 +160,14 @@ class ModelPredictor:
             else:
                 tr = layer.transpose_mode or default_transpose(layer.family)
                 by_triple.setdefault((layer.family, layer.dtype, tr), []).append(i)
-        # ---- compute layers: device resolution per triple
-        resolved: Dict[int, tuple] = {}
-        for triple, idx in by_triple.items():
-            try:
-                rec, match, dist = self.resolver.resolve_batch(
-                    *triple, [layers[i].shape.as_tuple() for i in idx])
-            except PredictionError as exc:
+        for triple, idx in list(by_triple.items()):
+            if not self.resolver._triples.get(triple):
+                exc = NoConfigAvailable(f"no recorded configuration for ({triple[0]}, "
+                                        f"{triple[1].value}, {triple[2].value})")
                 for i in idx:
                     errors[i] = wrap(i, exc)
-                continue
-            recs = self.resolver.triple_tables(*triple)[0]
-            for j, i in enumerate(idx):
-                key = recs[int(rec[j])].chosen_key
-                resolved[i] = (key, MATCH_EXACT if match[j] == 0 else MATCH_NEAREST)
-        curves = self.all_curves()
-        compute_idx, cids = [], []
-        for i in sorted(resolved):
-            key, _ = resolved[i]
-            if key not in self._curve_pos:
-                errors[i] = UnresolvedLayer(
-                    f"layer {layers[i].layer_id!r}: resolved kernel has no throughput curve "
-                    f"(family={layers[i].family}, algo={key.algorithm_id})")
-                continue
-            try:
-                _check_pair(key, curves[self._curve_pos[key]])
-            except PredictionError as exc:
-                errors[i] = wrap(i, exc)
-                continue
-            compute_idx.append(i)
-            cids.append(self._curve_pos[key])
-        # ---- utility layers: fitted (or on-demand refit) membound models
+                del by_triple[triple]
+        # utility layers: fitted (or on-demand refit) membound models
         models: List[MemBoundModel] = []
         pos: Dict[tuple, int] = {}
         util_ok, mids = [], []
@@ -168,42 +183,156 @@ class ModelPredictor:
                 continue
             util_ok.append(i)
             mids.append(pos[mk])
-        if errors:
-            raise errors[min(errors)]
-        if compute_idx:
-            lat, waves, det = predict_curve_batch([layers[i].shape.as_tuple() for i in compute_idx],
-                                                  curves, cids, self.wm, detail=True)
-            for j, i in enumerate(compute_idx):
-                key, match = resolved[i]
-                c = curves[cids[j]]
-                k = layers[i].shape.k
-                dims = c.dim_values()
-                clamp = CLAMP_BELOW if k < dims[0] else CLAMP_ABOVE if k > dims[-1] else None
-                comps = {"base_us": float(det[j, 0]), "ref_duration_us": c.ref_duration_us,
-                         "varying_value": k, "ref_dim_value": c.ref_dim_value,
-                         "new_throughput_gflops": float(det[j, 1]),
-                         "ref_throughput_gflops": c.ref_throughput, "waves": int(waves[j]),
-                         "ref_waves": c.ref_waves, "wave_scale": float(det[j, 2]),
-                         "blocks_per_wave": self.wm.for_curve(c).blocks_per_wave,
-                         "clamp": clamp, "config_match": match}
-                flags = (["nearest_config"] if match == MATCH_NEAREST else []) + \
-                    ([clamp] if clamp else [])
-                out[i] = (Prediction(float(lat[j]), key, comps), PREDICTOR_COMPUTE, flags)
-        if util_ok:
-            feats = [layers[i].features.as_vector() for i in util_ok]
-            lat, floored = predict_membound_batch(models, feats, mids,
-                                                  [self.floor_us] * len(models))
-            raw, _ = predict_membound_batch(models, feats, mids, [-np.inf] * len(models))
+
+        compute_idx = [i for idx in by_triple.values() for i in idx]
+        nc, nu = len(compute_idx), len(util_ok)
+        dev = _device.device()
+        t = _device.torch()
+        lib = _native.load()
+        sh = None
+        if nc:
+            try:
+                sh = _shapes_u32([layers[i].shape.as_tuple() for i in compute_idx])
+            except PredictionError as exc:
+                for i in compute_idx:
+                    errors[i] = wrap(i, exc)
+                nc = 0
+        # ---- device pipeline (no host sync until the single copy back)
+        parts = []
+        if nc:
+            st = self._device_state()
+            d_sh = _device.to_device(sh, dev)
+            ext_c, ext_l, n_ext = _log2_extension(sh, dev)
+            rec = t.empty(nc, dtype=t.int32, device=dev)
+            match = t.empty(nc, dtype=t.int8, device=dev)
+            dist = t.empty(nc, dtype=t.float64, device=dev)
+            cid = t.empty(nc, dtype=t.int32, device=dev)
+            lat = t.empty(nc, dtype=t.float64, device=dev)
+            det = t.empty((nc, 4), dtype=t.float64, device=dev)
+            s = _device.stream()
+            o = 0
+            for triple, idx in by_triple.items():
+                dt = self.resolver.triple_tables(*triple)[4]
+                k = len(idx)
+                _native.check(lib.pm2l_points_predict_ext(
+                    dt.handle, d_sh.data_ptr() + 16 * o, k, _native.ptr(ext_c), _native.ptr(ext_l),
+                    n_ext, lat.data_ptr() + 8 * o, 0, 0, match.data_ptr() + o,
+                    rec.data_ptr() + 4 * o, dist.data_ptr() + 8 * o, s), "pm2l_points_predict_ext")
+                cid[o:o + k] = self._rec_map(triple)[rec[o:o + k].clamp(min=0).long()].int()
+                o += k
+            _native.check(lib.pm2l_points_predict_curve(
+                st["cs"].dev.handle, d_sh.data_ptr(), cid.data_ptr(), nc, lat.data_ptr(),
+                0, det.data_ptr(), s), "pm2l_points_predict_curve")
+            parts += [rec, match, dist, cid, lat, det]
+        if nu:
+            f = np.array([layers[i].features.as_vector() for i in util_ok], np.float64)
+            w = np.array([m.weights for m in models], np.float64)
+            b = np.array([m.intercept for m in models], np.float64)
+            host = np.concatenate([f.ravel(), w.ravel(), b, np.full(len(models), self.floor_us),
+                                   np.full(len(models), -np.inf), np.array(mids, np.float64)])
+            d = _device.to_device(host, dev)
+            nf, nw = 5 * nu, 5 * len(models)
+            fl0 = nf + nw + len(models)
+            ids = d[fl0 + 2 * len(models):].to(t.int32)   # small integers: exact
+            mlat = t.empty(nu, dtype=t.float64, device=dev)
+            raw = t.empty(nu, dtype=t.float64, device=dev)
+            flo = t.empty(nu, dtype=t.uint8, device=dev)
+            flo2 = t.empty(nu, dtype=t.uint8, device=dev)
+            for fl_off, o_lat, o_flo in ((fl0, mlat, flo), (fl0 + len(models), raw, flo2)):
+                _native.check(lib.pm2l_membound_predict(
+                    d.data_ptr(), ids.data_ptr(), nu, d.data_ptr() + 8 * nf,
+                    d.data_ptr() + 8 * (nf + nw), d.data_ptr() + 8 * fl_off, len(models),
+                    o_lat.data_ptr(), o_flo.data_ptr(), _device.stream()), "pm2l_membound_predict")
+            parts += [mlat, raw, flo]
+        if parts:
+            blob = t.cat([p.reshape(-1).view(t.uint8) for p in parts]).cpu().numpy()
+            views, o = [], 0
+            for p in parts:
+                nb = p.numel() * p.element_size()
+                views.append(blob[o:o + nb].view(_np_dtype(p.dtype)).reshape(tuple(p.shape)))
+                o += nb
+        if nc:
+            rec, match, dist, cid, lat, det = views[:6]
+            views = views[6:]
+            curves = self.all_curves()
+            o = 0
+            for triple, idx in by_triple.items():
+                recs = self.resolver.triple_tables(*triple)[0]
+                for j, i in enumerate(idx, start=o):
+                    if match[j] == -2:
+                        errors[i] = wrap(i, ValidationError(
+                            f"shape {layers[i].shape.as_tuple()}: invalid coordinate"))
+                        continue
+                    key = recs[int(rec[j])].chosen_key
+                    if cid[j] < 0:
+                        errors[i] = UnresolvedLayer(
+                            f"layer {layers[i].layer_id!r}: resolved kernel has no throughput "
+                            f"curve (family={layers[i].family}, algo={key.algorithm_id})")
+                        continue
+                    c = curves[int(cid[j])]
+                    try:
+                        _check_pair(key, c)
+                    except PredictionError as exc:
+                        errors[i] = wrap(i, exc)
+                        continue
+                    if np.isnan(lat[j]):
+                        errors[i] = wrap(i, ValidationError(
+                            f"shape {layers[i].shape.as_tuple()}: block count exceeds 2^64"))
+                        continue
+                    m = MATCH_EXACT if match[j] == 0 else MATCH_NEAREST
+                    kk = layers[i].shape.k
+                    dims = c.dim_values()
+                    clamp = CLAMP_BELOW if kk < dims[0] else CLAMP_ABOVE if kk > dims[-1] else None
+                    comps = {"base_us": float(det[j, 0]), "ref_duration_us": c.ref_duration_us,
+                             "varying_value": kk, "ref_dim_value": c.ref_dim_value,
+                             "new_throughput_gflops": float(det[j, 1]),
+                             "ref_throughput_gflops": c.ref_throughput, "waves": int(det[j, 3]),
+                             "ref_waves": c.ref_waves, "wave_scale": float(det[j, 2]),
+                             "blocks_per_wave": self.wm.for_curve(c).blocks_per_wave,
+                             "clamp": clamp, "config_match": m}
+                    flags = (["nearest_config"] if m == MATCH_NEAREST else []) + \
+                        ([clamp] if clamp else [])
+                    out[i] = (Prediction(float(lat[j]), key, comps), PREDICTOR_COMPUTE, flags)
+                o += len(idx)
+        if nu:
+            mlat, raw, flo = views[:3]
             for j, i in enumerate(util_ok):
                 key = KernelKey.for_utility(models[mids[j]].kernel_name, layers[i].dtype)
                 comps = {"raw_us": float(raw[j]), "floor_us": self.floor_us,
-                         "floored": bool(floored[j])}
-                out[i] = (Prediction(float(lat[j]), key, comps), PREDICTOR_MEMBOUND,
-                          ["floored"] if floored[j] else [])
+                         "floored": bool(flo[j])}
+                try:
+                    out[i] = (Prediction(float(mlat[j]), key, comps), PREDICTOR_MEMBOUND,
+                              ["floored"] if flo[j] else [])
+                except PredictionError as exc:
+                    errors[i] = wrap(i, exc)
+        if errors:
+            raise errors[min(errors)]
         return out
 
     def predict_layer(self, layer: LayerSpec):
         return self.predict_layers([layer])[0]
+
+
+_PREDICTORS: Dict[tuple, tuple] = {}
+
+
+def _predictor(dataset: Dataset, wm: Optional[WaveModel], floor_us: float) -> ModelPredictor:
+    """The ModelPredictor of (dataset, wave model, floor), kept across calls:
+    its resolver holds the staged device tables of every triple it has seen
+    and its fitted membound models, so repeated predict_model calls on one
+    dataset stage nothing (the reference rebuilds both per call,
+    aggregate.py:178).  Keyed by object identity and checked through a weak
+    reference (Dataset is immutable); bounded."""
+    import weakref
+    key = (id(dataset), wm, floor_us)
+    hit = _PREDICTORS.get(key)
+    if hit is not None and hit[0]() is dataset:
+        return hit[1]
+    if len(_PREDICTORS) >= 16:
+        _PREDICTORS.clear()
+    p = ModelPredictor(dataset, wm, floor_us)
+    _PREDICTORS[key] = (weakref.ref(dataset), p)
+    return p
 
 
 def segment_fsum(values: np.ndarray, offsets: np.ndarray) -> np.ndarray:
@@ -224,7 +353,7 @@ def predict_models(graphs: Sequence[ModelGraph], dataset: Dataset,
                    wm: Optional[WaveModel] = None,
                    membound_floor_us: float = DEFAULT_LAUNCH_FLOOR_US) -> List[ModelPrediction]:
     """predict_model over many graphs with one device batch per stage."""
-    predictor = ModelPredictor(dataset, wm, membound_floor_us)
+    predictor = _predictor(dataset, wm, membound_floor_us)
     layers = [layer for g in graphs for layer in g.layers]
     offsets = np.zeros(len(graphs) + 1, dtype=np.int64)
     np.cumsum([len(g.layers) for g in graphs], out=offsets[1:])
@@ -269,9 +398,9 @@ def predict_model_grid(template: Sequence[TemplateLayer], shapes, features, data
     exact per-model totals, pm2l_segment_fsum).  Raises UnresolvedLayer for
     the first (model, layer) that cannot be predicted."""
     from . import _device, _native
-    from .compute import _shapes_u32
+    from .compute import _log2_extension, _shapes_u32
     from .membound import predict_membound_batch
-    pred = ModelPredictor(dataset, wm, membound_floor_us)
+    pred = _predictor(dataset, wm, membound_floor_us)
     L = len(template)
     shapes = np.asarray(shapes)
     n = shapes.shape[0] if shapes.ndim == 3 else np.asarray(features).shape[0]
@@ -290,13 +419,19 @@ def predict_model_grid(template: Sequence[TemplateLayer], shapes, features, data
     for triple, ls in by_triple.items():
         *_, dt = pred.resolver.triple_tables(*triple)
         s = _shapes_u32(shapes[:, ls, :].reshape(-1, 4))
-        if s.size and s.max() >= (1 << 22):
-            raise ValidationError("explicit-descriptor coordinates must be < 2^22")
         d_s = _device.to_device(s, dev)
+        ext_c, ext_l, n_ext = _log2_extension(s, dev)
         out = _device.empty(len(s), "float64", dev)
-        _native.check(_native.load().pm2l_points_predict(
-            dt.handle, _native.ptr(d_s), len(s), _native.ptr(out), 0, 0, 0, 0, 0,
-            _device.stream()), "pm2l_points_predict")
+        match = _device.empty(len(s), "int8", dev)
+        _native.check(_native.load().pm2l_points_predict_ext(
+            dt.handle, _native.ptr(d_s), len(s), _native.ptr(ext_c), _native.ptr(ext_l), n_ext,
+            _native.ptr(out), 0, 0, _native.ptr(match), 0, 0,
+            _device.stream()), "pm2l_points_predict_ext")
+        match = _device.to_numpy(match)
+        if (match == -3).any():
+            j = int(np.nonzero(match == -3)[0][0])
+            raise ValidationError(f"model {j // len(ls)} layer {template[ls[j % len(ls)]].layer_id!r}: "
+                                  f"block count exceeds 2^64")
         lat[:, ls] = _device.to_numpy(out).reshape(n, len(ls))
     if util:
         f = np.asarray(features, dtype=np.float64)

@@ -79,12 +79,19 @@ def predict_grid(prep, jobs: int = 1, force_python: bool = False) -> np.ndarray:
         raise BackendUnavailable("force_python: the B200 build has no Python/CPU fallback; "
                                  "the reference oracle lives in oracle/ (test-only)")
     card = prep.grid.cardinality
+    out = np.empty(card, dtype=np.float64)   # pageable, as backend.py:61 allocates it
     if card == 0:
-        return np.empty(0, np.float64)
-    lat = predict_grid_device(prep)
-    host = np.empty(card, dtype=np.float64)
-    _device.torch().from_numpy(host).copy_(lat)
-    return host
+        return out
+    _device.device()
+    dt = prep.device_tables(0)
+    ptrs, keep = _axes(prep)   # keep the host axis arrays alive across the call
+    (pb, lb), (pm, lm), (pn, ln), (pk, lk) = ptrs
+    # device kernel into HBM, then the chunked D2H through the library's
+    # pinned staging ring + host copy pool straight into ``out``
+    _native.check(_native.load().pm2l_grid_predict_host(
+        dt.handle, pb, lb, pm, lm, pn, ln, pk, lk, 0, lb, out.ctypes.data),
+        "pm2l_grid_predict_host")
+    return out
 
 
 def predict_grid_all_curves(prep, b_lo: int = 0, b_hi=None, stream=None, device: int = 0):

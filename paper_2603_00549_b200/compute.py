@@ -17,6 +17,7 @@ the device kernels carry their own u64 implementation of the same formulas
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, replace
 from typing import Dict, List, Optional, Tuple
 
@@ -115,33 +116,71 @@ def _check_pair(key: KernelKey, curve: ThroughputCurve) -> None:
 
 
 def _shapes_u32(shapes) -> np.ndarray:
-    a = np.asarray(shapes, dtype=np.int64).reshape(-1, 4)
+    """Shapes as the 16-byte explicit descriptor {b, m, n, k} (u32 each)."""
+    a = np.asarray(shapes, dtype=object if _has_big(shapes) else np.int64).reshape(-1, 4)
     if a.size and (a.min() < 1 or a.max() >= (1 << 32)):
-        raise ValidationError("shape coordinates must be in [1, 2^32)")
+        raise ValidationError("shape coordinates must be in [1, 2^32) (the explicit "
+                              "descriptor holds u32 coordinates)")
     return np.ascontiguousarray(a.astype(np.uint32))
+
+
+def _has_big(shapes) -> bool:
+    try:
+        np.asarray(shapes, dtype=np.int64)
+        return False
+    except OverflowError:
+        return True
+
+
+_LUT_N = None
+
+
+def _log2_extension(s: np.ndarray, dev):
+    """(coords, log2) device arrays for the query coordinates beyond the
+    per-device libm log2 table: math.log2 of each distinct m, n, k >= 2^22
+    (the reference resolver's own log2, compute.py:261)."""
+    from . import _device, _native
+    global _LUT_N
+    if _LUT_N is None:
+        _LUT_N = int(_native.load().pm2l_points_log2_table_size())
+    cols = s[:, 1:]
+    big = np.unique(cols[cols >= _LUT_N]) if s.size else np.empty(0, np.uint32)
+    if big.size == 0:
+        return None, None, 0
+    logs = np.array([math.log2(int(v)) for v in big], np.float64)
+    return (_device.to_device(np.ascontiguousarray(big, np.uint32), dev),
+            _device.to_device(logs, dev), int(big.size))
 
 
 def predict_curve_batch(shapes, curves: List[ThroughputCurve], curve_ids, wm: WaveModel,
                         detail: bool = False):
     """Device batch of predict_generic over explicit (shape, curve) pairs.
 
-    Returns (latency f64[n], waves u32[n], detail f64[n, 4] or None) with
-    detail = (base_us, new_throughput_gflops, wave_scale, blocks)."""
+    Returns (latency f64[n], waves u64[n], detail f64[n, 4] or None) with
+    detail = (base_us, new_throughput_gflops, wave_scale, waves).  A block
+    count past 2^64 (which the reference's unbounded Python integers would
+    still carry) raises ValidationError."""
     from . import _device, _native
     dev = _device.device()
     cs = _CurveSet.get(tuple(curves), wm)
     s = _shapes_u32(shapes)
     n = s.shape[0]
     d_s = _device.to_device(s, dev)
-    d_c = _device.to_device(np.ascontiguousarray(curve_ids, dtype=np.int32), dev)
+    cid = np.ascontiguousarray(curve_ids, dtype=np.int32)
+    d_c = _device.to_device(cid, dev)
     lat = _device.empty(n, "float64", dev)
     waves = _device.empty(n, "int32", dev)
-    det = _device.empty((n, 4), "float64", dev) if detail else None
+    det = _device.empty((n, 4), "float64", dev)
     _native.check(_native.load().pm2l_points_predict_curve(
         cs.dev.handle, _native.ptr(d_s), _native.ptr(d_c), n, _native.ptr(lat),
         _native.ptr(waves), _native.ptr(det), _device.stream()), "pm2l_points_predict_curve")
-    return (_device.to_numpy(lat), _device.to_numpy(waves).view(np.uint32),
-            _device.to_numpy(det) if detail else None)
+    lat, det = _device.to_numpy(lat), _device.to_numpy(det)
+    bad = np.isnan(lat) & np.array([curves[c] is not None for c in cid], bool)
+    if bad.any():
+        i = int(np.nonzero(bad)[0][0])
+        raise ValidationError(f"shape {tuple(int(x) for x in s[i])}: block count exceeds 2^64")
+    w = np.nan_to_num(det[:, 3]).astype(np.uint64)
+    return lat, w, det if detail else None
 
 
 def _interpolate_detail(curve: ThroughputCurve, new_dim: int) -> Tuple[float, Optional[str]]:
@@ -257,19 +296,23 @@ class ConfigResolver:
                                     f"{transpose.value})")
         recs, _, _, _, dt = self.triple_tables(family, dtype, transpose)
         s = _shapes_u32(shapes)
-        if s.size and s.max() >= (1 << 22):
-            raise ValidationError("explicit-descriptor coordinates must be < 2^22")
         n = s.shape[0]
         dev = _device.device()
         d_s = _device.to_device(s, dev)
+        ext_c, ext_l, n_ext = _log2_extension(s, dev)
         lat = _device.empty(n, "float64", dev)
         rec = _device.empty(n, "int32", dev)
         match = _device.empty(n, "int8", dev)
         dist = _device.empty(n, "float64", dev)
-        _native.check(_native.load().pm2l_points_predict(
-            dt.handle, _native.ptr(d_s), n, _native.ptr(lat), 0, 0, _native.ptr(match),
-            _native.ptr(rec), _native.ptr(dist), _device.stream()), "pm2l_points_predict")
-        return _device.to_numpy(rec), _device.to_numpy(match), _device.to_numpy(dist)
+        _native.check(_native.load().pm2l_points_predict_ext(
+            dt.handle, _native.ptr(d_s), n, _native.ptr(ext_c), _native.ptr(ext_l), n_ext,
+            _native.ptr(lat), 0, 0, _native.ptr(match), _native.ptr(rec), _native.ptr(dist),
+            _device.stream()), "pm2l_points_predict_ext")
+        match = _device.to_numpy(match)
+        if (match == -2).any():
+            i = int(np.nonzero(match == -2)[0][0])
+            raise ValidationError(f"shape {tuple(int(x) for x in s[i])}: invalid coordinate")
+        return _device.to_numpy(rec), match, _device.to_numpy(dist)
 
     def resolve(self, family: str, dtype: DType, transpose_mode: TransposeMode,
                 shape: MatMulShape) -> ResolvedConfig:

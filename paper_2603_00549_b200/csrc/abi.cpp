@@ -569,20 +569,37 @@ int pm2l_grid_predict_all_curves(pm2l_tables* t, const uint64_t* batch_vals, int
   return finish_call(t, s);
 }
 
-int pm2l_points_predict(pm2l_tables* t, const uint32_t* shapes, int64_t n, double* out_lat,
-                        int32_t* out_curve, uint32_t* out_waves, int8_t* out_match,
-                        int32_t* out_record, double* out_dist, void* stream) {
+int pm2l_points_predict_ext(pm2l_tables* t, const uint32_t* shapes, int64_t n,
+                            const uint32_t* ext_coords, const double* ext_log2, int64_t n_ext,
+                            double* out_lat, int32_t* out_curve, uint32_t* out_waves,
+                            int8_t* out_match, int32_t* out_record, double* out_dist,
+                            void* stream) {
   if (!t) return fail(PM2L_ERR_INVALID, "null tables");
-  if (n < 0) return fail(PM2L_ERR_INVALID, "negative count");
+  if (n < 0 || n_ext < 0) return fail(PM2L_ERR_INVALID, "negative count");
   if (n > 0 && (!shapes || !out_lat)) return fail(PM2L_ERR_INVALID, "null shapes/out_lat");
+  if (n_ext > 0 && (!ext_coords || !ext_log2)) return fail(PM2L_ERR_INVALID, "null log2 extension");
+  if (n_ext > (int64_t(1) << 31)) return fail(PM2L_ERR_INVALID, "log2 extension too long");
   DeviceGuard guard(t->device);
-  double* lut = nullptr;
-  if (int rc = get_lut(t->device, &lut)) return rc;
-  const int rc = launch_points(t->dev, shapes, n, lut, kLutN, out_lat, out_curve, out_waves,
-                               out_match, out_record, out_dist, stream);
+  LogSource logs;
+  if (int rc = get_lut(t->device, const_cast<double**>(&logs.lut))) return rc;
+  logs.lut_n = kLutN;
+  logs.ext_coord = ext_coords;
+  logs.ext_log = ext_log2;
+  logs.n_ext = n_ext;
+  const int rc = launch_points(t->dev, shapes, n, logs, out_lat, out_curve, out_waves, out_match,
+                               out_record, out_dist, stream);
   if (rc) return cuda_fail(cudaError_t(rc), "points kernel launch");
   return PM2L_OK;
 }
+
+int pm2l_points_predict(pm2l_tables* t, const uint32_t* shapes, int64_t n, double* out_lat,
+                        int32_t* out_curve, uint32_t* out_waves, int8_t* out_match,
+                        int32_t* out_record, double* out_dist, void* stream) {
+  return pm2l_points_predict_ext(t, shapes, n, nullptr, nullptr, 0, out_lat, out_curve, out_waves,
+                                 out_match, out_record, out_dist, stream);
+}
+
+int64_t pm2l_points_log2_table_size(void) { return kLutN; }
 
 int pm2l_points_predict_curve(pm2l_tables* t, const uint32_t* shapes, const int32_t* curve_ids,
                               int64_t n, double* out_lat, uint32_t* out_waves,
@@ -874,6 +891,38 @@ int drain_to_host(SliceDevice& sd, const double* d_out, double* out, size_t byte
   return PM2L_OK;
 }
 
+// The slice's latencies into a HOST buffer: the grid kernel writes the
+// per-device result buffer, then a page-locked `out` takes one D2H copy and
+// a pageable one the staged drain.  Synchronous.  Caller holds g_slice.mu.
+int predict_to_host_locked(pm2l_tables* t, int device, const uint64_t* batch_vals,
+                           int64_t n_batch, const uint64_t* m_vals, int64_t n_m,
+                           const uint64_t* n_vals, int64_t n_n, const uint64_t* k_vals,
+                           int64_t n_k, int64_t b_lo, int64_t b_hi, double* out) {
+  SliceDevice& sd = g_slice.dev[device];
+  cudaStream_t& s = sd.stream;
+  if (!s) PM2L_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  if (b_lo < 0 || b_hi < b_lo || b_hi > n_batch || n_m < 0 || n_n < 0 || n_k < 0)
+    return fail(PM2L_ERR_INVALID, "batch slice out of range");
+  const int64_t count = (b_hi - b_lo) * n_m * n_n * n_k;
+  if (count == 0) return PM2L_OK;
+  if (!out) return fail(PM2L_ERR_INVALID, "null out");
+  PM2L_CUDA(sd.out.reserve(size_t(count) * sizeof(double)));
+  double* d_out = static_cast<double*>(sd.out.ptr);
+  if (int rc = pm2l_grid_predict(t, batch_vals, n_batch, m_vals, n_m, n_vals, n_n, k_vals, n_k,
+                                 b_lo, b_hi, d_out, nullptr, nullptr, nullptr, s))
+    return rc;
+  // a page-locked caller buffer (cudaHostAlloc / cudaHostRegister, e.g. a
+  // pinned torch tensor's numpy view) takes the result straight from the
+  // copy engine; pageable buffers go through the staged drain
+  if (host_page_locked(out)) {
+    PM2L_CUDA(cudaMemcpyAsync(out, d_out, size_t(count) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  } else if (int rc = drain_to_host(sd, d_out, out, size_t(count) * sizeof(double))) {
+    return rc;
+  }
+  PM2L_CUDA(cudaStreamSynchronize(s));
+  return PM2L_OK;
+}
+
 }  // namespace
 
 int pm2l_predict_grid_slice(
@@ -952,28 +1001,19 @@ int pm2l_predict_grid_slice(
     e.last_use = ++g_slice.clock;
     g_slice.tables.emplace(h, std::move(e));
   }
-  SliceDevice& sd = g_slice.dev[device];
-  cudaStream_t& s = sd.stream;
-  if (!s) PM2L_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  const int64_t count = (b_hi - b_lo) * n_m * n_n * n_k;
-  if (count < 0) return fail(PM2L_ERR_INVALID, "batch slice out of range");
-  if (count == 0) return PM2L_OK;
-  if (!out) return fail(PM2L_ERR_INVALID, "null out");
-  PM2L_CUDA(sd.out.reserve(size_t(count) * sizeof(double)));
-  double* d_out = static_cast<double*>(sd.out.ptr);
-  if (int rc = pm2l_grid_predict(t, batch_vals, n_batch, m_vals, n_m, n_vals, n_n, k_vals, n_k,
-                                 b_lo, b_hi, d_out, nullptr, nullptr, nullptr, s))
-    return rc;
-  // a page-locked caller buffer (cudaHostAlloc / cudaHostRegister, e.g. a
-  // pinned torch tensor's numpy view) takes the result straight from the
-  // copy engine; pageable buffers go through the staged drain
-  if (host_page_locked(out)) {
-    PM2L_CUDA(cudaMemcpyAsync(out, d_out, size_t(count) * sizeof(double), cudaMemcpyDeviceToHost, s));
-  } else if (int rc = drain_to_host(sd, d_out, out, size_t(count) * sizeof(double))) {
-    return rc;
-  }
-  PM2L_CUDA(cudaStreamSynchronize(s));
-  return PM2L_OK;
+  return predict_to_host_locked(t, device, batch_vals, n_batch, m_vals, n_m, n_vals, n_n, k_vals,
+                                n_k, b_lo, b_hi, out);
+}
+
+int pm2l_grid_predict_host(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_batch,
+                           const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals,
+                           int64_t n_n, const uint64_t* k_vals, int64_t n_k, int64_t b_lo,
+                           int64_t b_hi, double* out) {
+  if (!t) return fail(PM2L_ERR_INVALID, "null tables");
+  DeviceGuard guard(t->device);
+  std::lock_guard<std::mutex> lk(g_slice.mu);
+  return predict_to_host_locked(t, t->device, batch_vals, n_batch, m_vals, n_m, n_vals, n_n,
+                                k_vals, n_k, b_lo, b_hi, out);
 }
 
 }  // extern "C"

@@ -92,7 +92,46 @@ struct TablesDev {
   int32_t n_mn = 0;
   const uint64_t* ex_mn_coord = nullptr;  // 4 per record
   const int32_t* ex_mn_curve = nullptr;
+  // explicit-descriptor mode (points.cu) -----------------------------------
+  // exact records with u32 coordinates as an open-addressing hash (linear
+  // probing, xh_hash below), staged in shared memory: capacity xh_mask + 1
+  // (a power of two >= 2x the records); key b == 0 marks an empty slot; the
+  // value is (curve, position in the caller's exact arrays) of the FIRST
+  // record of that shape.  xh_mask < 0: no table (bsearch over ex_coord).
+  int32_t xh_mask = -1;
+  const uint4* xh_key = nullptr;
+  const int2* xh_val = nullptr;
+  // one-class row decomposition of class 0's members: the distinct member
+  // (log m) values are rows and the distinct (log n) values columns, both
+  // ascending; member (i, j) is present iff bit j of rw_mask[i] (bit i of
+  // cl_mask[j]).  Valid (rw_n > 0) when every row and column count is <= 64
+  // and the deduplicated members in scan order are in (row, column)
+  // lexicographic order, so the first member in scan order satisfying a
+  // row and a column condition is the lowest row, then the lowest column.
+  // rw_pos[rw_off[i] + rank of j in row i] = the member's first position in
+  // the class member list.
+  int32_t rw_n = 0, cl_n = 0;
+  const double* rw_lm = nullptr;
+  const double* cl_ln = nullptr;
+  const uint64_t* rw_mask = nullptr;
+  const uint64_t* cl_mask = nullptr;
+  const int32_t* rw_off = nullptr;
+  const int32_t* rw_pos = nullptr;
 };
+
+#ifdef __CUDACC__
+#define PM2L_HD __host__ __device__ __forceinline__
+#else
+#define PM2L_HD inline
+#endif
+// Slot hash of an explicit descriptor (b, m, n, k) for TablesDev::xh_*.
+PM2L_HD uint32_t xh_hash(uint32_t b, uint32_t m, uint32_t n, uint32_t k) {
+  uint32_t h = (b * 0x9E3779B1u) ^ (m * 0x85EBCA77u) ^ (n * 0xC2B2AE3Du) ^ (k * 0x27D4EB2Fu);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  return h;
+}
 
 // k chunk of the one-class lookup kernel: ranks of the per-k distance are
 // taken inside chunks of this many k values (one warp's byte maps)
@@ -234,10 +273,19 @@ unsigned long long*& plan_timing_buffer();              // plan.cu: per-CTA entr
 #endif
 int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* workspace,
                            double* out, void* stream);
-int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n,
-                  const double* log_lut, int64_t lut_n, double* out_lat, int32_t* out_curve,
-                  uint32_t* out_waves, int8_t* out_match, int32_t* out_record, double* out_dist,
-                  void* stream);
+// Query log2 sources of the explicit-descriptor mode: the per-device libm
+// table for coordinates < lut_n, else a caller-given sorted (coordinate,
+// libm log2) extension (host-computed; n_ext may be 0).
+struct LogSource {
+  const double* lut = nullptr;
+  int64_t lut_n = 0;
+  const uint32_t* ext_coord = nullptr;
+  const double* ext_log = nullptr;
+  int64_t n_ext = 0;
+};
+int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const LogSource& logs,
+                  double* out_lat, int32_t* out_curve, uint32_t* out_waves, int8_t* out_match,
+                  int32_t* out_record, double* out_dist, void* stream);
 int launch_points_curve(const TablesDev& t, const uint32_t* shapes, const int32_t* curves,
                         int64_t n, double* out_lat, uint32_t* out_waves, double* out_detail,
                         void* stream);

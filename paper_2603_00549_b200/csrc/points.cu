@@ -120,37 +120,168 @@ __device__ int nearest_point(const TablesDev& t, const PointSmem& S, double qm, 
   return best_i;
 }
 
-// One member class (every shipped preset; equal logs imply equal
-// coordinates): the grid kernel's nearest_one_class decision per op, with
-// the row part from ONE pass over the members -- dmin and its first member
-// (case A: mn(k) <= dmin) and the first member within mn(k) (case B).
-// Returns the original candidate scan index; *out_best = the distance.
-__device__ int nearest_point_one_class(const TablesDev& t, const PointSmem& S, double qm,
-                                       double qn, double qk, uint64_t* out_best) {
-  const int G = t.G;
-  int lo = 0, hi = G;
+// Exact record of a u32 descriptor through the staged hash (TablesDev::xh_*):
+// linear probing from xh_hash until the key or an empty slot.
+__device__ __forceinline__ int exact_hash(const TablesDev& t, uint4 s, int* curve, int* record) {
+  uint32_t h = xh_hash(s.x, s.y, s.z, s.w) & uint32_t(t.xh_mask);
+  for (;;) {
+    const uint4 k = __ldg(t.xh_key + h);
+    if (k.x == 0) return 0;
+    if (k.x == s.x && k.y == s.y && k.z == s.z && k.w == s.w) {
+      const int2 v = __ldg(t.xh_val + h);
+      *curve = v.x;
+      *record = v.y;
+      return 1;
+    }
+    h = (h + 1) & uint32_t(t.xh_mask);
+  }
+}
+
+// host-libm log2 of a query coordinate: the per-device table below lut_n,
+// else the caller's sorted extension; false when neither holds it
+__device__ __forceinline__ bool query_log2(const LogSource& L, uint32_t x, double* out) {
+  if (x < L.lut_n) {
+    *out = __ldg(L.lut + x);
+    return true;
+  }
+  int lo = 0, hi = int(L.n_ext);
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (S.glk[mid] < qk) lo = mid + 1; else hi = mid;
+    if (__ldg(L.ext_coord + mid) < x) lo = mid + 1; else hi = mid;
   }
-  const int start = lo;
+  if (lo < L.n_ext && __ldg(L.ext_coord + lo) == x) {
+    *out = __ldg(L.ext_log + lo);
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ double dabs_sub(double a, double b) { return fabs(__dsub_rn(a, b)); }
+
+// number of v[0..n) below q (v ascending, n >= 0): fixed-trip branchless
+// search (the same trip count in every lane: no divergence)
+__device__ __forceinline__ int count_below(const double* v, int n, double q) {
+  int pos = 0;
+  for (int step = n > 0 ? 1 << (31 - __clz(n)) : 0; step > 0; step >>= 1)
+    if (pos + step <= n && v[pos + step - 1] < q) pos += step;
+  return pos;
+}
+
+struct RowSmem {
+  const double* rlm;      // [NR] distinct member log m, ascending
+  const double* cln;      // [NCl] distinct member log n, ascending
+  const uint64_t* rmask;  // [NR] present columns of each row
+  const uint64_t* cmask;  // [NCl] present rows of each column
+  const int32_t* roff;    // [NR+1]
+  const int32_t* rpos;    // [members] first position in the class member list
+  int NR, NCl;
+};
+
+// The member part of the one-class decision from the row decomposition, with
+// dm_i = |lm_i - qm| per row and dn_j = |ln_j - qn| per column (the member
+// (i, j) has D = max(dm_i, dn_j)):
+//  * row pass: per row the nearest present column to qn is the highest
+//    present column left of qn's insertion point pc or the lowest at or
+//    right of it (dn is V-shaped over the ascending columns: IEEE
+//    subtraction is monotone), so D_i = max(dm_i, nd_i) is the row minimum;
+//    dmin = min_i D_i, and irow = the first row attaining it (strict <);
+//    the rows within mn are collected as a mask;
+//  * column pass: the columns within dmin and within mn as masks;
+//  * case A (mn <= dmin): the argmin is the first member with D <= dmin --
+//    row irow (no earlier row reaches dmin), its lowest present column
+//    within dmin;  case B: the first member with D <= mn -- the lowest row
+//    within mn holding a present column within mn, that column.
+// Every row and column is visited once per op (fixed trip counts: no
+// divergence).  Returns the member's class position; *dmin_out = dmin.
+template <class Mask>  // uint32_t when rows and columns are <= 32, else uint64_t
+__device__ __forceinline__ int member_rows(const RowSmem& W, double qm, double qn, double mn,
+                                           double* dmin_out) {
+  constexpr int kBits = 8 * int(sizeof(Mask));
+  const double INF = __longlong_as_double(0x7FF0000000000000ll);
+  const int pc = count_below(W.cln, W.NCl, qn);
+  const Mask below = pc >= kBits ? ~Mask(0) : (Mask(1) << pc) - 1;
+  auto clz = [](Mask x) { return kBits == 32 ? __clz(uint32_t(x)) : __clzll(static_cast<long long>(x)); };
+  auto ffs = [](Mask x) { return kBits == 32 ? __ffs(uint32_t(x)) : __ffsll(static_cast<long long>(x)); };
+  double dmin = INF;
+  int irow = 0;
+  Mask rows_mn = 0;
+  for (int i = 0; i < W.NR; ++i) {
+    const Mask P = Mask(W.rmask[i]);
+    const double dm = dabs_sub(W.rlm[i], qm);
+    const Mask L = P & below, Rr = P & ~below;
+    const double dl = L ? dabs_sub(W.cln[kBits - 1 - clz(L)], qn) : INF;
+    const double dr = Rr ? dabs_sub(W.cln[ffs(Rr) - 1], qn) : INF;
+    const double nd = dl < dr ? dl : dr;
+    const double D = dm > nd ? dm : nd;
+    if (D < dmin) {
+      dmin = D;
+      irow = i;
+    }
+    rows_mn |= Mask(dm <= mn) << i;
+  }
+  Mask cols_d = 0, cols_mn = 0;
+  for (int j = 0; j < W.NCl; ++j) {
+    const double dn = dabs_sub(W.cln[j], qn);
+    cols_d |= Mask(dn <= dmin) << j;
+    cols_mn |= Mask(dn <= mn) << j;
+  }
+  int i = irow;
+  Mask cols = Mask(W.rmask[irow]) & cols_d;
+  if (!(mn <= dmin)) {
+    cols = 0;
+    for (Mask rr = rows_mn; rr && !cols; rr &= rr - 1) {
+      i = ffs(rr) - 1;
+      cols = Mask(W.rmask[i]) & cols_mn;
+    }
+  }
+  const int j = ffs(cols) - 1;
+  *dmin_out = dmin;
+  const Mask before = (Mask(1) << j) - 1;
+  const int rank = kBits == 32 ? __popc(uint32_t(Mask(W.rmask[i]) & before))
+                               : __popcll(static_cast<unsigned long long>(Mask(W.rmask[i]) & before));
+  return W.rpos[W.roff[i] + rank];
+}
+
+// One member class (every shipped preset; equal logs imply equal
+// coordinates): the grid kernel's nearest_one_class decision per op.  The
+// k part: mn = distance from qk to the nearest k-group.  The member part:
+// the row walk above when the class decomposes (ROWS), else one pass over
+// the members -- dmin and its first member (case A: mn <= dmin) and the
+// first member within mn (case B).  Returns the original candidate scan
+// index; *out_best = the distance as ordered |double| bits.
+template <int ROWS>  // 0 member pass, 1 rows (u32 masks), 2 rows (u64 masks)
+__device__ int nearest_point_one_class(const TablesDev& t, const PointSmem& S, const RowSmem& W,
+                                       double qm, double qn, double qk, uint64_t* out_best) {
+  const int G = t.G;
+  const int start = count_below(S.glk, G, qk);
   auto dk = [&](int g) { return abs_bits(__dsub_rn(S.glk[g], qk)); };
   const uint64_t dkL = start > 0 ? dk(start - 1) : ~0ull;
   const uint64_t dkR = start < G ? dk(start) : ~0ull;
   const uint64_t mn = dkL < dkR ? dkL : dkR;
-  const int CM = S.csize[0];
+  __syncwarp();  // every lane calls this (points_kernel): reconverge
   // distances are non-negative finite doubles, so FP64 order is the order
-  // of their |.| bits (member_d): compare them as doubles (DMNMX / DSETP)
+  // of their |.| bits: compare them as doubles (DSETP)
   const double mnd = __longlong_as_double(static_cast<long long>(mn));
-  double dminf = __longlong_as_double(0x7FF0000000000000ll);  // +inf
-  int argmin = 0, first_mn = -1;
-  for (int j = 0; j < CM; ++j) {
-    const double d = fmax(fabs(__dsub_rn(S.lm[j], qm)), fabs(__dsub_rn(S.ln[j], qn)));
-    if (d < dminf) { dminf = d; argmin = j; }
-    if (first_mn < 0 && d <= mnd) first_mn = j;
+  int pos;
+  uint64_t dmin;
+  if (ROWS) {
+    double dm;
+    pos = ROWS == 1 ? member_rows<uint32_t>(W, qm, qn, mnd, &dm)
+                    : member_rows<uint64_t>(W, qm, qn, mnd, &dm);
+    dmin = abs_bits(dm);
+  } else {
+    const int CM = S.csize[0];
+    double dminf = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+    int argmin = 0, first_mn = -1;
+    for (int j = 0; j < CM; ++j) {
+      const double d = fmax(fabs(__dsub_rn(S.lm[j], qm)), fabs(__dsub_rn(S.ln[j], qn)));
+      if (d < dminf) { dminf = d; argmin = j; }
+      if (first_mn < 0 && d <= mnd) first_mn = j;
+    }
+    dmin = abs_bits(dminf);
+    pos = mn <= dmin ? argmin : first_mn;
   }
-  const uint64_t dmin = abs_bits(dminf);
-  int g, pos;
+  int g;
   uint64_t best;
   if (mn <= dmin) {  // best == dmin: the leftmost group within dmin, member argmin
     if (dkL <= dmin) {
@@ -159,7 +290,6 @@ __device__ int nearest_point_one_class(const TablesDev& t, const PointSmem& S, d
     } else {
       g = start;
     }
-    pos = argmin;
     best = dmin;
   } else {           // best == mn: the leftmost nearest group, first member within mn
     if (dkL == mn) {
@@ -168,32 +298,92 @@ __device__ int nearest_point_one_class(const TablesDev& t, const PointSmem& S, d
     } else {
       g = start;
     }
-    pos = first_mn;
     best = mn;
   }
   *out_best = best;
   return S.gidx[S.gstart[g] + pos];
 }
 
-template <int NEARK>  // 0 general sweep, 1 sweep + tie mask (G <= 32), 2 one member class
+// blocks / waves of compute.block_count / wave_count with a flag for u64
+// overflow: the reference's Python path computes them in unbounded integers
+// (compute.py:78-106), so a product past 2^64 is reported, not wrapped.
+__device__ __forceinline__ bool predict_point_checked(const TablesDev& t, int c, uint64_t b,
+                                                      uint64_t m, uint64_t n, uint64_t k,
+                                                      double base, PointResult* r) {
+  if (t.rowblock[c]) {
+    r->blocks = ceil_div_c(t, c, 0, b * k, t.tile_m[c]);  // b, k < 2^32: no overflow
+  } else {
+    const uint64_t cm = ceil_div_c(t, c, 0, m, t.tile_m[c]), cn = ceil_div_c(t, c, 1, n, t.tile_n[c]);
+    const uint64_t sk = t.split_k[c];
+    uint64_t p;
+    if (((b | cm | cn | sk) >> 32) == 0) {  // the usual case: two exact 32x32 products
+      const uint64_t p1 = b * cm, p2 = cn * sk;
+      if (__umul64hi(p1, p2)) return false;
+      p = p1 * p2;
+    } else {
+      const uint64_t f[3] = {cm, cn, sk};
+      p = b;
+      bool over = false;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        over |= __umul64hi(p, f[i]) != 0;
+        p *= f[i];
+      }
+      if (over) return false;
+    }
+    r->blocks = p;
+  }
+  const uint64_t bpw = t.bpw[c];
+  if (r->blocks + bpw - 1 < r->blocks) return false;
+  r->waves = ceil_div_c(t, c, 2, r->blocks, bpw);
+  r->lat = __dmul_rn(base, wave_scale(t, c, r->waves));
+  return true;
+}
+
+__device__ __forceinline__ uint32_t waves_u32(uint64_t w) {
+  return w > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(w);  // saturated (detail has the value)
+}
+
+template <int NEARK>  // 0 general sweep, 1 sweep + tie mask (G <= 32), 2 one class,
+                      // 3 one class by rows (u32 masks), 4 by rows (u64 masks)
 __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uint4* __restrict__ shapes,
-                                                          int64_t n, const double* __restrict__ lut,
-                                                          int64_t lut_n, double* __restrict__ out_lat,
+                                                          int64_t n, LogSource L,
+                                                          double* __restrict__ out_lat,
                                                           int32_t* __restrict__ out_curve,
                                                           uint32_t* __restrict__ out_waves,
                                                           int8_t* __restrict__ out_match,
                                                           int32_t* __restrict__ out_record,
                                                           double* __restrict__ out_dist) {
   extern __shared__ __align__(16) uint8_t smem[];
-  double* lm = reinterpret_cast<double*>(smem);
-  double* ln = lm + t.CM;
-  double* glk = ln + t.CM;
+  constexpr bool kRows = NEARK >= 3;
+  const int NR = kRows ? t.rw_n : 0, NCl = kRows ? t.cl_n : 0;
+  const int NP = kRows ? t.rw_off[NR] : 0;
+  uint64_t* rmask = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* cmask = rmask + NR;
+  double* rlm = reinterpret_cast<double*>(cmask + NCl);
+  double* cln = rlm + NR;
+  double* lm = cln + NCl;
+  const int CMs = kRows ? 0 : t.CM;  // the row form needs no member list
+  double* ln = lm + CMs;
+  double* glk = ln + CMs;
   int32_t* gcls = reinterpret_cast<int32_t*>(glk + t.G);
   int32_t* gstart = gcls + t.G;
   int32_t* cstart = gstart + t.G;
   int32_t* csize = cstart + t.NC;
   int32_t* gidx = csize + t.NC;
-  for (int j = threadIdx.x; j < t.CM; j += blockDim.x) {
+  int32_t* roff = gidx + t.R;
+  int32_t* rpos = roff + NR + 1;
+  for (int j = threadIdx.x; j < NR; j += blockDim.x) {
+    rmask[j] = t.rw_mask[j];
+    rlm[j] = t.rw_lm[j];
+  }
+  for (int j = threadIdx.x; j < NCl; j += blockDim.x) {
+    cmask[j] = t.cl_mask[j];
+    cln[j] = t.cl_ln[j];
+  }
+  for (int j = threadIdx.x; j <= NR && kRows; j += blockDim.x) roff[j] = t.rw_off[j];
+  for (int j = threadIdx.x; j < NP; j += blockDim.x) rpos[j] = t.rw_pos[j];
+  for (int j = threadIdx.x; j < CMs; j += blockDim.x) {
     lm[j] = t.cls_lm[j];
     ln[j] = t.cls_ln[j];
   }
@@ -209,26 +399,62 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
   for (int j = threadIdx.x; j < t.R; j += blockDim.x) gidx[j] = t.g_idx[j];
   __syncthreads();
   const PointSmem S{lm, ln, glk, gcls, gstart, cstart, csize, gidx};
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const uint4 s = shapes[i];
-    const uint64_t b = s.x, m = s.y, nn = s.z, k = s.w;
+  const RowSmem W{rlm, cln, rmask, cmask, roff, rpos, NR, NCl};
+  // warp-uniform trip count (every lane runs every iteration, the tail lanes
+  // idle), so the warp can be reconverged before the shared prediction tail
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = blockIdx.x * int64_t(blockDim.x) + (threadIdx.x & ~31); base < n;
+       base += stride) {
+    const int64_t i = base + (threadIdx.x & 31);
+    const bool valid = i < n;
+    const uint4 s = valid ? shapes[i] : make_uint4(0, 0, 0, 0);
     int ci = -1, rec = -1;
     int8_t match = -1;
     double dist = 0.0;
-    if (s.x == 0 || s.y == 0 || s.z == 0 || s.w == 0 || s.y >= lut_n || s.z >= lut_n ||
-        s.w >= lut_n) {
-      match = -2;  // invalid coordinate (0, or beyond the libm log2 table)
-    } else if (exact_lookup(t, b, m, nn, k, &ci, &rec)) {
+    // divergent steps (probe loops, searches) are followed by explicit warp
+    // reconvergence: without it the lanes leave a loop at different trips
+    // and run the following nearest search in separate passes
+    const bool zero = s.x == 0 || s.y == 0 || s.z == 0 || s.w == 0;
+    const bool hit = !zero && (t.xh_mask >= 0 ? exact_hash(t, s, &ci, &rec)
+                                              : exact_lookup(t, s.x, s.y, s.z, s.w, &ci, &rec));
+    __syncwarp();
+    double qm = 0.0, qn = 0.0, qk = 0.0;
+    bool logs = !zero && !hit && t.R > 0;
+    if (logs) {
+      const bool a = query_log2(L, s.y, &qm), b = query_log2(L, s.z, &qn),
+                 c = query_log2(L, s.w, &qk);
+      logs = a && b && c;
+    }
+    __syncwarp();
+    // the nearest search runs in every lane (exact hits and invalid ops are
+    // rare; the warp would run it for the others anyway) so it can keep the
+    // warp converged; only the lanes that need it keep its answer
+    uint64_t best = 0;
+    int nrec = -1;
+    if (t.R > 0)
+      nrec = NEARK >= 2 ? nearest_point_one_class<NEARK - 2>(t, S, W, qm, qn, qk, &best)
+                        : nearest_point<NEARK == 1>(t, S, qm, qn, qk, &best);
+    if (zero) {
+      match = -2;  // invalid coordinate
+    } else if (hit) {
       match = 0;
     } else if (t.R > 0) {
-      uint64_t best;
-      rec = NEARK == 2 ? nearest_point_one_class(t, S, lut[s.y], lut[s.z], lut[s.w], &best)
-                       : nearest_point<NEARK == 1>(t, S, lut[s.y], lut[s.z], lut[s.w], &best);
-      ci = t.cand_curve[rec];
-      dist = __longlong_as_double(static_cast<long long>(best));
-      match = 1;
+      if (!logs) {
+        match = -2;  // no host log2 for this coordinate
+      } else {
+        rec = nrec;
+        ci = t.cand_curve[rec];
+        dist = __longlong_as_double(static_cast<long long>(best));
+        match = 1;
+      }
     }
+    __syncwarp();
+    PointResult r;
+    if (ci >= 0 && !predict_point_checked(t, ci, s.x, s.y, s.z, s.w, base_of(t, ci, s.w), &r)) {
+      match = -3;  // block count past 2^64
+      ci = -1;
+    }
+    if (!valid) continue;
     if (out_record) out_record[i] = rec;
     if (out_dist) out_dist[i] = dist;
     if (out_match) out_match[i] = match;
@@ -238,10 +464,9 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
       if (out_waves) out_waves[i] = 0;
       continue;
     }
-    const PointResult r = predict_point(t, ci, b, m, nn, k, base_of(t, ci, k));
     out_lat[i] = r.lat;
     if (out_curve) out_curve[i] = ci;
-    if (out_waves) out_waves[i] = uint32_t(r.waves);
+    if (out_waves) out_waves[i] = waves_u32(r.waves);
   }
 }
 
@@ -253,35 +478,47 @@ __global__ void points_curve_kernel(TablesDev t, const uint4* __restrict__ shape
        i += int64_t(gridDim.x) * blockDim.x) {
     const uint4 s = shapes[i];
     const int c = curves[i];
-    if (c < 0 || c >= t.C || !curve_valid(t, c)) {
+    PointResult r;
+    double thr = 0.0, base = 0.0;
+    bool ok = c >= 0 && c < t.C && curve_valid(t, c) && s.x && s.y && s.z && s.w;
+    if (ok) {
+      const double nd = __ull2double_rn(uint64_t(s.w));
+      thr = interp_thr(t, c, nd);
+      base = base_from_thr(t, c, nd, thr);
+      ok = predict_point_checked(t, c, s.x, s.y, s.z, s.w, base, &r);
+    }
+    if (!ok) {
       out_lat[i] = qnan();
       if (out_waves) out_waves[i] = 0;
+      if (out_detail)
+        for (int j = 0; j < 4; ++j) out_detail[4 * i + j] = qnan();
       continue;
     }
-    const double nd = __ull2double_rn(uint64_t(s.w));
-    const double thr = interp_thr(t, c, nd);
-    const double base = base_from_thr(t, c, nd, thr);
-    const PointResult r = predict_point(t, c, s.x, s.y, s.z, s.w, base);
     out_lat[i] = r.lat;
-    if (out_waves) out_waves[i] = uint32_t(r.waves);
-    if (out_detail) {  // Prediction.components: base_us, new_throughput, wave_scale, blocks
+    if (out_waves) out_waves[i] = waves_u32(r.waves);
+    if (out_detail) {  // Prediction.components: base_us, new_throughput, wave_scale, waves
       out_detail[4 * i] = base;
       out_detail[4 * i + 1] = thr;
       out_detail[4 * i + 2] = wave_scale(t, c, r.waves);
-      out_detail[4 * i + 3] = __ull2double_rn(r.blocks);
+      out_detail[4 * i + 3] = __ull2double_rn(r.waves);
     }
   }
 }
 
 }  // namespace
 
-int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const double* lut,
-                  int64_t lut_n, double* out_lat, int32_t* out_curve, uint32_t* out_waves,
-                  int8_t* out_match, int32_t* out_record, double* out_dist, void* stream) {
+int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const LogSource& logs,
+                  double* out_lat, int32_t* out_curve, uint32_t* out_waves, int8_t* out_match,
+                  int32_t* out_record, double* out_dist, void* stream) {
   if (n == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t smem = 16ll * t.CM + 8ll * t.G + 8ll * t.G + 8ll * t.NC + 4ll * t.R + 64;
-  auto* fn = (t.NC == 1 && t.lowest_wins) ? points_kernel<2>
+  const bool one = t.NC == 1 && t.lowest_wins;
+  const bool rows = one && t.rw_n > 0;
+  const int64_t NR = rows ? t.rw_n : 0, NCl = rows ? t.cl_n : 0;
+  const int64_t smem = 16ll * (NR + NCl) + (rows ? 0 : 16ll * t.CM) + 8ll * t.G + 8ll * t.G +
+                       8ll * t.NC + 4ll * t.R + (rows ? 4ll * (NR + 1 + t.CM) : 0) + 64;
+  auto* fn = rows ? (t.rw_n <= 32 && t.cl_n <= 32 ? points_kernel<3> : points_kernel<4>)
+             : one ? points_kernel<2>
              : t.G <= 32 ? points_kernel<1> : points_kernel<0>;
   if (smem > 227 * 1024) return int(cudaErrorInvalidValue);
   if (smem > 48 * 1024) {
@@ -289,7 +526,7 @@ int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const d
     if (e != cudaSuccess) return int(e);
   }
   const int nb = int(std::min<int64_t>((n + kThreads - 1) / kThreads, int64_t(sm_count()) * 8));
-  fn<<<nb, kThreads, smem, s>>>(t, reinterpret_cast<const uint4*>(shapes), n, lut, lut_n, out_lat,
+  fn<<<nb, kThreads, smem, s>>>(t, reinterpret_cast<const uint4*>(shapes), n, logs, out_lat,
                                 out_curve, out_waves, out_match, out_record, out_dist);
   return int(cudaGetLastError());
 }

@@ -264,6 +264,75 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   std::vector<uint8_t> rowblock(C);
   for (int64_t c = 0; c < C; ++c) rowblock[c] = v->family_rowblock[c] ? 1 : 0;
 
+  // --- explicit-descriptor exact hash (records whose coordinates fit u32;
+  // the first record of each shape in the caller's order, as a linear scan
+  // of the exact arrays finds it)
+  int32_t xh_mask = -1;
+  std::vector<uint4> xh_key;
+  std::vector<int2> xh_val;
+  if (R > 0) {
+    int64_t cap = 16;
+    while (cap < 2 * R) cap <<= 1;
+    xh_mask = int32_t(cap - 1);
+    xh_key.assign(size_t(cap), uint4{0, 0, 0, 0});
+    xh_val.assign(size_t(cap), int2{-1, -1});
+    // ex is sorted by shape, stable: equal shapes keep caller order
+    for (int64_t i = 0; i < R; ++i) {
+      const auto& e = ex[i];
+      if (i > 0 && std::equal(e.begin(), e.begin() + 4, ex[i - 1].begin())) continue;
+      if ((e[0] | e[1] | e[2] | e[3]) > 0xFFFFFFFFull || !e[0] || !e[1] || !e[2] || !e[3])
+        continue;  // cannot equal a u32 descriptor with coordinates >= 1
+      const uint4 key{uint32_t(e[0]), uint32_t(e[1]), uint32_t(e[2]), uint32_t(e[3])};
+      uint32_t h = xh_hash(key.x, key.y, key.z, key.w) & uint32_t(xh_mask);
+      while (xh_key[h].x) h = (h + 1) & uint32_t(xh_mask);
+      xh_key[h] = key;
+      xh_val[h] = int2{int32_t(int64_t(e[4])), int32_t(e[5])};
+    }
+  }
+  // --- row decomposition of class 0 (one member class)
+  std::vector<double> rw_lm, cl_ln;
+  std::vector<uint64_t> rw_mask, cl_mask;
+  std::vector<int32_t> rw_off, rw_pos;
+  if (cls_start.size() == 1) {
+    const int32_t CMm = cls_size[0];
+    auto bits = [](double x) { uint64_t u; std::memcpy(&u, &x, 8); return u; };
+    std::vector<double> lms(cls_lm.begin(), cls_lm.begin() + CMm);
+    std::vector<double> lns(cls_ln.begin(), cls_ln.begin() + CMm);
+    std::vector<double> rows = lms, cols = lns;
+    std::sort(rows.begin(), rows.end());
+    rows.erase(std::unique(rows.begin(), rows.end(),
+                           [&](double a, double b) { return bits(a) == bits(b); }), rows.end());
+    std::sort(cols.begin(), cols.end());
+    cols.erase(std::unique(cols.begin(), cols.end(),
+                           [&](double a, double b) { return bits(a) == bits(b); }), cols.end());
+    bool ok = rows.size() <= 64 && cols.size() <= 64 && !rows.empty();
+    std::vector<std::pair<int32_t, int32_t>> seen;  // deduplicated (row, col) in scan order
+    std::vector<int32_t> first_pos;
+    for (int32_t j = 0; ok && j < CMm; ++j) {
+      const int32_t r = int32_t(std::lower_bound(rows.begin(), rows.end(), lms[j]) - rows.begin());
+      const int32_t c = int32_t(std::lower_bound(cols.begin(), cols.end(), lns[j]) - cols.begin());
+      const std::pair<int32_t, int32_t> rc{r, c};
+      if (std::find(seen.begin(), seen.end(), rc) != seen.end()) continue;  // duplicate
+      if (!seen.empty() && !(seen.back() < rc)) ok = false;  // not (row, col)-lexicographic
+      seen.push_back(rc);
+      first_pos.push_back(j);
+    }
+    if (ok) {
+      rw_lm = rows;
+      cl_ln = cols;
+      rw_mask.assign(rows.size(), 0);
+      cl_mask.assign(cols.size(), 0);
+      rw_off.assign(rows.size() + 1, 0);
+      for (const auto& rc : seen) {
+        rw_mask[rc.first] |= uint64_t(1) << rc.second;
+        cl_mask[rc.second] |= uint64_t(1) << rc.first;
+        rw_off[rc.first + 1] += 1;
+      }
+      for (size_t i = 0; i < rows.size(); ++i) rw_off[i + 1] += rw_off[i];
+      rw_pos = first_pos;  // seen is lexicographic: row-major, columns ascending
+    }
+  }
+
   Blob blob;
   TablesDev& t = out->dev_offsets;
   t = TablesDev{};
@@ -318,6 +387,17 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.n_mn = int32_t(exm.size());
   t.ex_mn_coord = blob.add(exm_coord);
   t.ex_mn_curve = blob.add(exm_curve);
+  t.xh_mask = xh_mask;
+  t.xh_key = blob.add(xh_key);
+  t.xh_val = blob.add(xh_val);
+  t.rw_n = int32_t(rw_lm.size());
+  t.cl_n = int32_t(cl_ln.size());
+  t.rw_lm = blob.add(rw_lm);
+  t.cl_ln = blob.add(cl_ln);
+  t.rw_mask = blob.add(rw_mask);
+  t.cl_mask = blob.add(cl_mask);
+  t.rw_off = blob.add(rw_off);
+  t.rw_pos = blob.add(rw_pos);
   out->blob.swap(blob.bytes());
   out->max_group = max_group;
   return "";
@@ -345,6 +425,10 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.ex_rec = shift(o.ex_rec, base);
   t.ex_mn_coord = shift(o.ex_mn_coord, base);
   t.ex_mn_curve = shift(o.ex_mn_curve, base);
+  t.xh_key = shift(o.xh_key, base); t.xh_val = shift(o.xh_val, base);
+  t.rw_lm = shift(o.rw_lm, base); t.cl_ln = shift(o.cl_ln, base);
+  t.rw_mask = shift(o.rw_mask, base); t.cl_mask = shift(o.cl_mask, base);
+  t.rw_off = shift(o.rw_off, base); t.rw_pos = shift(o.rw_pos, base);
   return t;
 }
 

@@ -308,7 +308,8 @@ def test_sharded_predict_over_nccl_matches_single_process(gpu, tmp_path):
         prep = prepared(meta)
         res = shard.predict_sharded(prep, gather=True)
         ref = backend.predict_grid(prep)
-        assert np.array_equal(_bits(res.full), _bits(ref))
+        assert np.array_equal(_bits(res.full_numpy()), _bits(ref))
+        assert res.full.is_cuda and res.local.is_cuda   # device-resident gather
         assert res.first_unresolved == -1 and res.unresolved == 0
         ds = dataset(meta["dataset"])
         a, b = tmp_path / "a.bin", tmp_path / "b.bin"

@@ -290,3 +290,53 @@ def test_lookup_path_row_block_tables(gpu, seed, nk, nb, b_max):
     assert st[1] == nan.sum()
     if st[2] == 0:
         assert st[0] == (int(np.argmax(nan)) if nan.any() else -1)
+
+
+@pytest.mark.parametrize("seed,dup_batches", [(21, False), (22, True), (23, True)])
+def test_points_one_class_exact_ties(gpu, seed, dup_batches):
+    """Explicit descriptors on a one-class lattice whose coordinates are all
+    powers of two, so every log2 is an exact integer and distances tie
+    everywhere: the row-walk member search must return the reference's first
+    index (lexicographic (distance, scan index) minimum), bit for bit against
+    the oracle's linear scan.  Rows/columns are sparse (not a product set) and
+    members repeat across batch values."""
+    import math
+    import torch
+    from paper_2603_00549_b200 import _native
+    rng = np.random.default_rng(seed)
+    pm = [2 ** e for e in range(3, 14)]
+    pk = [2 ** e for e in range(4, 15, 2)]
+    mn = set()
+    while len(mn) < 40:
+        mn.add((int(rng.integers(1, 4)) if dup_batches else 1, int(rng.choice(pm)), int(rng.choice(pm))))
+    coords = sorted({(b, m, n, k) for (b, m, n) in mn for k in pk}, key=lambda c: (c[1], c[2], c[3], c[0]))
+    co = np.array(coords, np.uint64)
+    R, C = len(co), 7
+    cand = rng.integers(0, C, size=R).astype(np.int64)
+    t = {"exact_coords": co, "exact_coords_curve": cand.copy(), "cand_curve": cand, "exact_keys": None}
+    for name, col in (("log_m", 1), ("log_n", 2), ("log_k", 3)):
+        t[name] = np.array([math.log2(int(v)) for v in co[:, col]], np.float64)
+    t.update(sample_offsets=np.arange(0, 2 * C + 1, 2, dtype=np.int64),
+             sample_dims=np.tile([16.0, 20000.0], C), sample_thrs=rng.uniform(1, 900, 2 * C),
+             ref_dim=np.full(C, 20000.0), ref_dur=rng.uniform(1, 500, C), ref_waves=np.ones(C),
+             tile_m=np.full(C, 64, np.uint64), tile_n=np.full(C, 128, np.uint64),
+             split_k=np.ones(C, np.uint64), blocks_per_wave=np.full(C, 148, np.uint64),
+             family_rowblock=np.zeros(C, np.uint8))
+    t["ref_thr"] = t["sample_thrs"][1::2].copy()
+    dt = _native.DeviceTables(t, 0)
+    q = [2 ** e for e in range(0, 17)] + [3 * 2 ** e for e in range(0, 12)]
+    n = 60000
+    shapes = np.stack([rng.integers(1, 5, n), rng.choice(q, n), rng.choice(q, n),
+                       rng.choice(q + pk, n)], 1).astype(np.uint32)
+    d_s = torch.from_numpy(shapes).cuda()
+    outs = [torch.empty(n, dtype=dt_, device="cuda") for dt_ in
+            (torch.float64, torch.int32, torch.int32, torch.int8, torch.int32, torch.float64)]
+    _native.check(_native.load().pm2l_points_predict(
+        dt.handle, d_s.data_ptr(), n, *[o.data_ptr() for o in outs], _native.stream_handle()),
+        "points")
+    ref = oracle.points(t, shapes)
+    got = [o.cpu().numpy() for o in outs]
+    assert np.array_equal(got[4], ref[4])       # record (first index on ties)
+    assert np.array_equal(got[0].view(np.uint64), ref[0].view(np.uint64))
+    assert np.array_equal(got[3], ref[3])
+    assert np.array_equal(got[5].view(np.uint64), ref[5].view(np.uint64))
