@@ -17,10 +17,13 @@
  *   pm2l_tables_create         <- nascache.py:174-241  PreparedGrid.tables()
  *                                 (stages those arrays in HBM once per grid triple)
  *   pm2l_grid_predict          <- backend.py:49-88     predict_grid/_predict_grid_compiled
+ *   pm2l_grid_predict_host     <- backend.py:49-88     the same with the result in a host
+ *                                 buffer (backend.predict_grid returns a numpy array)
  *   pm2l_grid_dplan_*          <- nascache.py:140-245 + backend.py:58-76: the per-grid
  *                                 planning (PreparedGrid / tables() / axis logs) on the GPU
- *   pm2l_points_predict        <- compute.py:251-268 + 150-193
+ *   pm2l_points_predict(_ext)  <- compute.py:251-268 + 150-193
  *                                 ConfigResolver.resolve + predict_generic, batched
+ *                                 (_ext: coordinates >= 2^22 via a libm-log2 extension)
  *   pm2l_points_predict_curve  <- compute.py:150-193   predict_generic with an explicit
  *                                 kernel (no resolution; "mode X")
  *   pm2l_membound_predict      <- membound.py:117-127  predict_membound, batched
@@ -29,6 +32,8 @@
  *   pm2l_store_lookup          <- nascache.py:408-424  CacheStore.lookup, batched
  *   pm2l_segment_fsum          <- aggregate.py:193     math.fsum of per-layer latencies,
  *                                 per model segment (correctly rounded)
+ *   pm2l_grid_error_report     <- curvefit.py:192-219  grid_error_report
+ *   pm2l_partition_scan        <- partition.py:53-100  partition_two_device's cut scan
  */
 #ifndef PM2L_H_
 #define PM2L_H_
@@ -249,6 +254,31 @@ int pm2l_membound_predict(const double* features, const int32_t* model_ids, int6
                           const double* weights, const double* intercepts,
                           const double* floors, int64_t n_models,
                           double* out_lat, uint8_t* out_floored, void* stream);
+
+/* ------------------------------------------------ audits (§8f row 4) ---
+ * curvefit.grid_error_report (pm2lat/curvefit.py:192-219) for one curve:
+ * DEVICE arrays dims (int64, ascending sample dims) and thrs (throughputs),
+ * n_samples in [2, 1024]; per sample interval [lo, hi) the scan is
+ * range(lo, hi, stride) plus hi, the error |interp - truth| / truth, and
+ * out_err / out_argmax (n_samples - 1 each) the first maximum of the
+ * interval (initial (-1.0, lo)).  truth: the oracle's value per scan point,
+ * intervals concatenated, interval i starting at scan_off[i] -- or null
+ * with rational (a HOST array {a, b, c, d}): truth = (a*x + b) / (c*x + d). */
+int pm2l_grid_error_report(const int64_t* dims, const double* thrs, int64_t n_samples,
+                           int64_t stride, const double* truth, const int64_t* scan_off,
+                           const double* rational, double* out_err, int64_t* out_argmax,
+                           void* stream);
+
+/* partition.partition_two_device's cut scan (pm2lat/partition.py:53-100):
+ * DEVICE per-layer latencies of the two devices (n_layers each) and an
+ * optional per-cut transfer term (n_layers + 1); for every cut in
+ * [0, n_layers]: stage_a = left-to-right sum of lat_a[:cut], stage_b =
+ * left-to-right sum of lat_b[cut:] + transfer[cut], bottleneck = Python
+ * max(stage_a, stage_b); out_best_cut = the first cut of minimum
+ * bottleneck (the reference's strict-< scan). */
+int pm2l_partition_scan(const double* lat_a, const double* lat_b, int64_t n_layers,
+                        const double* transfer, double* out_stage_a, double* out_stage_b,
+                        double* out_bottleneck, int64_t* out_best_cut, void* stream);
 
 /* --------------------------------------------------- per-model totals ---
  * Correctly rounded sum (== math.fsum) of values[offsets[s] .. offsets[s+1])

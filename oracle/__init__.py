@@ -52,6 +52,9 @@ def lib():
         L.pm2lo_fsum.argtypes = [p, i64]
         L.pm2lo_fsum.restype = C.c_double
         L.pm2lo_segment_fsum.argtypes = [p, p, i64, p]
+        L.pm2lo_grid_error.argtypes = [p, p, i64, i64, p, p, p, p, p]
+        L.pm2lo_partition.argtypes = [p, p, i64, p, p, p, p]
+        L.pm2lo_partition.restype = i64
         _lib = L
     return _lib
 
@@ -165,6 +168,34 @@ def segment_fsum(values, offsets):
     out = np.empty(len(o) - 1, np.float64)
     lib().pm2lo_segment_fsum(v.ctypes.data, o.ctypes.data, len(o) - 1, out.ctypes.data)
     return out
+
+
+def grid_error(dims, thrs, stride, truth=None, scan_off=None, rational=None):
+    """curvefit.grid_error_report per interval: (max_rel_err f64[n-1], argmax i64[n-1])."""
+    d = np.ascontiguousarray(dims, np.int64)
+    t = np.ascontiguousarray(thrs, np.float64)
+    tr = None if truth is None else np.ascontiguousarray(truth, np.float64)
+    so = None if scan_off is None else np.ascontiguousarray(scan_off, np.int64)
+    r = None if rational is None else np.ascontiguousarray(rational, np.float64)
+    err = np.empty(len(d) - 1, np.float64)
+    arg = np.empty(len(d) - 1, np.int64)
+    P = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+    lib().pm2lo_grid_error(d.ctypes.data, t.ctypes.data, len(d), int(stride), P(tr), P(so), P(r),
+                           err.ctypes.data, arg.ctypes.data)
+    return err, arg
+
+
+def partition(lat_a, lat_b, transfer=None):
+    """partition_two_device's scan: (stage_a, stage_b, bottleneck, best cut)."""
+    la = np.ascontiguousarray(lat_a, np.float64)
+    lb = np.ascontiguousarray(lat_b, np.float64)
+    tr = None if transfer is None else np.ascontiguousarray(transfer, np.float64)
+    n = len(la)
+    sa, sb, bn = (np.empty(n + 1, np.float64) for _ in range(3))
+    best = lib().pm2lo_partition(la.ctypes.data, lb.ctypes.data, n,
+                                 None if tr is None else tr.ctypes.data, sa.ctypes.data,
+                                 sb.ctypes.data, bn.ctypes.data)
+    return sa, sb, bn, int(best)
 
 
 # ------------------------------------------------- the reference's own kernel

@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(PKG, LIB_NAME)
 OBJ_DIR = os.path.join(ROOT, "build", "obj")
 SOURCES = ["csrc/grid.cu", "csrc/grid_sweep.cu", "csrc/grid_lookup_nb1.cu",
            "csrc/grid_lookup_nb2.cu", "csrc/grid_lookup_nb4.cu", "csrc/grid_lookup_nb8.cu",
-           "csrc/plan.cu", "csrc/points.cu", "csrc/reduce.cu", "csrc/store.cu",
+           "csrc/plan.cu", "csrc/points.cu", "csrc/audit.cu", "csrc/reduce.cu", "csrc/store.cu",
            "csrc/tables.cpp", "csrc/abi.cpp"]
 HEADERS = ["csrc/pm2l_internal.h", "csrc/common.cuh", "csrc/grid_common.cuh",
            "csrc/grid_lookup.cuh", "../include/pm2l.h"]

@@ -74,6 +74,8 @@ SIGNATURES = {
     "pm2l_points_predict_curve": (_i32, [_p, _p, _p, _i64, _p, _p, _p, _p]),
     "pm2l_membound_predict": (_i32, [_p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p]),
     "pm2l_segment_fsum": (_i32, [_p, _p, _i64, _p, _p]),
+    "pm2l_grid_error_report": (_i32, [_p, _p, _i64, _i64, _p, _p, _p, _p, _p, _p]),
+    "pm2l_partition_scan": (_i32, [_p, _p, _i64, _p, _p, _p, _p, _p, _p]),
     "pm2l_store_encode_workspace": (_i64, [_i64]),
     "pm2l_store_encode": (_i32, [_p, _i64, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p, _p, _p]),
     "pm2l_store_lookup": (_i32, [_p, _i64, _p, _p, _p, _i64, _p, _p, _p]),
@@ -157,10 +159,21 @@ def ptr(a) -> int:
     return int(a.data_ptr())
 
 
+_RAW_STREAM = None
+
+
 def stream_handle(stream=None) -> int:
+    """cudaStream_t of ``stream`` or of torch's current stream on the current
+    device (the raw binding: no Stream object per call)."""
+    global _RAW_STREAM
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    if _RAW_STREAM is None:
+        _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", False)
+    if _RAW_STREAM:
+        return int(_RAW_STREAM(torch.cuda.current_device()))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 class DeviceTables:

@@ -126,7 +126,13 @@ class ModelPredictor:
 
     def predict_layers(self, layers: Sequence[LayerSpec]):
         """Device batch over layers: [(Prediction, kind, flags)] in order.
-        Raises like the reference on the first unresolvable layer.
+        Raises like the reference on the first unresolvable layer."""
+        return self._predict_layers(layers)[0]
+
+    def _predict_layers(self, layers: Sequence[LayerSpec], offsets=None):
+        """predict_layers, plus (with segment ``offsets`` over ``layers``) the
+        correctly rounded per-segment totals, computed on the device inside
+        the same pipeline.  Returns (out, totals or None).
 
         One host->device copy per input kind, then every kernel back to back
         on the stream (resolution per triple, record -> curve map, explicit-
@@ -197,11 +203,38 @@ class ModelPredictor:
                 for i in compute_idx:
                     errors[i] = wrap(i, exc)
                 nc = 0
-        # ---- device pipeline (no host sync until the single copy back)
+        # ---- device pipeline: two host->device copies (one integer blob,
+        # one float blob, through pinned staging), every kernel back to back
+        # on the stream, one device->host copy of every output
+        nseg = 0 if offsets is None else len(offsets) - 1
+        ints = np.concatenate([
+            sh.astype(np.int64).ravel() if nc else np.zeros(0, np.int64),
+            np.asarray(mids, np.int64), np.asarray(compute_idx[:nc], np.int64),
+            np.asarray(util_ok, np.int64),
+            np.zeros(0, np.int64) if offsets is None else np.asarray(offsets, np.int64)])
+        floats = np.zeros(0, np.float64)
+        if nu:
+            floats = np.concatenate([
+                np.array([layers[i].features.as_vector() for i in util_ok], np.float64).ravel(),
+                np.array([m.weights for m in models], np.float64).ravel(),
+                np.array([m.intercept for m in models], np.float64),
+                np.full(len(models), self.floor_us), np.full(len(models), -np.inf)])
+        s = _device.stream()
+        d_int = _staged_upload(ints, dev)
+        d_flt = _staged_upload(floats, dev) if nu else None
+        o = 4 * nc
+        d_mid = d_int[o:o + nu]
+        o += nu
+        d_posc = d_int[o:o + nc]
+        o += nc
+        d_posu = d_int[o:o + nu]
+        o += nu
+        d_off = d_int[o:o + nseg + 1] if offsets is not None else None
         parts = []
+        lay = t.empty(n, dtype=t.float64, device=dev) if offsets is not None else None
         if nc:
             st = self._device_state()
-            d_sh = _device.to_device(sh, dev)
+            d_sh = d_int[:4 * nc].to(t.int32)   # u32 descriptors (int32 bits)
             ext_c, ext_l, n_ext = _log2_extension(sh, dev)
             rec = t.empty(nc, dtype=t.int32, device=dev)
             match = t.empty(nc, dtype=t.int8, device=dev)
@@ -209,7 +242,6 @@ class ModelPredictor:
             cid = t.empty(nc, dtype=t.int32, device=dev)
             lat = t.empty(nc, dtype=t.float64, device=dev)
             det = t.empty((nc, 4), dtype=t.float64, device=dev)
-            s = _device.stream()
             o = 0
             for triple, idx in by_triple.items():
                 dt = self.resolver.triple_tables(*triple)[4]
@@ -224,26 +256,30 @@ class ModelPredictor:
                 st["cs"].dev.handle, d_sh.data_ptr(), cid.data_ptr(), nc, lat.data_ptr(),
                 0, det.data_ptr(), s), "pm2l_points_predict_curve")
             parts += [rec, match, dist, cid, lat, det]
+            if lay is not None:
+                lay[d_posc] = lat
         if nu:
-            f = np.array([layers[i].features.as_vector() for i in util_ok], np.float64)
-            w = np.array([m.weights for m in models], np.float64)
-            b = np.array([m.intercept for m in models], np.float64)
-            host = np.concatenate([f.ravel(), w.ravel(), b, np.full(len(models), self.floor_us),
-                                   np.full(len(models), -np.inf), np.array(mids, np.float64)])
-            d = _device.to_device(host, dev)
-            nf, nw = 5 * nu, 5 * len(models)
-            fl0 = nf + nw + len(models)
-            ids = d[fl0 + 2 * len(models):].to(t.int32)   # small integers: exact
+            nf, nw, nm = 5 * nu, 5 * len(models), len(models)
+            ids = d_mid.to(t.int32)
             mlat = t.empty(nu, dtype=t.float64, device=dev)
             raw = t.empty(nu, dtype=t.float64, device=dev)
             flo = t.empty(nu, dtype=t.uint8, device=dev)
             flo2 = t.empty(nu, dtype=t.uint8, device=dev)
-            for fl_off, o_lat, o_flo in ((fl0, mlat, flo), (fl0 + len(models), raw, flo2)):
+            base = d_flt.data_ptr()
+            for fl_off, o_lat, o_flo in ((nf + nw + nm, mlat, flo), (nf + nw + 2 * nm, raw, flo2)):
                 _native.check(lib.pm2l_membound_predict(
-                    d.data_ptr(), ids.data_ptr(), nu, d.data_ptr() + 8 * nf,
-                    d.data_ptr() + 8 * (nf + nw), d.data_ptr() + 8 * fl_off, len(models),
-                    o_lat.data_ptr(), o_flo.data_ptr(), _device.stream()), "pm2l_membound_predict")
+                    base, ids.data_ptr(), nu, base + 8 * nf, base + 8 * (nf + nw),
+                    base + 8 * fl_off, nm, o_lat.data_ptr(), o_flo.data_ptr(), s),
+                    "pm2l_membound_predict")
             parts += [mlat, raw, flo]
+            if lay is not None:
+                lay[d_posu] = mlat
+        totals = None
+        if offsets is not None and nseg > 0:
+            totals = t.empty(nseg, dtype=t.float64, device=dev)
+            _native.check(lib.pm2l_segment_fsum(lay.data_ptr(), d_off.data_ptr(), nseg,
+                                                totals.data_ptr(), s), "pm2l_segment_fsum")
+            parts.append(totals)
         if parts:
             blob = t.cat([p.reshape(-1).view(t.uint8) for p in parts]).cpu().numpy()
             views, o = [], 0
@@ -251,6 +287,8 @@ class ModelPredictor:
                 nb = p.numel() * p.element_size()
                 views.append(blob[o:o + nb].view(_np_dtype(p.dtype)).reshape(tuple(p.shape)))
                 o += nb
+            if totals is not None:
+                totals = views.pop()
         if nc:
             rec, match, dist, cid, lat, det = views[:6]
             views = views[6:]
@@ -307,10 +345,29 @@ class ModelPredictor:
                     errors[i] = wrap(i, exc)
         if errors:
             raise errors[min(errors)]
-        return out
+        return out, totals
 
     def predict_layer(self, layer: LayerSpec):
         return self.predict_layers([layer])[0]
+
+
+_PINNED: Dict[str, object] = {}
+
+
+def _staged_upload(a: np.ndarray, dev):
+    """Host array -> device through a reused page-locked staging buffer
+    (asynchronous copy on the current stream; the caller's single
+    device->host copy at the end of the pipeline orders the buffer's reuse)."""
+    import torch
+    key = a.dtype.str
+    buf = _PINNED.get(key)
+    if buf is None or buf.numel() < a.size:
+        cap = max(1024, 1 << int(max(a.size, 1) - 1).bit_length())
+        buf = _PINNED[key] = torch.empty(cap, dtype=torch.from_numpy(a[:0]).dtype,
+                                         pin_memory=True)
+    if a.size:
+        buf[:a.size].numpy()[:] = a
+    return buf[:max(a.size, 0)].to(dev, non_blocking=True)
 
 
 _PREDICTORS: Dict[tuple, tuple] = {}
@@ -357,8 +414,9 @@ def predict_models(graphs: Sequence[ModelGraph], dataset: Dataset,
     layers = [layer for g in graphs for layer in g.layers]
     offsets = np.zeros(len(graphs) + 1, dtype=np.int64)
     np.cumsum([len(g.layers) for g in graphs], out=offsets[1:])
-    res = predictor.predict_layers(layers)
-    totals = segment_fsum(np.array([r[0].latency_us for r in res], np.float64), offsets)
+    res, totals = predictor._predict_layers(layers, offsets)
+    if totals is None:
+        totals = np.zeros(len(graphs), np.float64)   # only when there are no layers
     out = []
     for gi, g in enumerate(graphs):
         lo, hi = int(offsets[gi]), int(offsets[gi + 1])

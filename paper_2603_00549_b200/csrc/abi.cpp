@@ -17,6 +17,8 @@
 #include <string>
 #include <unordered_map>
 #include <thread>
+
+#include <nvtx3/nvToolsExt.h>
 #include <vector>
 
 #include "../../include/pm2l.h"
@@ -27,6 +29,15 @@ using namespace pm2l;
 namespace {
 
 thread_local std::string g_error;
+
+// NVTX range over one C-ABI call (header-only NVTX v3: a no-op unless a
+// profiler such as nsys / ncu --nvtx is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int fail(int code, const std::string& msg) {
   g_error = msg;
@@ -292,6 +303,7 @@ int pm2l_device_count(void) {
 }
 
 int pm2l_tables_create(const pm2l_tables_view* view, int device, pm2l_tables** out) {
+  NvtxRange nvtx_("pm2l_tables_create");
   if (!out) return fail(PM2L_ERR_INVALID, "null output handle");
   *out = nullptr;
   if (int rc = check_device()) return rc;
@@ -337,6 +349,7 @@ int pm2l_grid_predict(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_batc
                       const uint64_t* k_vals, int64_t n_k, int64_t b_lo, int64_t b_hi,
                       double* out_lat, int32_t* out_curve, uint64_t* out_blocks,
                       uint64_t* out_waves, void* stream) {
+  NvtxRange nvtx_("pm2l_grid_predict");
   if (!t) return fail(PM2L_ERR_INVALID, "null tables");
   const bool any_v = out_curve || out_blocks || out_waves;
   if (any_v && !(out_curve && out_blocks && out_waves))
@@ -373,6 +386,7 @@ int pm2l_grid_plan_create(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_
                           const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals,
                           int64_t n_n, const uint64_t* k_vals, int64_t n_k, int64_t b_lo,
                           int64_t b_hi, pm2l_grid_plan** out) {
+  NvtxRange nvtx_("pm2l_grid_plan_create");
   if (!t || !out) return fail(PM2L_ERR_INVALID, "null tables/output handle");
   *out = nullptr;
   DeviceGuard guard(t->device);
@@ -396,6 +410,7 @@ int pm2l_grid_plan_create(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_
 int pm2l_grid_plan_launch(pm2l_grid_plan* p, double* out_lat, int32_t* out_curve,
                           uint64_t* out_blocks, uint64_t* out_waves, uint64_t* nan_stats,
                           int stages, void* stream) {
+  NvtxRange nvtx_("pm2l_grid_plan_launch");
   if (!p) return fail(PM2L_ERR_INVALID, "null plan");
   const bool any_v = out_curve || out_blocks || out_waves;
   if (any_v && !(out_curve && out_blocks && out_waves))
@@ -477,6 +492,7 @@ int pm2l_grid_dplan_launch(pm2l_grid_dplan* p, const uint64_t* batch_vals, int64
                            int64_t b_hi, double* out_lat, int32_t* out_curve,
                            uint64_t* out_blocks, uint64_t* out_waves, uint64_t* nan_stats,
                            int stages, void* stream) {
+  NvtxRange nvtx_("pm2l_grid_dplan_launch");
   if (!p) return fail(PM2L_ERR_INVALID, "null device plan");
   const bool any_v = out_curve || out_blocks || out_waves;
   if (any_v && !(out_curve && out_blocks && out_waves))
@@ -542,6 +558,7 @@ int pm2l_grid_dplan_destroy(pm2l_grid_dplan* p) {
 }
 
 int pm2l_nan_scan(const double* lat, int64_t n, uint64_t* first, void* stream) {
+  NvtxRange nvtx_("pm2l_nan_scan");
   if (n < 0 || (n > 0 && (!lat || !first))) return fail(PM2L_ERR_INVALID, "bad nan_scan args");
   if (int rc = check_device()) return rc;
   const int rc = launch_nan_scan(lat, n, reinterpret_cast<unsigned long long*>(first), stream);
@@ -553,6 +570,7 @@ int pm2l_grid_predict_all_curves(pm2l_tables* t, const uint64_t* batch_vals, int
                                  const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals,
                                  int64_t n_n, const uint64_t* k_vals, int64_t n_k, int64_t b_lo,
                                  int64_t b_hi, double* out_lat, void* stream) {
+  NvtxRange nvtx_("pm2l_grid_predict_all_curves");
   if (!t) return fail(PM2L_ERR_INVALID, "null tables");
   std::lock_guard<std::mutex> lk(t->mu);
   DeviceGuard guard(t->device);
@@ -574,6 +592,7 @@ int pm2l_points_predict_ext(pm2l_tables* t, const uint32_t* shapes, int64_t n,
                             double* out_lat, int32_t* out_curve, uint32_t* out_waves,
                             int8_t* out_match, int32_t* out_record, double* out_dist,
                             void* stream) {
+  NvtxRange nvtx_("pm2l_points_predict_ext");
   if (!t) return fail(PM2L_ERR_INVALID, "null tables");
   if (n < 0 || n_ext < 0) return fail(PM2L_ERR_INVALID, "negative count");
   if (n > 0 && (!shapes || !out_lat)) return fail(PM2L_ERR_INVALID, "null shapes/out_lat");
@@ -604,6 +623,7 @@ int64_t pm2l_points_log2_table_size(void) { return kLutN; }
 int pm2l_points_predict_curve(pm2l_tables* t, const uint32_t* shapes, const int32_t* curve_ids,
                               int64_t n, double* out_lat, uint32_t* out_waves,
                               double* out_detail, void* stream) {
+  NvtxRange nvtx_("pm2l_points_predict_curve");
   if (!t) return fail(PM2L_ERR_INVALID, "null tables");
   if (n < 0) return fail(PM2L_ERR_INVALID, "negative count");
   if (n > 0 && (!shapes || !curve_ids || !out_lat))
@@ -618,6 +638,7 @@ int pm2l_points_predict_curve(pm2l_tables* t, const uint32_t* shapes, const int3
 int pm2l_membound_predict(const double* features, const int32_t* model_ids, int64_t n,
                           const double* weights, const double* intercepts, const double* floors,
                           int64_t n_models, double* out_lat, uint8_t* out_floored, void* stream) {
+  NvtxRange nvtx_("pm2l_membound_predict");
   if (n < 0 || n_models < 0) return fail(PM2L_ERR_INVALID, "negative count");
   if (n > 0 && (!features || !model_ids || !out_lat || !weights || !intercepts || !floors))
     return fail(PM2L_ERR_INVALID, "null membound argument");
@@ -630,6 +651,7 @@ int pm2l_membound_predict(const double* features, const int32_t* model_ids, int6
 
 int pm2l_segment_fsum(const double* values, const int64_t* offsets, int64_t n_segments,
                       double* out_totals, void* stream) {
+  NvtxRange nvtx_("pm2l_segment_fsum");
   if (n_segments < 0) return fail(PM2L_ERR_INVALID, "negative count");
   if (n_segments > 0 && (!values || !offsets || !out_totals))
     return fail(PM2L_ERR_INVALID, "null fsum argument");
@@ -639,12 +661,45 @@ int pm2l_segment_fsum(const double* values, const int64_t* offsets, int64_t n_se
   return PM2L_OK;
 }
 
+int pm2l_grid_error_report(const int64_t* dims, const double* thrs, int64_t n_samples,
+                           int64_t stride, const double* truth, const int64_t* scan_off,
+                           const double* rational, double* out_err, int64_t* out_argmax,
+                           void* stream) {
+  NvtxRange nvtx_("pm2l_grid_error_report");
+  if (n_samples < 2) return fail(PM2L_ERR_INVALID, "a curve needs >= 2 samples");
+  if (n_samples > 1024) return fail(PM2L_ERR_INVALID, "more than 1024 samples");
+  if (stride < 1) return fail(PM2L_ERR_INVALID, "stride must be >= 1");
+  if (!dims || !thrs || !out_err || !out_argmax || (!truth && !rational) || (truth && !scan_off))
+    return fail(PM2L_ERR_INVALID, "null grid-error argument");
+  if (int rc = check_device()) return rc;
+  const int rc = launch_grid_error(dims, thrs, int(n_samples), stride, truth, scan_off, rational,
+                                   out_err, out_argmax, stream);
+  if (rc) return cuda_fail(cudaError_t(rc), "grid-error kernel launch");
+  return PM2L_OK;
+}
+
+int pm2l_partition_scan(const double* lat_a, const double* lat_b, int64_t n_layers,
+                        const double* transfer, double* out_stage_a, double* out_stage_b,
+                        double* out_bottleneck, int64_t* out_best_cut, void* stream) {
+  NvtxRange nvtx_("pm2l_partition_scan");
+  if (n_layers < 0) return fail(PM2L_ERR_INVALID, "negative layer count");
+  if ((n_layers > 0 && (!lat_a || !lat_b)) || !out_stage_a || !out_stage_b || !out_bottleneck ||
+      !out_best_cut)
+    return fail(PM2L_ERR_INVALID, "null partition argument");
+  if (int rc = check_device()) return rc;
+  const int rc = launch_partition(lat_a, lat_b, n_layers, transfer, out_stage_a, out_stage_b,
+                                  out_bottleneck, out_best_cut, stream);
+  if (rc) return cuda_fail(cudaError_t(rc), "partition kernel launch");
+  return PM2L_OK;
+}
+
 int64_t pm2l_store_encode_workspace(int64_t n) { return n < 0 ? -1 : store_encode_workspace(n); }
 
 int pm2l_store_encode(const double* lat, int64_t n, const uint64_t* batch_vals,
                       const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals, int64_t n_n,
                       const uint64_t* k_vals, int64_t n_k, void* workspace, uint8_t* records,
                       int64_t* count, void* stream) {
+  NvtxRange nvtx_("pm2l_store_encode");
   if (n < 0 || n_m < 0 || n_n < 0 || n_k < 0) return fail(PM2L_ERR_INVALID, "negative size");
   if (!count) return fail(PM2L_ERR_INVALID, "null count");
   if (n > 0 && (!lat || !batch_vals || !m_vals || !n_vals || !k_vals || !workspace || !records))
@@ -661,6 +716,7 @@ int pm2l_store_encode(const double* lat, int64_t n, const uint64_t* batch_vals,
 int pm2l_store_lookup(const uint8_t* records, int64_t n_records, const uint64_t* const* axes,
                       const int64_t* axis_lens, const uint64_t* queries, int64_t n, double* out,
                       uint64_t* first_missing, void* stream) {
+  NvtxRange nvtx_("pm2l_store_lookup");
   if (n < 0 || n_records < 0) return fail(PM2L_ERR_INVALID, "negative size");
   if (n > 0 && (!queries || !out || !first_missing || (n_records > 0 && !records)))
     return fail(PM2L_ERR_INVALID, "null store_lookup argument");
@@ -935,6 +991,7 @@ int pm2l_predict_grid_slice(
     const double* ref_waves, const uint64_t* tile_m, const uint64_t* tile_n,
     const uint64_t* split_k, const uint64_t* blocks_per_wave, const uint8_t* family_rowblock,
     double* out) {
+  NvtxRange nvtx_("pm2l_predict_grid_slice");
   if (int rc = check_device()) return rc;
   if (n_records < 0 || n_curves < 0 || !sample_offsets)
     return fail(PM2L_ERR_INVALID, "bad table sizes");
@@ -1009,6 +1066,7 @@ int pm2l_grid_predict_host(pm2l_tables* t, const uint64_t* batch_vals, int64_t n
                            const uint64_t* m_vals, int64_t n_m, const uint64_t* n_vals,
                            int64_t n_n, const uint64_t* k_vals, int64_t n_k, int64_t b_lo,
                            int64_t b_hi, double* out) {
+  NvtxRange nvtx_("pm2l_grid_predict_host");
   if (!t) return fail(PM2L_ERR_INVALID, "null tables");
   DeviceGuard guard(t->device);
   std::lock_guard<std::mutex> lk(g_slice.mu);

@@ -300,6 +300,11 @@ int launch_store_encode(const double* lat, int64_t n, const uint64_t* B, const u
 int launch_store_lookup(const uint8_t* records, int64_t n_rec, const uint64_t* const axes[4],
                         const int64_t lens[4], const uint64_t* queries, int64_t nq, double* out,
                         unsigned long long* first_missing, void* stream);
+int launch_grid_error(const int64_t* dims, const double* thrs, int ns, int64_t stride,
+                      const double* truth, const int64_t* scan_off, const double* rational,
+                      double* out_err, int64_t* out_arg, void* stream);
+int launch_partition(const double* la, const double* lb, int64_t n, const double* transfer,
+                     double* sa, double* sb, double* bn, int64_t* best, void* stream);
 int launch_segment_fsum(const double* v, const int64_t* off, int64_t nseg, double* out,
                         void* stream);
 

@@ -1,0 +1,48 @@
+"""compute-sanitizer over every kernel of libpm2l_b200.so (tools/sanitize_smoke.py:
+small launches of each kernel, results checked against the oracle):
+memcheck (out-of-bounds / misaligned device accesses), racecheck
+(shared-memory hazards: the planner's rank sort, the sweep kernel's
+staircases, the points kernel's staged tables, the reductions) and
+synccheck (barrier / warp-sync misuse: the points kernel's __syncwarp
+reconvergence)."""
+
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _sanitizer():
+    for c in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if c and os.path.exists(c):
+            return c
+    pytest.fail("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_kernels_are_clean_under_compute_sanitizer(gpu, tool):
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "99", "--print-limit", "20"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    if tool == "racecheck":
+        # grid_ring_kernel orders its shared-memory tile slots with mbarriers
+        # (FULL/EMPTY/ready arrive + try_wait chains across warp roles,
+        # grid_lookup.cuh), which racecheck does not model: it reports every
+        # slot reuse as a WAR hazard although each one is ordered by the
+        # slot's EMPTY barrier.  Its outputs are checked bit for bit by the
+        # parity suites; every other kernel is raced here.
+        cmd += ["--racecheck-report", "all", "--kernel-name-exclude", "kns=grid_ring_kernel"]
+    cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_smoke.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500,
+                       env=dict(os.environ, PYTHONUNBUFFERED="1"))
+    tail = (r.stdout + r.stderr)[-6000:]
+    assert r.returncode == 0, tail
+    assert "sanitize_smoke: ok" in r.stdout, tail
+    out = r.stdout + r.stderr
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards displayed (0 errors" in out, tail
