@@ -222,12 +222,14 @@ int pm2l_grid_predict_all_curves(pm2l_tables* t,
  * out_record (matched record: scan index for nearest; position in the exact
  * arrays given at pm2l_tables_create for exact hits -- the first record of
  * that shape), out_dist (ResolvedConfig.distance: 0 exact, Chebyshev log2
- * distance otherwise). */
+ * distance otherwise), out_detail (_ext only; 4 doubles per op, the
+ * Prediction.components of compute.py:177-193: base_us,
+ * new_throughput_gflops, wave_scale, waves; NaN when unresolved). */
 int pm2l_points_predict_ext(pm2l_tables* t, const uint32_t* shapes, int64_t n,
                             const uint32_t* ext_coords, const double* ext_log2, int64_t n_ext,
                             double* out_lat, int32_t* out_curve, uint32_t* out_waves,
                             int8_t* out_match, int32_t* out_record, double* out_dist,
-                            void* stream);
+                            double* out_detail, void* stream);
 int pm2l_points_predict(pm2l_tables* t, const uint32_t* shapes, int64_t n,
                         double* out_lat, int32_t* out_curve, uint32_t* out_waves,
                         int8_t* out_match, int32_t* out_record, double* out_dist,
@@ -254,6 +256,12 @@ int pm2l_membound_predict(const double* features, const int32_t* model_ids, int6
                           const double* weights, const double* intercepts,
                           const double* floors, int64_t n_models,
                           double* out_lat, uint8_t* out_floored, void* stream);
+/* The same, plus (nullable) out_raw: the pre-floor value (the reference's
+ * Prediction component "raw_us", membound.py:117-127). */
+int pm2l_membound_predict_raw(const double* features, const int32_t* model_ids, int64_t n,
+                              const double* weights, const double* intercepts,
+                              const double* floors, int64_t n_models, double* out_lat,
+                              uint8_t* out_floored, double* out_raw, void* stream);
 
 /* ------------------------------------------------ audits (§8f row 4) ---
  * curvefit.grid_error_report (pm2lat/curvefit.py:192-219) for one curve:

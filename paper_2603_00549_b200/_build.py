@@ -22,7 +22,7 @@ ROOT = os.path.dirname(PKG)
 LIB_NAME = "libpm2l_b200.so"
 LIB_PATH = os.path.join(PKG, LIB_NAME)
 OBJ_DIR = os.path.join(ROOT, "build", "obj")
-SOURCES = ["csrc/grid.cu", "csrc/grid_sweep.cu", "csrc/grid_lookup_nb1.cu",
+SOURCES = ["csrc/grid.cu", "csrc/grid_sweep.cu", "csrc/grid_single.cu", "csrc/grid_lookup_nb1.cu",
            "csrc/grid_lookup_nb2.cu", "csrc/grid_lookup_nb4.cu", "csrc/grid_lookup_nb8.cu",
            "csrc/plan.cu", "csrc/points.cu", "csrc/audit.cu", "csrc/reduce.cu", "csrc/store.cu",
            "csrc/tables.cpp", "csrc/abi.cpp"]

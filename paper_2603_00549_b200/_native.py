@@ -69,10 +69,12 @@ SIGNATURES = {
     "pm2l_grid_predict_all_curves": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64,
                                             _i64, _i64, _p, _p]),
     "pm2l_points_predict": (_i32, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
-    "pm2l_points_predict_ext": (_i32, [_p, _p, _i64, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
+    "pm2l_points_predict_ext": (_i32, [_p, _p, _i64, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p,
+                                       _p]),
     "pm2l_points_log2_table_size": (_i64, []),
     "pm2l_points_predict_curve": (_i32, [_p, _p, _p, _i64, _p, _p, _p, _p]),
     "pm2l_membound_predict": (_i32, [_p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p]),
+    "pm2l_membound_predict_raw": (_i32, [_p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p, _p]),
     "pm2l_segment_fsum": (_i32, [_p, _p, _i64, _p, _p]),
     "pm2l_grid_error_report": (_i32, [_p, _p, _i64, _i64, _p, _p, _p, _p, _p, _p]),
     "pm2l_partition_scan": (_i32, [_p, _p, _i64, _p, _p, _p, _p, _p, _p]),

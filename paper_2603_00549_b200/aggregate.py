@@ -80,7 +80,6 @@ class ModelPredictor:
         self._membound: Dict[Tuple[str, DType], MemBoundModel] = {
             (m.kernel_name, m.dtype): m for m in dataset.membound_models}
         self._curves = None
-        self._dev = None
 
     def membound_model(self, kernel_name: str, dtype: DType) -> MemBoundModel:
         got = self._membound.get((kernel_name, dtype))
@@ -103,26 +102,6 @@ class ModelPredictor:
             self._curves = list(self.dataset.curves.values())
             self._curve_pos = {c.kernel: i for i, c in enumerate(self._curves)}
         return self._curves
-
-    def _device_state(self):
-        """Per-predictor device state, built once: the curve set of every
-        curve of the dataset (explicit-curve prediction) and, per triple, the
-        map record (scan index) -> curve-set id (-1: kernel without curve)."""
-        if self._dev is None:
-            from .compute import _CurveSet
-            curves = self.all_curves()
-            self._dev = {"cs": _CurveSet.get(tuple(curves), self.wm), "maps": {}}
-        return self._dev
-
-    def _rec_map(self, triple):
-        from . import _device
-        st = self._device_state()
-        m = st["maps"].get(triple)
-        if m is None:
-            recs = self.resolver.triple_tables(*triple)[0]
-            host = np.array([self._curve_pos.get(r.chosen_key, -1) for r in recs], np.int64)
-            m = st["maps"][triple] = _device.to_device(host, _device.device())
-        return m
 
     def predict_layers(self, layers: Sequence[LayerSpec]):
         """Device batch over layers: [(Prediction, kind, flags)] in order.
@@ -230,92 +209,85 @@ class ModelPredictor:
         d_posu = d_int[o:o + nu]
         o += nu
         d_off = d_int[o:o + nseg + 1] if offsets is not None else None
-        parts = []
-        lay = t.empty(n, dtype=t.float64, device=dev) if offsets is not None else None
+        # every output in ONE device buffer (f64 slots; the int32 / int8
+        # outputs live in their own slots), copied back once
+        lay_n = n if offsets is not None else 0
+        tot_n = nseg if offsets is not None else 0
+        sizes = [nc, nc, nc, 4 * nc, nc, nu, nu, nu, lay_n, tot_n]   # rec|cur, match, dist, det, lat, mlat, raw, flo, lay, tot
+        starts = [0]
+        for z in sizes:
+            starts.append(starts[-1] + int(z))
+        buf = t.empty(int(starts[-1]), dtype=t.float64, device=dev)
+        bp = buf.data_ptr()
+        sl = lambda k: buf[starts[k]:starts[k + 1]]  # noqa: E731
         if nc:
-            st = self._device_state()
             d_sh = d_int[:4 * nc].to(t.int32)   # u32 descriptors (int32 bits)
             ext_c, ext_l, n_ext = _log2_extension(sh, dev)
-            rec = t.empty(nc, dtype=t.int32, device=dev)
-            match = t.empty(nc, dtype=t.int8, device=dev)
-            dist = t.empty(nc, dtype=t.float64, device=dev)
-            cid = t.empty(nc, dtype=t.int32, device=dev)
-            lat = t.empty(nc, dtype=t.float64, device=dev)
-            det = t.empty((nc, 4), dtype=t.float64, device=dev)
             o = 0
             for triple, idx in by_triple.items():
                 dt = self.resolver.triple_tables(*triple)[4]
                 k = len(idx)
+                # rec (int32) and curve (int32) share slot 0; match (int8) slot 1
                 _native.check(lib.pm2l_points_predict_ext(
                     dt.handle, d_sh.data_ptr() + 16 * o, k, _native.ptr(ext_c), _native.ptr(ext_l),
-                    n_ext, lat.data_ptr() + 8 * o, 0, 0, match.data_ptr() + o,
-                    rec.data_ptr() + 4 * o, dist.data_ptr() + 8 * o, s), "pm2l_points_predict_ext")
-                cid[o:o + k] = self._rec_map(triple)[rec[o:o + k].clamp(min=0).long()].int()
+                    n_ext, bp + 8 * (starts[4] + o), bp + 8 * starts[0] + 4 * o, 0,
+                    bp + 8 * starts[1] + o, bp + 8 * starts[0] + 4 * (nc + o),
+                    bp + 8 * (starts[2] + o), bp + 8 * (starts[3] + 4 * o), s),
+                    "pm2l_points_predict_ext")
                 o += k
-            _native.check(lib.pm2l_points_predict_curve(
-                st["cs"].dev.handle, d_sh.data_ptr(), cid.data_ptr(), nc, lat.data_ptr(),
-                0, det.data_ptr(), s), "pm2l_points_predict_curve")
-            parts += [rec, match, dist, cid, lat, det]
-            if lay is not None:
-                lay[d_posc] = lat
+            if offsets is not None:
+                sl(8)[d_posc] = sl(4)
         if nu:
             nf, nw, nm = 5 * nu, 5 * len(models), len(models)
             ids = d_mid.to(t.int32)
-            mlat = t.empty(nu, dtype=t.float64, device=dev)
-            raw = t.empty(nu, dtype=t.float64, device=dev)
-            flo = t.empty(nu, dtype=t.uint8, device=dev)
-            flo2 = t.empty(nu, dtype=t.uint8, device=dev)
             base = d_flt.data_ptr()
-            for fl_off, o_lat, o_flo in ((nf + nw + nm, mlat, flo), (nf + nw + 2 * nm, raw, flo2)):
-                _native.check(lib.pm2l_membound_predict(
-                    base, ids.data_ptr(), nu, base + 8 * nf, base + 8 * (nf + nw),
-                    base + 8 * fl_off, nm, o_lat.data_ptr(), o_flo.data_ptr(), s),
-                    "pm2l_membound_predict")
-            parts += [mlat, raw, flo]
-            if lay is not None:
-                lay[d_posu] = mlat
+            _native.check(lib.pm2l_membound_predict_raw(
+                base, ids.data_ptr(), nu, base + 8 * nf, base + 8 * (nf + nw),
+                base + 8 * (nf + nw + nm), nm, bp + 8 * starts[5], bp + 8 * starts[7],
+                bp + 8 * starts[6], s), "pm2l_membound_predict_raw")
+            if offsets is not None:
+                sl(8)[d_posu] = sl(5)
         totals = None
         if offsets is not None and nseg > 0:
-            totals = t.empty(nseg, dtype=t.float64, device=dev)
-            _native.check(lib.pm2l_segment_fsum(lay.data_ptr(), d_off.data_ptr(), nseg,
-                                                totals.data_ptr(), s), "pm2l_segment_fsum")
-            parts.append(totals)
-        if parts:
-            blob = t.cat([p.reshape(-1).view(t.uint8) for p in parts]).cpu().numpy()
-            views, o = [], 0
-            for p in parts:
-                nb = p.numel() * p.element_size()
-                views.append(blob[o:o + nb].view(_np_dtype(p.dtype)).reshape(tuple(p.shape)))
-                o += nb
-            if totals is not None:
-                totals = views.pop()
+            _native.check(lib.pm2l_segment_fsum(bp + 8 * starts[8], d_off.data_ptr(), nseg,
+                                                bp + 8 * starts[9], s), "pm2l_segment_fsum")
+        host = _staged_download(buf)
+        v = lambda k, dt_: host[8 * starts[k]:8 * starts[k + 1]].view(dt_)  # noqa: E731
+        if offsets is not None and nseg > 0:
+            totals = v(9, np.float64).copy()
         if nc:
-            rec, match, dist, cid, lat, det = views[:6]
-            views = views[6:]
-            curves = self.all_curves()
+            ints32 = v(0, np.int32)
+            cur, rec = ints32[:nc], ints32[nc:2 * nc]
+            match = v(1, np.int8)[:nc]
+            dist = v(2, np.float64)
+            det = v(3, np.float64).reshape(nc, 4)
+            lat = v(4, np.float64)
+        if nu:
+            mlat, raw, flo = v(5, np.float64), v(6, np.float64), v(7, np.uint8)[:nu]
+        if nc:
             o = 0
             for triple, idx in by_triple.items():
-                recs = self.resolver.triple_tables(*triple)[0]
+                recs, clist = self.resolver.triple_tables(*triple)[:2]
                 for j, i in enumerate(idx, start=o):
                     if match[j] == -2:
                         errors[i] = wrap(i, ValidationError(
                             f"shape {layers[i].shape.as_tuple()}: invalid coordinate"))
                         continue
                     key = recs[int(rec[j])].chosen_key
-                    if cid[j] < 0:
+                    if match[j] == -3:
+                        errors[i] = wrap(i, ValidationError(
+                            f"shape {layers[i].shape.as_tuple()}: block count exceeds 2^64"))
+                        continue
+                    if cur[j] < 0:
                         errors[i] = UnresolvedLayer(
                             f"layer {layers[i].layer_id!r}: resolved kernel has no throughput "
                             f"curve (family={layers[i].family}, algo={key.algorithm_id})")
                         continue
-                    c = curves[int(cid[j])]
+                    c = clist[int(cur[j])]
                     try:
                         _check_pair(key, c)
                     except PredictionError as exc:
                         errors[i] = wrap(i, exc)
-                        continue
-                    if np.isnan(lat[j]):
-                        errors[i] = wrap(i, ValidationError(
-                            f"shape {layers[i].shape.as_tuple()}: block count exceeds 2^64"))
                         continue
                     m = MATCH_EXACT if match[j] == 0 else MATCH_NEAREST
                     kk = layers[i].shape.k
@@ -333,7 +305,6 @@ class ModelPredictor:
                     out[i] = (Prediction(float(lat[j]), key, comps), PREDICTOR_COMPUTE, flags)
                 o += len(idx)
         if nu:
-            mlat, raw, flo = views[:3]
             for j, i in enumerate(util_ok):
                 key = KernelKey.for_utility(models[mids[j]].kernel_name, layers[i].dtype)
                 comps = {"raw_us": float(raw[j]), "floor_us": self.floor_us,
@@ -368,6 +339,22 @@ def _staged_upload(a: np.ndarray, dev):
     if a.size:
         buf[:a.size].numpy()[:] = a
     return buf[:max(a.size, 0)].to(dev, non_blocking=True)
+
+
+def _staged_download(d) -> np.ndarray:
+    """A device tensor's bytes into a reused page-locked buffer (one copy on
+    the current stream, then a stream synchronize); returns a uint8 view,
+    valid until the next call."""
+    import torch
+    nb = d.numel() * d.element_size()
+    buf = _PINNED.get("down")
+    if buf is None or buf.numel() < nb:
+        buf = _PINNED["down"] = torch.empty(max(4096, 1 << int(max(nb, 1) - 1).bit_length()),
+                                            dtype=torch.uint8, pin_memory=True)
+    if nb:
+        buf[:nb].copy_(d.reshape(-1).view(torch.uint8), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return buf[:nb].numpy()
 
 
 _PREDICTORS: Dict[tuple, tuple] = {}
@@ -483,7 +470,7 @@ def predict_model_grid(template: Sequence[TemplateLayer], shapes, features, data
         match = _device.empty(len(s), "int8", dev)
         _native.check(_native.load().pm2l_points_predict_ext(
             dt.handle, _native.ptr(d_s), len(s), _native.ptr(ext_c), _native.ptr(ext_l), n_ext,
-            _native.ptr(out), 0, 0, _native.ptr(match), 0, 0,
+            _native.ptr(out), 0, 0, _native.ptr(match), 0, 0, 0,
             _device.stream()), "pm2l_points_predict_ext")
         match = _device.to_numpy(match)
         if (match == -3).any():

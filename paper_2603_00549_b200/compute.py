@@ -306,7 +306,7 @@ class ConfigResolver:
         dist = _device.empty(n, "float64", dev)
         _native.check(_native.load().pm2l_points_predict_ext(
             dt.handle, _native.ptr(d_s), n, _native.ptr(ext_c), _native.ptr(ext_l), n_ext,
-            _native.ptr(lat), 0, 0, _native.ptr(match), _native.ptr(rec), _native.ptr(dist),
+            _native.ptr(lat), 0, 0, _native.ptr(match), _native.ptr(rec), _native.ptr(dist), 0,
             _device.stream()), "pm2l_points_predict_ext")
         match = _device.to_numpy(match)
         if (match == -2).any():

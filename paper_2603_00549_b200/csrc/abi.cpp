@@ -591,7 +591,7 @@ int pm2l_points_predict_ext(pm2l_tables* t, const uint32_t* shapes, int64_t n,
                             const uint32_t* ext_coords, const double* ext_log2, int64_t n_ext,
                             double* out_lat, int32_t* out_curve, uint32_t* out_waves,
                             int8_t* out_match, int32_t* out_record, double* out_dist,
-                            void* stream) {
+                            double* out_detail, void* stream) {
   NvtxRange nvtx_("pm2l_points_predict_ext");
   if (!t) return fail(PM2L_ERR_INVALID, "null tables");
   if (n < 0 || n_ext < 0) return fail(PM2L_ERR_INVALID, "negative count");
@@ -606,7 +606,7 @@ int pm2l_points_predict_ext(pm2l_tables* t, const uint32_t* shapes, int64_t n,
   logs.ext_log = ext_log2;
   logs.n_ext = n_ext;
   const int rc = launch_points(t->dev, shapes, n, logs, out_lat, out_curve, out_waves, out_match,
-                               out_record, out_dist, stream);
+                               out_record, out_dist, out_detail, stream);
   if (rc) return cuda_fail(cudaError_t(rc), "points kernel launch");
   return PM2L_OK;
 }
@@ -615,7 +615,7 @@ int pm2l_points_predict(pm2l_tables* t, const uint32_t* shapes, int64_t n, doubl
                         int32_t* out_curve, uint32_t* out_waves, int8_t* out_match,
                         int32_t* out_record, double* out_dist, void* stream) {
   return pm2l_points_predict_ext(t, shapes, n, nullptr, nullptr, 0, out_lat, out_curve, out_waves,
-                                 out_match, out_record, out_dist, stream);
+                                 out_match, out_record, out_dist, nullptr, stream);
 }
 
 int64_t pm2l_points_log2_table_size(void) { return kLutN; }
@@ -635,18 +635,26 @@ int pm2l_points_predict_curve(pm2l_tables* t, const uint32_t* shapes, const int3
   return PM2L_OK;
 }
 
-int pm2l_membound_predict(const double* features, const int32_t* model_ids, int64_t n,
-                          const double* weights, const double* intercepts, const double* floors,
-                          int64_t n_models, double* out_lat, uint8_t* out_floored, void* stream) {
+int pm2l_membound_predict_raw(const double* features, const int32_t* model_ids, int64_t n,
+                              const double* weights, const double* intercepts,
+                              const double* floors, int64_t n_models, double* out_lat,
+                              uint8_t* out_floored, double* out_raw, void* stream) {
   NvtxRange nvtx_("pm2l_membound_predict");
   if (n < 0 || n_models < 0) return fail(PM2L_ERR_INVALID, "negative count");
   if (n > 0 && (!features || !model_ids || !out_lat || !weights || !intercepts || !floors))
     return fail(PM2L_ERR_INVALID, "null membound argument");
   if (int rc = check_device()) return rc;
   const int rc = launch_membound(features, model_ids, n, weights, intercepts, floors, n_models,
-                                 out_lat, out_floored, stream);
+                                 out_lat, out_floored, out_raw, stream);
   if (rc) return cuda_fail(cudaError_t(rc), "membound kernel launch");
   return PM2L_OK;
+}
+
+int pm2l_membound_predict(const double* features, const int32_t* model_ids, int64_t n,
+                          const double* weights, const double* intercepts, const double* floors,
+                          int64_t n_models, double* out_lat, uint8_t* out_floored, void* stream) {
+  return pm2l_membound_predict_raw(features, model_ids, n, weights, intercepts, floors, n_models,
+                                   out_lat, out_floored, nullptr, stream);
 }
 
 int pm2l_segment_fsum(const double* values, const int64_t* offsets, int64_t n_segments,

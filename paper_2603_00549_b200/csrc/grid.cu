@@ -275,6 +275,7 @@ GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
 
 #ifdef PM2L_TIMING
 // diagnostic build only: device buffers of the per-tile / per-CTA stamps
+}  // namespace
 unsigned long long** timing_buffers() {
   static unsigned long long* b[2] = {nullptr, nullptr};
   if (!b[0]) {
@@ -283,6 +284,7 @@ unsigned long long** timing_buffers() {
   }
   return b;
 }
+namespace {
 #endif
 
 // Launch-shape overrides for tuning experiments (tools/ab_*.sh), read once
@@ -396,6 +398,7 @@ int64_t grid_workspace_elems(const TablesDev& t, const GridDev& g) {
 }
 
 int grid_kernel_path(const TablesDev& t, const GridDev& g, const LaunchOut& out) {
+  if (single_ok(t, g, out)) return 4;
   const GridLaunch gl = plan_grid(t, g, false);
   int nb = 0;
   return plan_rows(t, g, gl, out, &nb).tiles > 0 ? 3 : gl.near;
@@ -406,6 +409,8 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
   if (card == 0) return 0;
+  // single-member tables: one planner-free kernel (its exact hits inline)
+  if (single_ok(t, g, out)) return int(launch_single(t, g, out, stages, s));
   const GridLaunch gl = plan_grid(t, g, false);
   const int64_t nbase = int64_t(t.C) * g.nK, need = nbase + g.n_fix;
   if ((need > 0 && (!ws || ws_elems < need)) || !grid_dims_ok(g, gl) || gl.smem > 227 * 1024 ||
@@ -430,10 +435,12 @@ int launch_grid(const TablesDev& t, const GridDev& g, int64_t /*max_group*/, dou
   const bool v = out.curve != nullptr;
   cudaError_t e = cudaSuccess;
   if ((stages & kStageGrid) && rl.tiles > 0) {
-    e = row_nb == 8   ? launch_rows_t<8>(t, g, rl, base, out, s)
-        : row_nb == 4 ? launch_rows_t<4>(t, g, rl, base, out, s)
-        : row_nb == 2 ? launch_rows_t<2>(t, g, rl, base, out, s)
-                      : launch_rows_t<1>(t, g, rl, base, out, s);
+    GridDev gr = g;
+    gr.plan_ready = g.dev_planned && !(stages & kStageBase);
+    e = row_nb == 8   ? launch_rows_t<8>(t, gr, rl, base, out, s)
+        : row_nb == 4 ? launch_rows_t<4>(t, gr, rl, base, out, s)
+        : row_nb == 2 ? launch_rows_t<2>(t, gr, rl, base, out, s)
+                      : launch_rows_t<1>(t, gr, rl, base, out, s);
   } else if (stages & kStageGrid) {
     e = launch_sweep(t, g, gl, base, out, s);
   }

@@ -123,6 +123,13 @@ inline void row_layout(const TablesDev& t, const GridDev& g, int nb, bool stage_
   rl.smem = o + int64_t(rl.slots) * w;
 }
 
+#ifdef PM2L_TIMING
+unsigned long long** timing_buffers();  // grid.cu: [0] per-tile rows, [1] per-CTA stamps
+#endif
+// single-member tables (grid_single.cu): no planner, no tile builds
+bool single_ok(const TablesDev& t, const GridDev& g, const LaunchOut& out);
+cudaError_t launch_single(const TablesDev& t, const GridDev& g, const LaunchOut& out, int stages,
+                          cudaStream_t s);
 // general k-group sweep kernel (grid_sweep.cu)
 cudaError_t launch_sweep(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
                          const double* base, const LaunchOut& out, cudaStream_t s);

@@ -767,9 +767,10 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     row_prologue<STAGE>(smem, c, t, g, rl, bar);
-    // host plans: the per-k tables are ready now; device plans: the first
-    // writer warp issues them after the planner kernel (below)
-    if (STAGE && !g.dev_planned) row_prologue_k<STAGE>(smem, c, g, rl, bar);
+    // host plans (and device plans completed by an earlier launch): the
+    // per-k tables are ready now; device plans of this launch sequence: the
+    // first writer warp issues them after the planner kernel (below)
+    if (STAGE && (!g.dev_planned || g.plan_ready)) row_prologue_k<STAGE>(smem, c, g, rl, bar);
   }
   __syncthreads();  // mbarriers initialised before anyone waits on them
   if (warp < P) {
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
         build_w_table<NB, STAGE>(c, g, r0, reinterpret_cast<double*>(wb0 + rl.w_W), lane);
       if (g.dev_planned) {
         pdl_wait();  // the planner kernel's per-k tables are complete and visible
-        if (STAGE && cw == 0 && lane == 0) row_prologue_k<STAGE>(smem, c, g, rl, bar);
+        if (STAGE && cw == 0 && lane == 0 && !g.plan_ready) row_prologue_k<STAGE>(smem, c, g, rl, bar);
       }
       if (tile0 < rl.tiles && !rl.direct) {
         if (STAGE) mbar_wait(bar + 1, 0);

@@ -38,6 +38,7 @@ struct TablesDev {
   int32_t all_gemm = 1; // no row-block curve referenced
   int32_t all_rowblock = 0;  // >= 1 curve referenced, all of them row-block
   int32_t lowest_wins = 0;  // equal logs imply equal coordinates (all < 2^44)
+  int32_t single_mn = 0;    // one member class whose members all share one (log m, log n)
   int32_t n_samples = 0;
   // per curve [C]
   const double* ref_dim = nullptr;
@@ -74,6 +75,9 @@ struct TablesDev {
   const int32_t* grp_start = nullptr;
   const int32_t* grp_size = nullptr;
   const int32_t* grp_class = nullptr;
+  const int32_t* grp_curve0 = nullptr;  // [G] curve of each group's first member (scan order)
+  int32_t n_rec_k = 0;                  // distinct exact-record k values
+  const uint64_t* rec_k = nullptr;      // [n_rec_k] ascending
   // member classes: groups whose member (log m, log n) sequences are equal
   // share one D sequence and one staircase per (m, n) row (the shipped
   // presets collect every kernel at every sample k, so all k-groups of a
@@ -197,6 +201,10 @@ struct GridDev {
   // ib == -1 for records off the slice); status collects axis violations
   // (kPlanBad*), 0 for a valid plan.
   int32_t dev_planned = 0;
+  // device plan already complete when the grid kernel launches (the planner
+  // ran in an earlier launch, not as this launch's PDL primary): the per-k
+  // tables are fetched at kernel entry instead of after griddepcontrol.wait
+  int32_t plan_ready = 0;
   // device plans: per (m, n) row the [lo, hi) range of its records in the
   // fix-up list (entries of records off the slice have ib == -1 and
   // fix_pos == -1); null for host plans (fixr_off)
@@ -285,13 +293,13 @@ struct LogSource {
 };
 int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const LogSource& logs,
                   double* out_lat, int32_t* out_curve, uint32_t* out_waves, int8_t* out_match,
-                  int32_t* out_record, double* out_dist, void* stream);
+                  int32_t* out_record, double* out_dist, double* out_detail, void* stream);
 int launch_points_curve(const TablesDev& t, const uint32_t* shapes, const int32_t* curves,
                         int64_t n, double* out_lat, uint32_t* out_waves, double* out_detail,
                         void* stream);
 int launch_membound(const double* f, const int32_t* mid, int64_t n, const double* w,
                     const double* b, const double* floors, int64_t n_models, double* out,
-                    uint8_t* floored, void* stream);
+                    uint8_t* floored, double* out_raw, void* stream);
 int launch_nan_scan(const double* v, int64_t n, unsigned long long* first, void* stream);
 int64_t store_encode_workspace(int64_t n);
 int launch_store_encode(const double* lat, int64_t n, const uint64_t* B, const uint64_t* M,

@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
                                                           uint32_t* __restrict__ out_waves,
                                                           int8_t* __restrict__ out_match,
                                                           int32_t* __restrict__ out_record,
-                                                          double* __restrict__ out_dist) {
+                                                          double* __restrict__ out_dist,
+                                                          double* __restrict__ out_detail) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr bool kRows = NEARK >= 3;
   const int NR = kRows ? t.rw_n : 0, NCl = kRows ? t.cl_n : 0;
@@ -450,9 +451,15 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
     }
     __syncwarp();
     PointResult r;
-    if (ci >= 0 && !predict_point_checked(t, ci, s.x, s.y, s.z, s.w, base_of(t, ci, s.w), &r)) {
-      match = -3;  // block count past 2^64
-      ci = -1;
+    double thr = 0.0, bse = 0.0;
+    if (ci >= 0) {
+      const double nd = __ull2double_rn(uint64_t(s.w));
+      thr = interp_thr(t, ci, nd);
+      bse = base_from_thr(t, ci, nd, thr);
+      if (!predict_point_checked(t, ci, s.x, s.y, s.z, s.w, bse, &r)) {
+        match = -3;  // block count past 2^64
+        ci = -1;
+      }
     }
     if (!valid) continue;
     if (out_record) out_record[i] = rec;
@@ -462,11 +469,19 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
       out_lat[i] = qnan();
       if (out_curve) out_curve[i] = -1;
       if (out_waves) out_waves[i] = 0;
+      if (out_detail)
+        for (int j = 0; j < 4; ++j) out_detail[4 * i + j] = qnan();
       continue;
     }
     out_lat[i] = r.lat;
     if (out_curve) out_curve[i] = ci;
     if (out_waves) out_waves[i] = waves_u32(r.waves);
+    if (out_detail) {  // Prediction.components: base_us, new_throughput, wave_scale, waves
+      out_detail[4 * i] = bse;
+      out_detail[4 * i + 1] = thr;
+      out_detail[4 * i + 2] = wave_scale(t, ci, r.waves);
+      out_detail[4 * i + 3] = __ull2double_rn(r.waves);
+    }
   }
 }
 
@@ -509,7 +524,7 @@ __global__ void points_curve_kernel(TablesDev t, const uint4* __restrict__ shape
 
 int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const LogSource& logs,
                   double* out_lat, int32_t* out_curve, uint32_t* out_waves, int8_t* out_match,
-                  int32_t* out_record, double* out_dist, void* stream) {
+                  int32_t* out_record, double* out_dist, double* out_detail, void* stream) {
   if (n == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool one = t.NC == 1 && t.lowest_wins;
@@ -527,7 +542,7 @@ int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const L
   }
   const int nb = int(std::min<int64_t>((n + kThreads - 1) / kThreads, int64_t(sm_count()) * 8));
   fn<<<nb, kThreads, smem, s>>>(t, reinterpret_cast<const uint4*>(shapes), n, logs, out_lat,
-                                out_curve, out_waves, out_match, out_record, out_dist);
+                                out_curve, out_waves, out_match, out_record, out_dist, out_detail);
   return int(cudaGetLastError());
 }
 

@@ -19,13 +19,14 @@ __global__ void membound_kernel(const double* __restrict__ f, const int32_t* __r
                                 int64_t n, const double* __restrict__ w,
                                 const double* __restrict__ icpt, const double* __restrict__ floors,
                                 int64_t n_models, double* __restrict__ out,
-                                uint8_t* __restrict__ floored) {
+                                uint8_t* __restrict__ floored, double* __restrict__ out_raw) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int mi = mid[i];
     if (mi < 0 || mi >= n_models) {
       out[i] = qnan();
       if (floored) floored[i] = 0;
+      if (out_raw) out_raw[i] = qnan();
       continue;
     }
     const double* x = f + 5 * i;
@@ -38,6 +39,7 @@ __global__ void membound_kernel(const double* __restrict__ f, const int32_t* __r
     const bool below = raw < fl;
     out[i] = below ? fl : raw;
     if (floored) floored[i] = below ? 1 : 0;
+    if (out_raw) out_raw[i] = raw;
   }
 }
 
@@ -217,11 +219,12 @@ __global__ void segment_fsum_kernel(const double* __restrict__ v, const int64_t*
 
 int launch_membound(const double* f, const int32_t* mid, int64_t n, const double* w,
                     const double* b, const double* floors, int64_t n_models, double* out,
-                    uint8_t* floored, void* stream) {
+                    uint8_t* floored, double* out_raw, void* stream) {
   if (n == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int nb = int(std::min<int64_t>((n + kThreads - 1) / kThreads, int64_t(sm_count()) * 16));
-  membound_kernel<<<nb, kThreads, 0, s>>>(f, mid, n, w, b, floors, n_models, out, floored);
+  membound_kernel<<<nb, kThreads, 0, s>>>(f, mid, n, w, b, floors, n_models, out, floored,
+                                          out_raw);
   return int(cudaGetLastError());
 }
 

@@ -347,6 +347,15 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
       small = small && v->log_m[i] < 44.0 && v->log_n[i] < 44.0 && v->log_k[i] < 44.0;
     t.lowest_wins = small ? 1 : 0;
   }
+  {
+    // every member of the one class at one (log m, log n): batch values are
+    // the only difference, so the first member (scan order) attains every
+    // row's minimum (grid_single.cu)
+    bool one = cls_start.size() == 1 && !cls_lm.empty();
+    for (size_t j = 1; one && j < cls_lm.size(); ++j)
+      one = std::memcmp(&cls_lm[j], &cls_lm[0], 8) == 0 && std::memcmp(&cls_ln[j], &cls_ln[0], 8) == 0;
+    t.single_mn = one ? 1 : 0;
+  }
   t.ref_dim = blob.add(v->ref_dim, C);
   t.ref_dur = blob.add(v->ref_dur, C);
   t.ref_thr = blob.add(v->ref_thr, C);
@@ -373,6 +382,17 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.wcp = blob.add(wcp);
   t.grp_lk = blob.add(grp_lk);
   t.grp_start = blob.add(grp_start);
+  {
+    std::vector<int32_t> gc0(grp_start.size());
+    for (size_t gi = 0; gi < grp_start.size(); ++gi) gc0[gi] = g_curve[grp_start[gi]];
+    t.grp_curve0 = blob.add(gc0);
+    std::vector<uint64_t> rk;
+    for (int64_t i = 0; i < R; ++i) rk.push_back(ex[i][3]);
+    std::sort(rk.begin(), rk.end());
+    rk.erase(std::unique(rk.begin(), rk.end()), rk.end());
+    t.n_rec_k = int32_t(rk.size());
+    t.rec_k = blob.add(rk);
+  }
   t.grp_size = blob.add(grp_size);
   t.grp_class = blob.add(grp_class);
   t.NC = int32_t(cls_start.size());
@@ -419,6 +439,7 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.g_cw = shift(o.g_cw, base); t.wcp = shift(o.wcp, base);
   t.grp_lk = shift(o.grp_lk, base); t.grp_start = shift(o.grp_start, base);
   t.grp_size = shift(o.grp_size, base); t.grp_class = shift(o.grp_class, base);
+  t.grp_curve0 = shift(o.grp_curve0, base); t.rec_k = shift(o.rec_k, base);
   t.cls_start = shift(o.cls_start, base); t.cls_size = shift(o.cls_size, base);
   t.cls_lm = shift(o.cls_lm, base); t.cls_ln = shift(o.cls_ln, base);
   t.ex_coord = shift(o.ex_coord, base); t.ex_curve = shift(o.ex_curve, base);

@@ -68,10 +68,11 @@ def host_vs_device(dt, axes, b_lo=0, b_hi=None, verify=True):
             assert np.array_equal(d[k], h[k]), k
         assert np.array_equal(_bits(d["vlat"]), _bits(h["vlat"]))
     assert dp.status() == 0
-    assert dp.fixups() == plan.n_fixups
     probe = torch.empty(n, dtype=torch.float64, device=dev)
     dp.launch(d_axes, probe, b_lo=b_lo, b_hi=b_hi)
     assert dp.kernel_path() == plan.kernel_path(probe)
+    if dp.kernel_path() != 4:   # the single-member kernel runs no planner (no fix-up list)
+        assert dp.fixups() == plan.n_fixups
     plan.close()
     dp.close()
     return d["lat"]

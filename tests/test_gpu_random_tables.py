@@ -340,3 +340,77 @@ def test_points_one_class_exact_ties(gpu, seed, dup_batches):
     assert np.array_equal(got[0].view(np.uint64), ref[0].view(np.uint64))
     assert np.array_equal(got[3], ref[3])
     assert np.array_equal(got[5].view(np.uint64), ref[5].view(np.uint64))
+
+
+@pytest.mark.parametrize("seed,rowblock,ties", [(31, True, False), (32, True, True), (33, False, False),
+                                                (34, False, True)])
+def test_single_member_tables(gpu, seed, rowblock, ties):
+    """Tables whose records all share one (m, n) (the attention / triton
+    presets' shape): the planner-free single-member kernel (path 4) through
+    the host plan and the device planner, against the oracle bit for bit --
+    many-row grids, exact hits on several batch values, kernels without a
+    curve (NaN + statistics) and, with ``ties``, k values equidistant from
+    two k-groups (powers of two)."""
+    import math
+    import torch
+    from paper_2603_00549_b200 import _native
+    rng = np.random.default_rng(seed)
+    m0, n0 = (1, 1) if rowblock else (int(rng.integers(16, 512)), int(rng.integers(16, 512)))
+    ks = sorted({2 ** int(e) for e in rng.integers(4, 16, 6)}) if ties else \
+        sorted({int(x) for x in rng.integers(16, 40000, 7)})
+    bs = [1, 3, 96]
+    coords = sorted({(b, m0, n0, k) for b in bs for k in ks}, key=lambda c: (c[1], c[2], c[3], c[0]))
+    co = np.array(coords, np.uint64)
+    R, C = len(co), 5
+    cand = rng.integers(-1, C, R).astype(np.int64)
+    t = {"exact_coords": co, "exact_coords_curve": cand.copy(), "cand_curve": cand, "exact_keys": None}
+    for name, col in (("log_m", 1), ("log_n", 2), ("log_k", 3)):
+        t[name] = np.array([math.log2(int(v)) for v in co[:, col]], np.float64)
+    offs = [0]
+    dims, thrs = [], []
+    for _ in range(C):
+        d = np.sort(rng.choice(np.arange(1, 60000), 8, replace=False)).astype(np.float64)
+        dims += list(d)
+        thrs += list(rng.uniform(1.0, 900.0, 8))
+        offs.append(len(dims))
+    t.update(sample_offsets=np.array(offs, np.int64), sample_dims=np.array(dims),
+             sample_thrs=np.array(thrs), ref_dim=np.array([dims[o - 1] for o in offs[1:]]),
+             ref_dur=rng.uniform(1, 500, C), ref_waves=rng.integers(1, 5, C).astype(np.float64),
+             tile_m=rng.choice([64, 128, 256], C).astype(np.uint64),
+             tile_n=rng.choice([64, 128], C).astype(np.uint64),
+             split_k=rng.choice([1, 2], C).astype(np.uint64),
+             blocks_per_wave=rng.choice([30, 148, 296], C).astype(np.uint64),
+             family_rowblock=np.full(C, 1 if rowblock else 0, np.uint8))
+    t["ref_thr"] = np.array([thrs[o - 1] for o in offs[1:]])
+    dt = _native.DeviceTables(t, 0)
+    B = np.array(sorted(set(bs) | {2, 7, 500}), np.uint64)
+    if rowblock:
+        M = N = np.array([1], np.uint64)
+    else:
+        M = np.array(sorted({m0, 1, 5, 4000} | set(rng.integers(2, 3000, 4).tolist())), np.uint64)
+        N = np.array(sorted({n0, 3, 7000} | set(rng.integers(2, 3000, 3).tolist())), np.uint64)
+    K = np.array(sorted(set(ks) | {3 * k // 2 for k in ks} | set(rng.integers(1, 70000, 500).tolist())),
+                 np.uint64)
+    o_lat = oracle.grid(t, (B, M, N, K), use_coords=True, verify=False)
+    nan = np.isnan(o_lat)
+    # host plan
+    plan = _native.GridPlan(dt, (B, M, N, K))
+    lat = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
+    stats = torch.tensor([-1, 0, 0], dtype=torch.int64, device="cuda")
+    assert plan.kernel_path(lat) == 4
+    plan.launch(lat, nan_stats=stats)
+    assert np.array_equal(lat.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+    st = stats.cpu().numpy()
+    assert st[1] == nan.sum() and st[0] == (int(np.argmax(nan)) if nan.any() else -1)
+    # device planner (device-resident axes)
+    axes = [torch.from_numpy(a.view(np.int64)).cuda() for a in (B, M, N, K)]
+    dp = _native.DeviceGridPlanner(dt, *(len(a) for a in axes))
+    out = torch.full((plan.cardinality,), -1.0, dtype=torch.float64, device="cuda")
+    dp.launch(axes, out, nan_stats=stats)
+    assert dp.kernel_path() == 4 and dp.status() == 0
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), o_lat.view(np.uint64))
+    # a batch sub-slice
+    part = torch.empty((2 * len(M) * len(N) * len(K),), dtype=torch.float64, device="cuda")
+    dp.launch(axes, part, b_lo=1, b_hi=3)
+    inner = len(M) * len(N) * len(K)
+    assert np.array_equal(part.cpu().numpy().view(np.uint64), o_lat[inner:3 * inner].view(np.uint64))

@@ -46,15 +46,32 @@ def main():
         ds = bench.load_bf16()
         grid = bench.grid_for(1)
     prep = PreparedGrid(ds, grid, WaveModel(ds.device.sm_count))
-    plan = _native.GridPlan(prep.device_tables(0), prep.axis_arrays())
-    out = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    print("kernel path", plan.kernel_path(out))
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    mode = os.environ.get("ROW_TIMING_PLAN", "host")   # host | dplan (step) | dplan2 (grid alone)
+    if mode == "host":
+        plan = _native.GridPlan(prep.device_tables(0), prep.axis_arrays())
+        out = torch.empty(plan.cardinality, dtype=torch.float64, device="cuda")
+        print("kernel path", plan.kernel_path(out))
+        run = lambda: plan.launch(out, stages=7)  # noqa: E731
+    else:
+        axes = [torch.from_numpy(np.ascontiguousarray(a, np.uint64).view(np.int64)).cuda()
+                for a in prep.axis_arrays()]
+        dp = _native.DeviceGridPlanner(prep.device_tables(0), *(len(a) for a in axes))
+        out = torch.empty(grid.cardinality, dtype=torch.float64, device="cuda")
+        dp.launch(axes, out)
+        print("kernel path", dp.kernel_path())
+        if mode == "dplan":
+            run = lambda: dp.launch(axes, out)  # noqa: E731
+        else:
+            def run():
+                dp.launch(axes, out, stages=1)
+                torch.cuda.synchronize()
+                dp.launch(axes, out, stages=2)
     for _ in range(5):
         flush.zero_()
         ev[0].record()
-        plan.launch(out, stages=7)
+        run()
         ev[1].record()
     torch.cuda.synchronize()
     print("step ms (last)", ev[0].elapsed_time(ev[1]))
