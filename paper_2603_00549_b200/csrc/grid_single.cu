@@ -296,7 +296,16 @@ cudaError_t launch_single(const TablesDev& t, const GridDev& g, const LaunchOut&
     const int64_t nbc = (g.b_hi - g.b_lo + kSingleBatch - 1) / kSingleBatch;
     const int64_t work = g.nM * g.nN * g.nK * nbc;
     const int64_t want = (work + kSingleThreads - 1) / kSingleThreads;
-    const int ctas = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sm_count()) * 32)));
+    // persistent: one wave of resident CTAs (each stages the tables once)
+    static int resident = 0;
+    if (!resident) {
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, single_kernel<true>, kSingleThreads, 0) !=
+              cudaSuccess || per_sm < 1)
+        per_sm = 2;
+      resident = per_sm;
+    }
+    const int ctas = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sm_count()) * resident)));
     SingleLaunch sl{};
 #ifdef PM2L_TIMING
     sl.dbg = timing_buffers()[1];
