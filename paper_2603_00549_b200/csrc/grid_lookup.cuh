@@ -720,8 +720,18 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
       if (ci < 0) {
         *o = qnan();
       } else {
-        const uint64_t* c4 = g.fix_coord + 4 * int64_t(fe.fix);
-        *o = predict_point(t, ci, c4[0], c4[1], c4[2], c4[3], base_tab[ci * nK + fe.ik]).lat;
+        // the record's curve: base(curve, k) x the wave scale of its wave
+        // class for this batch value -- the tile's W table (GEMM), or the
+        // row-block scale from the staged class parameters: no dependent
+        // global loads on a tile's last writer
+        const double bse = base_tab[ci * nK + fe.ik];
+        const int ibl = fe.ib - x.slab * NB;
+        if (RB) {
+          const uint64_t b = uint64_t(__double_as_longlong(W[ibl]));
+          *o = __dmul_rn(bse, rb_scale(c.wcp[fe.wc], b, g.K[fe.ik]));
+        } else {
+          *o = __dmul_rn(bse, W[fe.wc * NB + ibl]);
+        }
       }
     }
   }

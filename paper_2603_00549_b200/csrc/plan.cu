@@ -242,7 +242,8 @@ __device__ void plan_records(const TablesDev& t, const GridDev& g, const PlanArg
   const int64_t ik = jn < 0 ? -1 : find_sorted(Ks, g.nK, c4[3]);
   const bool on = ik >= 0;
   const int32_t ci = t.ex_mn_curve[r];
-  const_cast<FixEntry*>(g.fixr)[r] = FixEntry{on ? int32_t(ik) : -1, on ? int32_t(ib) : -1, ci, r};
+  const_cast<FixEntry*>(g.fixr)[r] =
+      FixEntry{on ? int32_t(ik) : -1, on ? int32_t(ib) : -1, ci, ci >= 0 ? t.wc_of[ci] : -1};
   const_cast<int64_t*>(g.fix_pos)[r] = on ? ((ib * g.nM + im) * g.nN + jn) * g.nK + ik : -1;
 }
 

@@ -158,7 +158,8 @@ struct alignas(16) FixEntry {
   int32_t ik;     // k index
   int32_t ib;     // batch index, slice-relative
   int32_t curve;  // recorded kernel's curve (-1: no curve -> NaN)
-  int32_t fix;    // index into the flat fix-up list (fix_pos / fix_coord)
+  int32_t wc;     // wave class of the curve (-1 without a curve): the lookup
+                  // kernel rescales the tile's base by its W table entry
 };
 
 // Per-launch grid description (device pointers into one per-call upload).

@@ -588,12 +588,13 @@ std::string build_grid(const TablesHost& th, const uint64_t* const axes[4],
   fixr.resize(fix_pos.size());
   {
     std::vector<int32_t> fill(fixr_off.begin(), fixr_off.end() - 1);
-    size_t i = 0;
+    const int32_t* wc_of = reinterpret_cast<const int32_t*>(
+        th.blob.data() + reinterpret_cast<uintptr_t>(tt.wc_of));
     for (auto& [pos, val] : fix) {
       const int64_t ib = pos / inner, rem = pos - ib * inner;
       const int64_t row = rem / nK, ik = rem - row * nK;
-      fixr[fill[row]++] = FixEntry{int32_t(ik), int32_t(ib), val.second, int32_t(i)};
-      ++i;
+      const int32_t ci = val.second;
+      fixr[fill[row]++] = FixEntry{int32_t(ik), int32_t(ib), ci, ci >= 0 ? wc_of[ci] : -1};
     }
   }
 
