@@ -106,7 +106,11 @@ def load(required: bool = True):
                     f"{_LIB_PATH} is not built (run __graft_entry__.build() or "
                     f"python -m paper_2603_00549_b200._build); there is no CPU fallback")
             lib = C.CDLL(_LIB_PATH)
+            ab = bool(os.environ.get("PM2L_LIB_PATH"))  # diagnostic / A-B builds
             for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name, None)
+                if fn is None and ab:   # an older build: entry points it lacks stay unbound
+                    continue
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -290,7 +290,7 @@ namespace {
 // Launch-shape overrides for tuning experiments (tools/ab_*.sh), read once
 // per process -- never on the launch path.  PM2L_DEBUG_PLAN prints the plan.
 struct Tuning {
-  int nb = 0, prod = 0, slots = 0, ctas = 0, direct = -1;
+  int nb = 0, prod = 0, slots = 0, ctas = 0;
   bool debug = false;
 };
 const Tuning& tuning() {
@@ -304,7 +304,6 @@ const Tuning& tuning() {
     t.prod = geti("PM2L_RING_PROD");
     t.slots = geti("PM2L_RING_SLOTS");
     t.ctas = geti("PM2L_ROW_CTAS");
-    if (const char* e = std::getenv("PM2L_ROW_DIRECT")) t.direct = std::atoi(e);
     t.debug = std::getenv("PM2L_DEBUG_PLAN") != nullptr;
     return t;
   }();
@@ -356,7 +355,8 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
   // ranks, a map serves NB batch values) or the per-k closed-form resolve
   // (row-block grids: one (m, n) row and a long k axis, where the planner's
   // k ranks would dominate a plan-inclusive launch)
-  rl.direct = tu.direct >= 0 ? (tu.direct != 0) : (t.all_rowblock ? 1 : 0);
+  // (device code keys the variant on the row-block template parameter)
+  rl.direct = t.all_rowblock ? 1 : 0;
   rl.prod = tu.prod > 0 ? std::min(tu.prod, kRowWarps - 1) : kRingProd;
   rl.slots = tu.slots > 0 ? std::min(tu.slots, kRingMaxSlots) : kRingSlots;
   const int64_t tiles = g.nM * g.nN * rl.nbs * rl.nkc;

@@ -318,7 +318,7 @@ __device__ __forceinline__ void build_tile(const RowCtx<STAGE>& c, const GridDev
       if (lane == ib) W[ib] = __longlong_as_double(static_cast<long long>(cur.b[ib]));
   }
   __syncwarp();
-  if (rl.direct) {
+  if (RB) {  // row-block tables resolve per k in closed form (rl.direct)
     // per-k closed form at emission: the tile state is the staircase, its
     // minimum and first minimiser, and the W table
     if (lane == 0) {
@@ -568,7 +568,7 @@ __device__ __forceinline__ void emit_tile(const RowCtx<STAGE>& c, const TablesDe
     for (int u = 0; u < U; ++u) {
       pp[u] = (bq + u * bstep) * 32 + lane;
       const int p = min(pp[u], nP - 1);
-      if (rl.direct) {
+      if (RB) {  // compile-time: the GEMM emission loop carries no direct-resolve code
         v[u][0] = resolve(c.ki[k0 + 2 * p]);
         v[u][1] = has_second(p) ? resolve(c.ki[k0 + 2 * p + 1]) : v[u][0];
       } else {
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
       build_tile<NB, STAGE, SEGW, RB>(c, g, rl, tile_xy(rl, tile, c.nK), cur,
                                   smem + rl.off_warp + slot * rl.warp_bytes, lane, tile,
                                   /*with_w=*/j >= nhelp,
-                                  j < nhelp && !rl.direct ? sready + j : nullptr,
+                                  j < nhelp && !RB ? sready + j : nullptr,
                                   first ? bar + 1 : nullptr, first && g.dev_planned);
       __syncwarp();
       ROW_MARK(tile, 2);
@@ -827,7 +827,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) grid_ring_kernel(TablesDev 
         pdl_wait();  // the planner kernel's per-k tables are complete and visible
         if (STAGE && cw == 0 && lane == 0 && !g.plan_ready) row_prologue_k<STAGE>(smem, c, g, rl, bar);
       }
-      if (tile0 < rl.tiles && !rl.direct) {
+      if (tile0 < rl.tiles && !RB) {
         if (STAGE) mbar_wait(bar + 1, 0);
         mbar_wait(sready + cw, 0);  // the builder's staircase is published
         help_group_map<STAGE, SEGW>(c, g, rl, tile_xy(rl, tile0, c.nK), wb0, lane);
