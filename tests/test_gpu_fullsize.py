@@ -239,3 +239,36 @@ def test_mode_x_full_c2_grid_sample_matches_oracle(gpu):
         res = list(pool.map(lambda p: oracle.points_curve(t, shapes[p], ci[p])[0], parts))
     assert np.array_equal(_bits(got), _bits(np.concatenate(res)))
     assert bool(torch.isfinite(allc).all())
+
+
+def test_c4_nas_grid_matches_reference_predict_model(gpu):
+    """C4 (BASELINE configs[3], tools/c4.py): all 2,142 transformer-block
+    models through the array path (predict_model_grid: one resolution +
+    prediction launch per kernel triple, one membound batch, exact segmented
+    fsum) and a seeded subset through the object API (predict_models),
+    against the reference's own predict_model (tests/golden/c4.npz,
+    make_golden_c4.py): every per-layer latency and every fsum total
+    bit-identical."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "tools"))
+    import c4
+    from conftest import GOLDEN
+    from paper_2603_00549_b200.aggregate import TemplateLayer, predict_model_grid, predict_models
+    from paper_2603_00549_b200.core import DType
+    z = np.load(os.path.join(GOLDEN, "c4.npz"))
+    params = [tuple(int(x) for x in p) for p in z["params"]]
+    ds = dataset("fp32_full")
+    fams = ("linear", "linear", "linear", "batched_matmul", "utility:softmax", "linear", "linear",
+            "linear")
+    template = [TemplateLayer(i, f, DType.FP32) for i, f in zip(c4.TEMPLATE_IDS, fams)]
+    shapes, feats = c4.grid_arrays(params)
+    lat, totals = predict_model_grid(template, shapes, feats, ds)
+    assert np.array_equal(_bits(lat), _bits(z["lat"]))
+    assert np.array_equal(_bits(totals), _bits(z["total"]))
+    sel = np.random.default_rng(4).choice(len(params), 120, replace=False)
+    res = predict_models([c4.block(*params[i]) for i in sel], ds)
+    for r, i in zip(res, sel):
+        assert r.total_latency_us.hex() == float(z["total"][i]).hex()
+        assert [lp.prediction.latency_us.hex() for lp in r.per_layer] == \
+            [float(x).hex() for x in z["lat"][i]]
