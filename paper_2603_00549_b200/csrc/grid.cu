@@ -358,7 +358,7 @@ RowLaunch plan_rows(const TablesDev& t, const GridDev& g, const GridLaunch& gl,
   // (device code keys the variant on the row-block template parameter)
   rl.direct = t.all_rowblock ? 1 : 0;
   rl.prod = tu.prod > 0 ? std::min(tu.prod, kRowWarps - 1) : kRingProd;
-  rl.slots = tu.slots > 0 ? std::min(tu.slots, kRingMaxSlots) : kRingSlots;
+  rl.slots = tu.slots > 0 ? std::min(tu.slots, kRingMaxSlots) : stage_k ? kRingSlotsStaged : kRingSlots;
   const int64_t tiles = g.nM * g.nN * rl.nbs * rl.nkc;
   if (tiles > 0x7FFFFFFFll || t.G + t.CM > 4096) return rl;
   row_layout(t, g, NB, stage_k, rl);

@@ -46,7 +46,8 @@ struct GridLaunch {
 
 constexpr int kRowWarps = 8;
 constexpr int kRingProd = 4;   // grid_ring_kernel: default builder warps per CTA
-constexpr int kRingSlots = 6;  // default tile-state slots per CTA
+constexpr int kRingSlots = 6;  // default tile-state slots per CTA (k axes longer than a chunk)
+constexpr int kRingSlotsStaged = 4;  // k axis in one staged chunk (C2 sweep of 3 / 4 / 5 / 6 / 8)
 constexpr int kRingMaxSlots = 16;
 constexpr int kRowCtasPerSm = 3;    // __launch_bounds__ minimum of grid_ring_kernel
 constexpr int kSweepCtasPerSm = 3;

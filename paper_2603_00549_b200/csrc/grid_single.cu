@@ -88,28 +88,52 @@ __global__ void __launch_bounds__(kSingleThreads) single_kernel(TablesDev t, Gri
   __shared__ uint8_t c_rb[kSingleMaxCurves];
   SINGLE_MARK(0);
   const int G = t.G, R = t.n_exact, C = t.C, S = t.n_samples, NXK = t.n_rec_k;
-  for (int i = threadIdx.x; i < G; i += blockDim.x) {
-    glk[i] = t.grp_lk[i];
-    gcur[i] = t.grp_curve0[i];
-  }
-  for (int i = threadIdx.x; i < 4 * R; i += blockDim.x) ex[i] = t.ex_coord[i];
-  for (int i = threadIdx.x; i < R; i += blockDim.x) exc[i] = t.ex_curve[i];
-  for (int i = threadIdx.x; i < NXK; i += blockDim.x) exk[i] = t.rec_k[i];
   const int64_t nb = g.b_hi - g.b_lo;
   const bool bstage = nb <= kSingleMaxB;
-  for (int i = threadIdx.x; bstage && i < nb; i += blockDim.x) bsm[i] = g.B[g.b_lo + i];
-  for (int i = threadIdx.x; i <= C; i += blockDim.x) c_off[i] = t.s_off[i];
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
-    c_dims[i] = t.s_dims[i];
-    c_thrs[i] = t.s_thrs[i];
-  }
-  for (int i = threadIdx.x; i < C; i += blockDim.x) {
-    c_ref[3 * i] = t.ref_dur[i];
-    c_ref[3 * i + 1] = t.ref_dim[i];
-    c_ref[3 * i + 2] = t.ref_thr[i];
-    c_rb[i] = t.rowblock[i];
-    const int wc = t.wc_of[i];
-    if (wc >= 0) c_wp[i] = t.wcp[wc];
+  // staging: every array's loads of one index issued together (one memory
+  // round trip for the lot instead of one per array), then the stores
+  {
+    int n_max = G;
+    n_max = max(n_max, 4 * R);
+    n_max = max(n_max, S);
+    n_max = max(n_max, C + 1);
+    n_max = max(n_max, bstage ? int(nb) : 0);
+    for (int i = threadIdx.x; i < n_max; i += blockDim.x) {
+      const bool in_g = i < G, in_x = i < 4 * R, in_r = i < R, in_k = i < NXK, in_s = i < S,
+                 in_c = i < C, in_o = i <= C, in_b = bstage && i < nb;
+      const double v_glk = in_g ? t.grp_lk[i] : 0.0;
+      const int32_t v_gc = in_g ? t.grp_curve0[i] : 0;
+      const uint64_t v_ex = in_x ? t.ex_coord[i] : 0;
+      const int32_t v_exc = in_r ? t.ex_curve[i] : 0;
+      const uint64_t v_exk = in_k ? t.rec_k[i] : 0;
+      const double v_sd = in_s ? t.s_dims[i] : 0.0, v_st = in_s ? t.s_thrs[i] : 0.0;
+      const int32_t v_off = in_o ? t.s_off[i] : 0;
+      const uint64_t v_b = in_b ? g.B[g.b_lo + i] : 0;
+      double v_rd = 0.0, v_rm = 0.0, v_rt = 0.0;
+      uint8_t v_rb = 0;
+      int32_t v_wc = -1;
+      if (in_c) {
+        v_rd = t.ref_dur[i];
+        v_rm = t.ref_dim[i];
+        v_rt = t.ref_thr[i];
+        v_rb = t.rowblock[i];
+        v_wc = t.wc_of[i];
+      }
+      if (in_g) { glk[i] = v_glk; gcur[i] = v_gc; }
+      if (in_x) ex[i] = v_ex;
+      if (in_r) exc[i] = v_exc;
+      if (in_k) exk[i] = v_exk;
+      if (in_s) { c_dims[i] = v_sd; c_thrs[i] = v_st; }
+      if (in_o) c_off[i] = v_off;
+      if (in_b) bsm[i] = v_b;
+      if (in_c) {
+        c_ref[3 * i] = v_rd;
+        c_ref[3 * i + 1] = v_rm;
+        c_ref[3 * i + 2] = v_rt;
+        c_rb[i] = v_rb;
+        if (v_wc >= 0) c_wp[i] = t.wcp[v_wc];
+      }
+    }
   }
   __syncthreads();
   SINGLE_MARK(1);
