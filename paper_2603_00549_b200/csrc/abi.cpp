@@ -123,6 +123,7 @@ int get_lut(int device, double** out) {
   double* d = nullptr;
   PM2L_CUDA(cudaMalloc(&d, kLutN * sizeof(double)));
   PM2L_CUDA(cudaMemcpy(d, host.data(), kLutN * sizeof(double), cudaMemcpyHostToDevice));
+  PM2L_CUDA(cudaDeviceSynchronize());  // complete before any stream may read it
   g_lut[device] = d;
   *out = d;
   return PM2L_OK;
@@ -199,6 +200,10 @@ int dplan_reserve(pm2l_grid_dplan* p, const DPlanCaps& need) {
   p->buf.release();
   PM2L_CUDA(p->buf.reserve(size_t(dplan_bytes(t, c))));
   PM2L_CUDA(cudaMemset(p->buf.ptr, 0, size_t(dplan_bytes(t, c))));
+  // cudaMemset runs on the legacy default stream, which the callers'
+  // non-blocking streams do not order against: without this wait the zero
+  // fill could land after (and erase) the first call's axis upload
+  PM2L_CUDA(cudaDeviceSynchronize());
   PM2L_CUDA(p->workspace.reserve(size_t(std::max<int64_t>(int64_t(t.C) * c.nK, 1)) * sizeof(double)));
   p->caps = c;
   return PM2L_OK;
@@ -316,6 +321,10 @@ int pm2l_tables_create(const pm2l_tables_view* view, int device, pm2l_tables** o
   if (!t->host.blob.empty())
     PM2L_CUDA(cudaMemcpy(t->blob.ptr, t->host.blob.data(), t->host.blob.size(),
                          cudaMemcpyHostToDevice));
+  // a pageable-source cudaMemcpy may return before its DMA lands, and
+  // launches on non-blocking streams (the drop-in's) are not ordered after
+  // it: the tables must be complete before the handle is handed out
+  PM2L_CUDA(cudaDeviceSynchronize());
   t->dev = rebase(t->host.dev_offsets, t->blob.ptr);
   PM2L_CUDA(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
   *out = t.release();
@@ -399,6 +408,7 @@ int pm2l_grid_plan_create(pm2l_tables* t, const uint64_t* batch_vals, int64_t n_
   p->tables = t;
   PM2L_CUDA(p->blob.reserve(gh.blob.size()));
   PM2L_CUDA(cudaMemcpy(p->blob.ptr, gh.blob.data(), gh.blob.size(), cudaMemcpyHostToDevice));
+  PM2L_CUDA(cudaDeviceSynchronize());  // the plan is complete before any stream may read it
   p->grid = rebase(gh.dev_offsets, p->blob.ptr);
   p->staged_bytes = int64_t(gh.blob.size());
   p->ws_elems = grid_workspace_elems(t->dev, p->grid);
@@ -525,6 +535,7 @@ int pm2l_grid_dplan_status(pm2l_grid_dplan* p, uint32_t* status) {
   PM2L_CUDA(cudaDeviceSynchronize());
   PM2L_CUDA(cudaMemcpy(status, g.status, sizeof(uint32_t), cudaMemcpyDeviceToHost));
   PM2L_CUDA(cudaMemset(g.status, 0, sizeof(uint32_t)));
+  PM2L_CUDA(cudaDeviceSynchronize());  // cleared before any non-blocking stream plans again
   return PM2L_OK;
 }
 

@@ -91,7 +91,20 @@ def test_c2_full_grid_equals_reference_kernel(gpu):
     prep = _prep("bf16", "matmul", "bf16", "nn", _c2_axes())
     ref = _reference(prep)
     got = backend.predict_grid(prep)
-    assert np.array_equal(_bits(got), _bits(ref))
+    if not np.array_equal(_bits(got), _bits(ref)):   # diagnostics for an intermittent mismatch
+        dev = backend.predict_grid_device(prep).cpu().numpy()
+        again = backend.predict_grid(prep)
+        d = np.nonzero(_bits(got) != _bits(ref))[0]
+        try:
+            from cuda.bindings import runtime as cr
+            err, a = cr.cudaPointerGetAttributes(got.ctypes.data)
+            kind = (int(err), int(a.type), hex(int(a.hostPointer or 0)), hex(got.ctypes.data))
+        except Exception as exc:  # diagnostics only
+            kind = repr(exc)
+        raise AssertionError(f"pointer attributes of the result {kind}; "
+            f"predict_grid mismatch: {len(d)} points, nonzero {np.count_nonzero(got)}, first {d[:4]}, "
+            f"device path ok {np.array_equal(_bits(dev), _bits(ref))}, second call ok "
+            f"{np.array_equal(_bits(again), _bits(ref))}, 8 MB chunks {sorted(set((d * 8) >> 23))[:12]}")
     # bench.py's plan-inclusive path: device-resident axes, planner kernel
     axes = [torch.from_numpy(np.ascontiguousarray(a, np.uint64).view(np.int64)).cuda()
             for a in prep.axis_arrays()]
@@ -118,7 +131,14 @@ def test_c3_attention_full_grid_equals_reference_kernel(gpu, family, dtype):
                  {"batch": tuple(bh), "m": (1,), "n": (1,), "k": tuple(range(64, 65536))})
     from paper_2603_00549_b200 import backend
     got = backend.predict_grid(prep)
-    assert np.array_equal(_bits(got), _bits(_reference(prep)))
+    ref = _reference(prep)
+    if not np.array_equal(_bits(got), _bits(ref)):   # diagnostics for an intermittent mismatch
+        from cuda.bindings import runtime as cr
+        err, a = cr.cudaPointerGetAttributes(got.ctypes.data)
+        again = backend.predict_grid(prep)
+        raise AssertionError(f"C3 predict_grid mismatch: nonzero {np.count_nonzero(got)}, pointer "
+                             f"type {int(a.type)}, second call ok "
+                             f"{np.array_equal(_bits(again), _bits(ref))}")
     lat, cur, blk, wav = (x.cpu().numpy() for x in backend.predict_grid_device(prep, verify=True))
     assert np.array_equal(_bits(lat), _bits(got))
 
