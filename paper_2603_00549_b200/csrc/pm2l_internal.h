@@ -105,6 +105,10 @@ struct TablesDev {
   int32_t xh_mask = -1;
   const uint4* xh_key = nullptr;
   const int2* xh_val = nullptr;
+  // per slot a nonzero 32-bit tag of the key (xh_tag below), 0 when empty:
+  // the kernel probes the tags in shared memory and reads the full key only
+  // on a tag match
+  const uint32_t* xh_tags = nullptr;
   // one-class row decomposition of class 0's members: the distinct member
   // (log m) values are rows and the distinct (log n) values columns, both
   // ascending; member (i, j) is present iff bit j of rw_mask[i] (bit i of
@@ -121,6 +125,10 @@ struct TablesDev {
   const uint64_t* cl_mask = nullptr;
   const int32_t* rw_off = nullptr;
   const int32_t* rw_pos = nullptr;
+  // rw_lr[2 * (i * (cl_n + 1) + pc) + {0, 1}]: log n of row i's highest
+  // present column below column insertion point pc / lowest at or above it
+  // (-inf / +inf where none): the row minimum without mask scans
+  const double* rw_lr = nullptr;
 };
 
 #ifdef __CUDACC__
@@ -135,6 +143,15 @@ PM2L_HD uint32_t xh_hash(uint32_t b, uint32_t m, uint32_t n, uint32_t k) {
   h *= 0x2C1B3C6Du;
   h ^= h >> 12;
   return h;
+}
+
+// second, independent mix of the same key: the slot tag (never 0)
+PM2L_HD uint32_t xh_tag(uint32_t b, uint32_t m, uint32_t n, uint32_t k) {
+  uint32_t h = (b * 0xCC9E2D51u) + (m * 0x1B873593u) + (n * 0xE6546B64u) + (k * 0x85EBCA6Bu);
+  h ^= h >> 16;
+  h *= 0x7FEB352Du;
+  h ^= h >> 13;
+  return h | 1u;
 }
 
 // k chunk of the one-class lookup kernel: ranks of the per-k distance are

@@ -14,6 +14,19 @@
 
 #include "common.cuh"
 
+// PTS_VARIANT (diagnostic builds only, wrong results): 1 no nearest search,
+// 2 no prediction tail, 3 no exact lookup, 4 no log2 loads, 5 = 1 + 2
+#ifndef PTS_VARIANT
+#define PTS_VARIANT 0
+#endif
+#ifndef PTS_MINB
+#define PTS_MINB 4  // 64 registers: 4 CTAs per SM (measured best; 5 spills)
+#endif
+
+namespace {
+constexpr int kTagSmemSlots = 4096;  // exact-hash tags staged in shared memory up to 16 KB
+}
+
 namespace pm2l {
 namespace {
 
@@ -120,18 +133,25 @@ __device__ int nearest_point(const TablesDev& t, const PointSmem& S, double qm, 
   return best_i;
 }
 
-// Exact record of a u32 descriptor through the staged hash (TablesDev::xh_*):
-// linear probing from xh_hash until the key or an empty slot.
-__device__ __forceinline__ int exact_hash(const TablesDev& t, uint4 s, int* curve, int* record) {
+// Exact record of a u32 descriptor through the hash (TablesDev::xh_*):
+// linear probing over the slot tags (shared memory when they fit) from
+// xh_hash until the key or an empty slot; the full key is read only on a
+// tag match.
+__device__ __forceinline__ int exact_hash(const TablesDev& t, const uint32_t* tags, uint4 s,
+                                          int* curve, int* record) {
   uint32_t h = xh_hash(s.x, s.y, s.z, s.w) & uint32_t(t.xh_mask);
+  const uint32_t tg = xh_tag(s.x, s.y, s.z, s.w);
   for (;;) {
-    const uint4 k = __ldg(t.xh_key + h);
-    if (k.x == 0) return 0;
-    if (k.x == s.x && k.y == s.y && k.z == s.z && k.w == s.w) {
-      const int2 v = __ldg(t.xh_val + h);
-      *curve = v.x;
-      *record = v.y;
-      return 1;
+    const uint32_t u = tags[h];
+    if (u == 0) return 0;
+    if (u == tg) {
+      const uint4 k = __ldg(t.xh_key + h);
+      if (k.x == s.x && k.y == s.y && k.z == s.z && k.w == s.w) {
+        const int2 v = __ldg(t.xh_val + h);
+        *curve = v.x;
+        *record = v.y;
+        return 1;
+      }
     }
     h = (h + 1) & uint32_t(t.xh_mask);
   }
@@ -156,6 +176,23 @@ __device__ __forceinline__ bool query_log2(const LogSource& L, uint32_t x, doubl
   return false;
 }
 
+struct QueryLogs {
+  double m, n, k;
+  bool ok;
+};
+
+// the three query logs of a descriptor (zero coordinates give ok = false
+// with zeros: the op is invalid and its logs unused)
+__device__ __forceinline__ QueryLogs query_logs(const LogSource& L, uint4 s) {
+  QueryLogs q{0.0, 0.0, 0.0, false};
+  if (s.y && s.z && s.w) {
+    const bool a = query_log2(L, s.y, &q.m), b = query_log2(L, s.z, &q.n),
+               c = query_log2(L, s.w, &q.k);
+    q.ok = a && b && c;
+  }
+  return q;
+}
+
 __device__ __forceinline__ double dabs_sub(double a, double b) { return fabs(__dsub_rn(a, b)); }
 
 // number of v[0..n) below q (v ascending, n >= 0): fixed-trip branchless
@@ -174,44 +211,51 @@ struct RowSmem {
   const uint64_t* cmask;  // [NCl] present rows of each column
   const int32_t* roff;    // [NR+1]
   const int32_t* rpos;    // [members] first position in the class member list
+  const double2* lr;      // [NR x (NCl + 1)] nearest present column per side (TablesDev::rw_lr)
   int NR, NCl;
 };
 
 // The member part of the one-class decision from the row decomposition, with
 // dm_i = |lm_i - qm| per row and dn_j = |ln_j - qn| per column (the member
-// (i, j) has D = max(dm_i, dn_j)):
-//  * row pass: per row the nearest present column to qn is the highest
-//    present column left of qn's insertion point pc or the lowest at or
-//    right of it (dn is V-shaped over the ascending columns: IEEE
-//    subtraction is monotone), so D_i = max(dm_i, nd_i) is the row minimum;
-//    dmin = min_i D_i, and irow = the first row attaining it (strict <);
-//    the rows within mn are collected as a mask;
+// (i, j) has D = max(dm_i, dn_j)).  Rows and columns are ascending, so with
+// pc the insertion point of qn every column distance is a difference of
+// known sign (IEEE subtraction is exact in sign and monotone: |a - b| =
+// b - a for a < b), V-shaped around pc:
+//  * row pass (every row, a fixed trip count: no divergence): per row the
+//    nearest present column is the highest present column below pc or the
+//    lowest at or above it (TablesDev::rw_lr), so D_i = max(dm_i, nd_i) is
+//    the row minimum; dmin = min_i D_i, irow = the first row attaining it
+//    (strict <), and the rows within mn as a mask;
 //  * column pass: the columns within dmin and within mn as masks;
 //  * case A (mn <= dmin): the argmin is the first member with D <= dmin --
 //    row irow (no earlier row reaches dmin), its lowest present column
 //    within dmin;  case B: the first member with D <= mn -- the lowest row
 //    within mn holding a present column within mn, that column.
-// Every row and column is visited once per op (fixed trip counts: no
-// divergence).  Returns the member's class position; *dmin_out = dmin.
+// (Branch-free passes beat outward scans with early exits and lazy
+// column searches here: measured, the divergence costs more than the
+// rows it skips.)
+// Returns the member's class position; *dmin_out = dmin.
 template <class Mask>  // uint32_t when rows and columns are <= 32, else uint64_t
 __device__ __forceinline__ int member_rows(const RowSmem& W, double qm, double qn, double mn,
                                            double* dmin_out) {
   constexpr int kBits = 8 * int(sizeof(Mask));
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
   const int pc = count_below(W.cln, W.NCl, qn);
-  const Mask below = pc >= kBits ? ~Mask(0) : (Mask(1) << pc) - 1;
-  auto clz = [](Mask x) { return kBits == 32 ? __clz(uint32_t(x)) : __clzll(static_cast<long long>(x)); };
   auto ffs = [](Mask x) { return kBits == 32 ? __ffs(uint32_t(x)) : __ffsll(static_cast<long long>(x)); };
+  const int ld = W.NCl + 1;
+  const double2* lr = W.lr + pc;  // row i's neighbours of pc at lr[i * ld]
+  // rw_lr holds -inf for an empty lower side and +inf for an empty upper one
+  auto row_nd = [&](int i) {
+    const double2 v = lr[i * ld];
+    const double dl = __dsub_rn(qn, v.x), dr = __dsub_rn(v.y, qn);
+    return dl < dr ? dl : dr;
+  };
   double dmin = INF;
   int irow = 0;
   Mask rows_mn = 0;
-  for (int i = 0; i < W.NR; ++i) {
-    const Mask P = Mask(W.rmask[i]);
+  for (int i = 0; i < W.NR; ++i) {  // fixed trip count: no divergence
     const double dm = dabs_sub(W.rlm[i], qm);
-    const Mask L = P & below, Rr = P & ~below;
-    const double dl = L ? dabs_sub(W.cln[kBits - 1 - clz(L)], qn) : INF;
-    const double dr = Rr ? dabs_sub(W.cln[ffs(Rr) - 1], qn) : INF;
-    const double nd = dl < dr ? dl : dr;
+    const double nd = row_nd(i);
     const double D = dm > nd ? dm : nd;
     if (D < dmin) {
       dmin = D;
@@ -220,7 +264,7 @@ __device__ __forceinline__ int member_rows(const RowSmem& W, double qm, double q
     rows_mn |= Mask(dm <= mn) << i;
   }
   Mask cols_d = 0, cols_mn = 0;
-  for (int j = 0; j < W.NCl; ++j) {
+  for (int j = 0; j < W.NCl; ++j) {  // the columns within dmin and within mn
     const double dn = dabs_sub(W.cln[j], qn);
     cols_d |= Mask(dn <= dmin) << j;
     cols_mn |= Mask(dn <= mn) << j;
@@ -346,7 +390,7 @@ __device__ __forceinline__ uint32_t waves_u32(uint64_t w) {
 
 template <int NEARK>  // 0 general sweep, 1 sweep + tie mask (G <= 32), 2 one class,
                       // 3 one class by rows (u32 masks), 4 by rows (u64 masks)
-__global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uint4* __restrict__ shapes,
+__global__ void __launch_bounds__(kThreads, PTS_MINB) points_kernel(TablesDev t, const uint4* __restrict__ shapes,
                                                           int64_t n, LogSource L,
                                                           double* __restrict__ out_lat,
                                                           int32_t* __restrict__ out_curve,
@@ -359,7 +403,9 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
   constexpr bool kRows = NEARK >= 3;
   const int NR = kRows ? t.rw_n : 0, NCl = kRows ? t.cl_n : 0;
   const int NP = kRows ? t.rw_off[NR] : 0;
-  uint64_t* rmask = reinterpret_cast<uint64_t*>(smem);
+  double2* lr = reinterpret_cast<double2*>(smem);
+  const int NLR = NR * (NCl + 1);
+  uint64_t* rmask = reinterpret_cast<uint64_t*>(lr + NLR);
   uint64_t* cmask = rmask + NR;
   double* rlm = reinterpret_cast<double*>(cmask + NCl);
   double* cln = rlm + NR;
@@ -383,6 +429,8 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
     cln[j] = t.cl_ln[j];
   }
   for (int j = threadIdx.x; j <= NR && kRows; j += blockDim.x) roff[j] = t.rw_off[j];
+  for (int j = threadIdx.x; j < NLR; j += blockDim.x)
+    lr[j] = reinterpret_cast<const double2*>(t.rw_lr)[j];
   for (int j = threadIdx.x; j < NP; j += blockDim.x) rpos[j] = t.rw_pos[j];
   for (int j = threadIdx.x; j < CMs; j += blockDim.x) {
     lm[j] = t.cls_lm[j];
@@ -398,9 +446,13 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
     csize[j] = t.cls_size[j];
   }
   for (int j = threadIdx.x; j < t.R; j += blockDim.x) gidx[j] = t.g_idx[j];
+  uint32_t* stags = reinterpret_cast<uint32_t*>(rpos + NP);
+  const int ntag = t.xh_mask >= 0 && t.xh_mask < kTagSmemSlots ? t.xh_mask + 1 : 0;
+  for (int j = threadIdx.x; j < ntag; j += blockDim.x) stags[j] = t.xh_tags[j];
+  const uint32_t* tags = ntag ? stags : t.xh_tags;
   __syncthreads();
   const PointSmem S{lm, ln, glk, gcls, gstart, cstart, csize, gidx};
-  const RowSmem W{rlm, cln, rmask, cmask, roff, rpos, NR, NCl};
+  const RowSmem W{rlm, cln, rmask, cmask, roff, rpos, lr, NR, NCl};
   // warp-uniform trip count (every lane runs every iteration, the tail lanes
   // idle), so the warp can be reconverged before the shared prediction tail
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -409,6 +461,7 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
     const int64_t i = base + (threadIdx.x & 31);
     const bool valid = i < n;
     const uint4 s = valid ? shapes[i] : make_uint4(0, 0, 0, 0);
+    const QueryLogs ql = query_logs(L, s);
     int ci = -1, rec = -1;
     int8_t match = -1;
     double dist = 0.0;
@@ -416,25 +469,31 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
     // reconvergence: without it the lanes leave a loop at different trips
     // and run the following nearest search in separate passes
     const bool zero = s.x == 0 || s.y == 0 || s.z == 0 || s.w == 0;
-    const bool hit = !zero && (t.xh_mask >= 0 ? exact_hash(t, s, &ci, &rec)
+#if PTS_VARIANT == 3
+    const bool hit = false;  // diagnostic build: no exact lookup
+#else
+    const bool hit = !zero && (t.xh_mask >= 0 ? exact_hash(t, tags, s, &ci, &rec)
                                               : exact_lookup(t, s.x, s.y, s.z, s.w, &ci, &rec));
+#endif
     __syncwarp();
-    double qm = 0.0, qn = 0.0, qk = 0.0;
-    bool logs = !zero && !hit && t.R > 0;
-    if (logs) {
-      const bool a = query_log2(L, s.y, &qm), b = query_log2(L, s.z, &qn),
-                 c = query_log2(L, s.w, &qk);
-      logs = a && b && c;
-    }
+    double qm = ql.m, qn = ql.n, qk = ql.k;
+    const bool logs = !zero && !hit && t.R > 0 && ql.ok;
+#if PTS_VARIANT == 4
+    qm = double(s.y); qn = double(s.z); qk = double(s.w);  // diagnostic build: no log2 loads
+#endif
     __syncwarp();
     // the nearest search runs in every lane (exact hits and invalid ops are
     // rare; the warp would run it for the others anyway) so it can keep the
     // warp converged; only the lanes that need it keep its answer
     uint64_t best = 0;
     int nrec = -1;
+#if PTS_VARIANT == 1 || PTS_VARIANT == 5
+    nrec = int(s.x) & 7;  // diagnostic build: no nearest search
+#else
     if (t.R > 0)
       nrec = NEARK >= 2 ? nearest_point_one_class<NEARK - 2>(t, S, W, qm, qn, qk, &best)
                         : nearest_point<NEARK == 1>(t, S, qm, qn, qk, &best);
+#endif
     if (zero) {
       match = -2;  // invalid coordinate
     } else if (hit) {
@@ -452,7 +511,12 @@ __global__ void __launch_bounds__(kThreads) points_kernel(TablesDev t, const uin
     __syncwarp();
     PointResult r;
     double thr = 0.0, bse = 0.0;
+#if PTS_VARIANT == 2 || PTS_VARIANT == 5
+    r.lat = qm + qk; r.waves = s.x;  // diagnostic build: no prediction tail
+    if (false) {
+#else
     if (ci >= 0) {
+#endif
       const double nd = __ull2double_rn(uint64_t(s.w));
       thr = interp_thr(t, ci, nd);
       bse = base_from_thr(t, ci, nd, thr);
@@ -530,8 +594,9 @@ int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const L
   const bool one = t.NC == 1 && t.lowest_wins;
   const bool rows = one && t.rw_n > 0;
   const int64_t NR = rows ? t.rw_n : 0, NCl = rows ? t.cl_n : 0;
-  const int64_t smem = 16ll * (NR + NCl) + (rows ? 0 : 16ll * t.CM) + 8ll * t.G + 8ll * t.G +
-                       8ll * t.NC + 4ll * t.R + (rows ? 4ll * (NR + 1 + t.CM) : 0) + 64;
+  const int64_t smem = 16ll * NR * (NCl + 1) + 16ll * (NR + NCl) + (rows ? 0 : 16ll * t.CM) + 8ll * t.G + 8ll * t.G +
+                       8ll * t.NC + 4ll * t.R + (rows ? 4ll * (NR + 1 + t.CM) : 0) +
+                       (t.xh_mask >= 0 && t.xh_mask < kTagSmemSlots ? 4ll * (t.xh_mask + 1) : 0) + 64;
   auto* fn = rows ? (t.rw_n <= 32 && t.cl_n <= 32 ? points_kernel<3> : points_kernel<4>)
              : one ? points_kernel<2>
              : t.G <= 32 ? points_kernel<1> : points_kernel<0>;

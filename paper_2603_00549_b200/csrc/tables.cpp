@@ -8,6 +8,7 @@
 // and the Python resolver's math.log2 (compute.py:261) obtain it — device
 // log2 differs by an ulp on some integers and is never used.
 #include <algorithm>
+#include <limits>
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -270,12 +271,14 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   int32_t xh_mask = -1;
   std::vector<uint4> xh_key;
   std::vector<int2> xh_val;
+  std::vector<uint32_t> xh_tags;
   if (R > 0) {
     int64_t cap = 16;
     while (cap < 2 * R) cap <<= 1;
     xh_mask = int32_t(cap - 1);
     xh_key.assign(size_t(cap), uint4{0, 0, 0, 0});
     xh_val.assign(size_t(cap), int2{-1, -1});
+    xh_tags.assign(size_t(cap), 0u);
     // ex is sorted by shape, stable: equal shapes keep caller order
     for (int64_t i = 0; i < R; ++i) {
       const auto& e = ex[i];
@@ -287,12 +290,14 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
       while (xh_key[h].x) h = (h + 1) & uint32_t(xh_mask);
       xh_key[h] = key;
       xh_val[h] = int2{int32_t(int64_t(e[4])), int32_t(e[5])};
+      xh_tags[h] = xh_tag(key.x, key.y, key.z, key.w);
     }
   }
   // --- row decomposition of class 0 (one member class)
   std::vector<double> rw_lm, cl_ln;
   std::vector<uint64_t> rw_mask, cl_mask;
   std::vector<int32_t> rw_off, rw_pos;
+  std::vector<double> rw_lr;
   if (cls_start.size() == 1) {
     const int32_t CMm = cls_size[0];
     auto bits = [](double x) { uint64_t u; std::memcpy(&u, &x, 8); return u; };
@@ -330,6 +335,21 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
       }
       for (size_t i = 0; i < rows.size(); ++i) rw_off[i + 1] += rw_off[i];
       rw_pos = first_pos;  // seen is lexicographic: row-major, columns ascending
+      // nearest present column of each row on either side of each column
+      // insertion point pc: (log n of the highest present column < pc, of
+      // the lowest present column >= pc), -inf / +inf where the side is
+      // empty (so qn - lower and upper - qn are +inf there)
+      const size_t NCp = cols.size() + 1;
+      const double inf = std::numeric_limits<double>::infinity();
+      rw_lr.assign(2 * rows.size() * NCp, inf);
+      for (size_t e = 0; e < rw_lr.size(); e += 2) rw_lr[e] = -inf;
+      for (size_t i = 0; i < rows.size(); ++i)
+        for (size_t pc = 0; pc < NCp; ++pc) {
+          for (size_t j = pc; j-- > 0;)
+            if (rw_mask[i] >> j & 1) { rw_lr[2 * (i * NCp + pc)] = cols[j]; break; }
+          for (size_t j = pc; j < cols.size(); ++j)
+            if (rw_mask[i] >> j & 1) { rw_lr[2 * (i * NCp + pc) + 1] = cols[j]; break; }
+        }
     }
   }
 
@@ -410,6 +430,7 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.xh_mask = xh_mask;
   t.xh_key = blob.add(xh_key);
   t.xh_val = blob.add(xh_val);
+  t.xh_tags = blob.add(xh_tags);
   t.rw_n = int32_t(rw_lm.size());
   t.cl_n = int32_t(cl_ln.size());
   t.rw_lm = blob.add(rw_lm);
@@ -418,6 +439,7 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.cl_mask = blob.add(cl_mask);
   t.rw_off = blob.add(rw_off);
   t.rw_pos = blob.add(rw_pos);
+  t.rw_lr = blob.add(rw_lr);
   out->blob.swap(blob.bytes());
   out->max_group = max_group;
   return "";
@@ -447,9 +469,11 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.ex_mn_coord = shift(o.ex_mn_coord, base);
   t.ex_mn_curve = shift(o.ex_mn_curve, base);
   t.xh_key = shift(o.xh_key, base); t.xh_val = shift(o.xh_val, base);
+  t.xh_tags = shift(o.xh_tags, base);
   t.rw_lm = shift(o.rw_lm, base); t.cl_ln = shift(o.cl_ln, base);
   t.rw_mask = shift(o.rw_mask, base); t.cl_mask = shift(o.cl_mask, base);
   t.rw_off = shift(o.rw_off, base); t.rw_pos = shift(o.rw_pos, base);
+  t.rw_lr = shift(o.rw_lr, base);
   return t;
 }
 
