@@ -17,7 +17,7 @@
 //
 // Work item = ((m, n) row, k), k fastest so a warp's stores for one batch
 // value are contiguous; the item's resolve and base(curve, k) are done once
-// and the thread walks every batch value of the slice (staged in shared
+// and the thread walks a chunk of the slice's batch values (staged in shared
 // memory), whose points are independent (unrolled for FP64 ILP).
 #include <cstdint>
 
@@ -27,16 +27,20 @@ namespace pm2l {
 namespace gk {
 namespace {
 
+#ifndef SINGLE_MINB
+#define SINGLE_MINB 1
+#endif
 constexpr int kSingleThreads = 256;
 constexpr int kSingleMaxRec = 64;
 constexpr int kSingleMaxGroups = 1024;
 constexpr int kSingleMaxB = 1024;   // batch values staged in shared memory
-constexpr int kSingleBatch = 8;     // batch values per work item
+constexpr int kSingleUnroll = 8;    // batch values per work item, in flight together (FP64 ILP)
 constexpr int kSingleMaxCurves = 32;
 constexpr int kSingleMaxSamples = 512;
 
 struct SingleLaunch {
   FastDiv d_item, d_nK, d_nN;   // work-item index decomposition (32-bit indices)
+  int bchunk;                   // batch values per work item (launch_single)
 #ifdef PM2L_TIMING
   unsigned long long* dbg;  // per CTA: entry, staged, first item resolved, exit (globaltimer)
 #endif
@@ -71,7 +75,7 @@ __device__ __forceinline__ uint64_t rb_waves(const WcParam& p, uint64_t bk) {
 }
 
 template <bool IDX32>
-__global__ void __launch_bounds__(kSingleThreads) single_kernel(TablesDev t, GridDev g,
+__global__ void __launch_bounds__(kSingleThreads, SINGLE_MINB) single_kernel(TablesDev t, GridDev g,
                                                                  SingleLaunch sl, LaunchOut out) {
   __shared__ double glk[kSingleMaxGroups];
   __shared__ int32_t gcur[kSingleMaxGroups];  // curve of each group's first member
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(kSingleThreads) single_kernel(TablesDev t, Gri
   SINGLE_MARK(1);
   const double lm0 = t.cls_lm[0], ln0 = t.cls_ln[0];
   const int64_t nK = g.nK, nMN = g.nM * g.nN, plane = nMN * nK;
-  const int64_t nbc = (nb + kSingleBatch - 1) / kSingleBatch;
+  const int64_t nbc = (nb + sl.bchunk - 1) / sl.bchunk;
   const int64_t per_bc = nMN * nK, work = per_bc * nbc;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   // base(c, k) = (ref_dur * (k / ref_dim)) * (ref_thr / thr(c, k)) from the
@@ -149,7 +153,10 @@ __global__ void __launch_bounds__(kSingleThreads) single_kernel(TablesDev t, Gri
     return __dmul_rn(__dmul_rn(c_ref[3 * c], __ddiv_rn(nd, c_ref[3 * c + 1])),
                      __ddiv_rn(c_ref[3 * c + 2], thr));
   };
-  for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < work; w += stride) {
+  // one work item (per lane); the loop below is warp-uniform so the warp
+  // reconverges after every item (an exact-hit item's slower path would
+  // otherwise leave the warp split for the rest of the loop)
+  auto item = [&](int64_t w) {
     int64_t bc, row, ik, im, jn;
     if (IDX32) {  // magic divisions by the host-computed divisors
       const int wi = int(w);
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(kSingleThreads) single_kernel(TablesDev t, Gri
                       n < uint64_t(g.lut_n) && k < uint64_t(g.lut_n);
       if (!ok) {
         if (g.status) atomicOr(g.status, uint32_t(kPlanBadValue));
-        continue;
+        return;
       }
       qm = g.lut[m];
       qn = g.lut[n];
@@ -222,8 +229,8 @@ __global__ void __launch_bounds__(kSingleThreads) single_kernel(TablesDev t, Gri
     const double nd = __ull2double_rn(k);
     // exact records on this (m, n, k): they can only sit on a recorded k
     int nhit = 0;
-    uint64_t hb[4];
-    int32_t hc[4];
+    uint64_t hb[4] = {0, 0, 0, 0};
+    int32_t hc[4] = {0, 0, 0, 0};
     {
       int lo = 0;
       for (int step = NXK > 0 ? 1 << (31 - __clz(NXK)) : 0; step > 0; step >>= 1)
@@ -233,19 +240,22 @@ __global__ void __launch_bounds__(kSingleThreads) single_kernel(TablesDev t, Gri
           if (ex[4 * r + 3] == k && ex[4 * r + 1] == m && ex[4 * r + 2] == n) {
             const uint64_t rb_ = ex[4 * r];
             bool dup = false;  // a shape recorded twice: the first record wins
-            for (int q = 0; q < nhit && q < 4; ++q) dup |= hb[q] == rb_;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dup |= q < nhit && hb[q] == rb_;
             if (dup) continue;
-            if (nhit < 4) {
-              hb[nhit] = rb_;
-              hc[nhit] = exc[r];
-            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)  // constant indices: registers, not local memory
+              if (q == nhit) {
+                hb[q] = rb_;
+                hc[q] = exc[r];
+              }
             ++nhit;
           }
     }
     if (nhit > 4) nhit = -1;  // more than 4 batch values recorded here: scan per point
-    const int64_t b0 = g.b_lo + bc * kSingleBatch;
-    const int cnt = g.b_hi - b0 < kSingleBatch ? int(g.b_hi - b0) : kSingleBatch;
-    double* o = out.lat + (bc * kSingleBatch * nMN + row) * nK + ik;
+    const int64_t b0 = g.b_lo + bc * sl.bchunk;
+    const int cnt = g.b_hi - b0 < sl.bchunk ? int(g.b_hi - b0) : sl.bchunk;
+    double* o = out.lat + (bc * sl.bchunk * nMN + row) * nK + ik;
     if (w < int64_t(blockDim.x) * gridDim.x) SINGLE_MARK(2);
     // the item's curve, its base and wave parameters once
     double base = 0.0;
@@ -256,43 +266,59 @@ __global__ void __launch_bounds__(kSingleThreads) single_kernel(TablesDev t, Gri
       prm = c_wp[ci];
       rb = c_rb[ci] != 0;
     }
+    const uint64_t* bv = bstage ? bsm + (b0 - g.b_lo) : g.B + b0;
+    uint64_t rowc = 0;  // GEMM: ceil(m / tm) * ceil(n / tn) * split_k, per item
+    if (ci >= 0 && !rb) rowc = ceil_div_p(prm, 0, m, prm.tm) * ceil_div_p(prm, 1, n, prm.tn) * prm.sk;
+    // per batch value: the exact record's curve when (b, m, n, k) is recorded
+    // (nhit > 0: the item's <= 4 recorded batch values; nhit < 0: a scan),
+    // else the item's curve.  Points on the item's curve take the unrolled
+    // arithmetic below; another curve (or none) the general path
+    for (int j0 = 0; j0 < cnt; j0 += kSingleUnroll) {
 #pragma unroll
-    for (int j = 0; j < kSingleBatch; ++j) {
-      if (j >= cnt) break;
-      const int64_t ib = b0 + j - g.b_lo;
-      const uint64_t b = bstage ? bsm[ib] : g.B[g.b_lo + ib];
-      double* oj = o + j * plane;
-      int c = ci;
-      if (nhit != 0) {
+      for (int jj = 0; jj < kSingleUnroll; ++jj) {
+        const int j = j0 + jj;
+        if (j >= cnt) continue;
+        const uint64_t b = bv[j];
+        int c = ci;
         if (nhit > 0) {
-          for (int q = 0; q < nhit; ++q)
-            if (hb[q] == b) c = hc[q];
-        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < nhit && hb[q] == b) c = hc[q];
+        } else if (nhit < 0) {
           for (int r = 0; r < R; ++r)
             if (ex[4 * r] == b && ex[4 * r + 1] == m && ex[4 * r + 2] == n && ex[4 * r + 3] == k) {
               c = exc[r];
               break;
             }
         }
-      }
-      if (c < 0) {
-        *oj = qnan();
-        if (out.nan_stats) {
-          atomicMin(out.nan_stats, (unsigned long long)(oj - out.lat));
-          atomicAdd(out.nan_stats + 1, 1ull);
+        double* oj = o + j * plane;
+        if (c == ci && c >= 0) {
+          const uint64_t wv = rb ? rb_waves(prm, b * k) : ceil_div_p(prm, 2, b * rowc, prm.bpw);
+          const double wd = __ull2double_rn(wv);
+          *oj = __dmul_rn(base, prm.rw == 1.0 ? wd : __ddiv_rn(wd, prm.rw));
+        } else if (c < 0) {
+          *oj = qnan();
+          if (out.nan_stats) {
+            atomicMin(out.nan_stats, (unsigned long long)(oj - out.lat));
+            atomicAdd(out.nan_stats + 1, 1ull);
+          }
+        } else {
+          const WcParam& p = c_wp[c];
+          const double bs = base_of_s(c, nd);
+          const uint64_t wv =
+              c_rb[c] ? rb_waves(p, b * k)
+                      : ceil_div_p(p, 2, b * ceil_div_p(p, 0, m, p.tm) * ceil_div_p(p, 1, n, p.tn) * p.sk,
+                                   p.bpw);
+          const double wd = __ull2double_rn(wv);
+          *oj = __dmul_rn(bs, p.rw == 1.0 ? wd : __ddiv_rn(wd, p.rw));
         }
-        continue;
       }
-      const WcParam& p = c == ci ? prm : c_wp[c];
-      const bool crb = c == ci ? rb : c_rb[c] != 0;
-      const double bs = c == ci ? base : base_of_s(c, nd);
-      const uint64_t wv =
-          crb ? rb_waves(p, b * k)
-              : ceil_div_p(p, 2, b * ceil_div_p(p, 0, m, p.tm) * ceil_div_p(p, 1, n, p.tn) * p.sk,
-                           p.bpw);
-      const double wd = __ull2double_rn(wv);
-      *oj = __dmul_rn(bs, p.rw == 1.0 ? wd : __ddiv_rn(wd, p.rw));
     }
+  };
+  const int lane = threadIdx.x & 31;
+  for (int64_t wb = blockIdx.x * int64_t(blockDim.x) + (threadIdx.x & ~31); wb < work; wb += stride) {
+    if (wb + lane < work) item(wb + lane);
+    __syncwarp();
   }
   __syncthreads();
   SINGLE_MARK(3);
@@ -317,9 +343,6 @@ cudaError_t launch_single(const TablesDev& t, const GridDev& g, const LaunchOut&
                           cudaStream_t s) {
   if ((stages & kStageBase) && out.nan_stats) stats_reset_kernel<<<1, 1, 0, s>>>(out.nan_stats);
   if (stages & kStageGrid) {
-    const int64_t nbc = (g.b_hi - g.b_lo + kSingleBatch - 1) / kSingleBatch;
-    const int64_t work = g.nM * g.nN * g.nK * nbc;
-    const int64_t want = (work + kSingleThreads - 1) / kSingleThreads;
     // persistent: one wave of resident CTAs (each stages the tables once)
     static int resident = 0;
     if (!resident) {
@@ -329,8 +352,17 @@ cudaError_t launch_single(const TablesDev& t, const GridDev& g, const LaunchOut&
         per_sm = 2;
       resident = per_sm;
     }
+    // batch values per work item: one unrolled group (measured: larger
+    // chunks, which share the item's resolve among more batch values, lose
+    // more to the lower thread count than they save)
+    const int64_t nb = g.b_hi - g.b_lo, rows = g.nM * g.nN * g.nK;
+    const int bchunk = kSingleUnroll;
+    const int64_t nbc = (nb + bchunk - 1) / bchunk;
+    const int64_t work = rows * nbc;
+    const int64_t want = (work + kSingleThreads - 1) / kSingleThreads;
     const int ctas = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sm_count()) * resident)));
     SingleLaunch sl{};
+    sl.bchunk = bchunk;
 #ifdef PM2L_TIMING
     sl.dbg = timing_buffers()[1];
 #endif
