@@ -122,3 +122,79 @@ def test_model_grid_rejects_nonpositive_layer(gpu):
         assert (lat2 > 0).all()
         for i in range(len(params)):
             assert tot2[i] == math.fsum(lat2[i])
+
+
+@pytest.mark.parametrize("name", ["matmul_bf16", "exact_mix_bf16", "cutlass_attn_bf16"])
+def test_empty_single_and_partial_slices_through_ffi_slice(gpu, name):
+    """Slice bounds as the reference's callers pass them (_kernels.pyx:76-90,
+    backend.py:64-76): an empty batch slice writes nothing, a one-point grid
+    and a partial batch slice equal the oracle point for point."""
+    prep = prepared(GRIDS[name])
+    t = dict(prep.tables())
+    B, M, N, K = prep.axis_arrays()
+    # empty slice: nothing written
+    out = np.full(4, 7.0)
+    ffi_slice(t, (B, M, N, K), 1, 1, out)
+    assert np.all(out == 7.0)
+    # one point
+    axes1 = (B[:1].copy(), M[-1:].copy(), N[:1].copy(), K[len(K) // 2:len(K) // 2 + 1].copy())
+    out1 = np.empty(1, np.float64)
+    ffi_slice(t, axes1, 0, 1, out1)
+    assert np.array_equal(_bits(out1), _bits(oracle.grid(t, axes1, 0, 1, verify=False)))
+    # a partial slice of the batch axis: the slice's points, in slice order
+    if len(B) > 1:
+        lo, hi = 1, len(B)
+        outp = np.empty((hi - lo) * len(M) * len(N) * len(K), np.float64)
+        ffi_slice(t, (B, M, N, K), lo, hi, outp)
+        want = oracle.grid(t, (B, M, N, K), lo, hi, verify=False)
+        assert np.array_equal(_bits(outp), _bits(want))
+
+
+@pytest.mark.parametrize("name", ["matmul_bf16", "exact_mix_bf16"])
+def test_repeated_and_shuffled_axis_values_through_ffi_slice(gpu, name):
+    """The reference loops over whatever axis arrays it is given: repeated
+    values and shuffled m / n / batch axes must give the oracle's points."""
+    prep = prepared(GRIDS[name])
+    t = dict(prep.tables())
+    B, M, N, K = prep.axis_arrays()
+    rng = np.random.default_rng(5)
+    cases = [
+        (B, M, N, np.repeat(K[:7], 2)),                                   # repeated k
+        (np.repeat(B[:2], 2), M[rng.permutation(len(M))].copy(), N, K),  # repeated b, shuffled m
+        (B[::-1].copy(), M, N[rng.permutation(len(N))].copy(), K),       # reversed b, shuffled n
+    ]
+    for axes in cases:
+        axes = tuple(np.ascontiguousarray(a, np.uint64) for a in axes)
+        n = len(axes[0]) * len(axes[1]) * len(axes[2]) * len(axes[3])
+        out = np.empty(n, np.float64)
+        ffi_slice(t, axes, 0, len(axes[0]), out)
+        want = oracle.grid(t, axes, 0, len(axes[0]), verify=False)
+        assert np.array_equal(_bits(out), _bits(want))
+
+
+def test_points_empty_batch_and_invalid_coordinates(gpu):
+    """Explicit descriptors: an empty batch is a no-op; a zero coordinate is
+    an invalid op (NaN latency, curve -1), as the reference's resolver
+    refuses non-positive shapes (core.py validation)."""
+    import torch
+    from paper_2603_00549_b200 import _native
+    prep = prepared(GRIDS["matmul_bf16"])
+    dt = prep.device_tables(0)
+    lib = _native.load()
+    lat = torch.full((4,), 7.0, dtype=torch.float64, device="cuda")
+    cur = torch.full((4,), 9, dtype=torch.int32, device="cuda")
+    wav = torch.zeros(4, dtype=torch.int32, device="cuda")
+    shapes = torch.tensor([[1, 128, 128, 64], [0, 128, 128, 64], [1, 0, 128, 64], [1, 128, 128, 0]],
+                          dtype=torch.int32, device="cuda")
+    _native.check(lib.pm2l_points_predict(dt.handle, shapes.data_ptr(), 0, lat.data_ptr(),
+                                          cur.data_ptr(), wav.data_ptr(), 0, 0, 0,
+                                          _native.stream_handle()), "points n=0")
+    torch.cuda.synchronize()
+    assert torch.all(lat == 7.0) and torch.all(cur == 9)
+    _native.check(lib.pm2l_points_predict(dt.handle, shapes.data_ptr(), 4, lat.data_ptr(),
+                                          cur.data_ptr(), wav.data_ptr(), 0, 0, 0,
+                                          _native.stream_handle()), "points")
+    torch.cuda.synchronize()
+    l, c = lat.cpu().numpy(), cur.cpu().numpy()
+    assert math.isfinite(l[0]) and c[0] >= 0
+    assert np.all(np.isnan(l[1:])) and np.all(c[1:] == -1)
