@@ -23,8 +23,12 @@
 #define PTS_MINB 4  // 64 registers: 4 CTAs per SM (measured best; 5 spills)
 #endif
 
+#ifndef PTS_PAIR
+#define PTS_PAIR 1  // 2 measured slower (spills at 64 registers, no gain at 80)
+#endif
 namespace {
 constexpr int kTagSmemSlots = 4096;  // exact-hash tags staged in shared memory up to 16 KB
+constexpr int kPointsPerLane = PTS_PAIR;  // one-class ops per lane per iteration (interleaved)
 }
 
 namespace pm2l {
@@ -195,12 +199,20 @@ __device__ __forceinline__ QueryLogs query_logs(const LogSource& L, uint4 s) {
 
 __device__ __forceinline__ double dabs_sub(double a, double b) { return fabs(__dsub_rn(a, b)); }
 
-// number of v[0..n) below q (v ascending, n >= 0): fixed-trip branchless
-// search (the same trip count in every lane: no divergence)
-__device__ __forceinline__ int count_below(const double* v, int n, double q) {
+// smallest power of two > n: sorted shared arrays padded with +inf to it
+// take the unguarded search below
+__host__ __device__ __forceinline__ int pow2_above(int n) {
+  int p = 1;
+  while (p <= n) p <<= 1;
+  return p;
+}
+
+// number of v[0..np2) below q, v ascending and padded with +inf to np2 (a
+// power of two > the real length): the same trip count in every lane and
+// no bounds test per step
+__device__ __forceinline__ int count_below_p2(const double* v, int np2, double q) {
   int pos = 0;
-  for (int step = n > 0 ? 1 << (31 - __clz(n)) : 0; step > 0; step >>= 1)
-    if (pos + step <= n && v[pos + step - 1] < q) pos += step;
+  for (int step = np2 >> 1; step > 0; step >>= 1) pos += v[pos + step - 1] < q ? step : 0;
   return pos;
 }
 
@@ -235,55 +247,72 @@ struct RowSmem {
 // column searches here: measured, the divergence costs more than the
 // rows it skips.)
 // Returns the member's class position; *dmin_out = dmin.
-template <class Mask>  // uint32_t when rows and columns are <= 32, else uint64_t
-__device__ __forceinline__ int member_rows(const RowSmem& W, double qm, double qn, double mn,
-                                           double* dmin_out) {
+template <class Mask, int P>  // Mask: uint32_t when rows and columns are <= 32, else uint64_t;
+                              // P queries interleaved (independent FP64 chains per row)
+__device__ __forceinline__ void member_rows(const RowSmem& W, const double* qm, const double* qn,
+                                            const double* mn, double* dmin_out, int* pos_out) {
   constexpr int kBits = 8 * int(sizeof(Mask));
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
-  const int pc = count_below(W.cln, W.NCl, qn);
   auto ffs = [](Mask x) { return kBits == 32 ? __ffs(uint32_t(x)) : __ffsll(static_cast<long long>(x)); };
-  const int ld = W.NCl + 1;
-  const double2* lr = W.lr + pc;  // row i's neighbours of pc at lr[i * ld]
-  // rw_lr holds -inf for an empty lower side and +inf for an empty upper one
-  auto row_nd = [&](int i) {
-    const double2 v = lr[i * ld];
-    const double dl = __dsub_rn(qn, v.x), dr = __dsub_rn(v.y, qn);
-    return dl < dr ? dl : dr;
-  };
-  double dmin = INF;
-  int irow = 0;
-  Mask rows_mn = 0;
+  const int ld = W.NCl + 1, NClp = pow2_above(W.NCl);
+  const double2* lr[P];
+  double dmin[P];
+  int irow[P];
+  Mask rows_mn[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    lr[p] = W.lr + count_below_p2(W.cln, NClp, qn[p]);  // row i's neighbours of pc at lr[i * ld]
+    dmin[p] = INF;
+    irow[p] = 0;
+    rows_mn[p] = 0;
+  }
   for (int i = 0; i < W.NR; ++i) {  // fixed trip count: no divergence
-    const double dm = dabs_sub(W.rlm[i], qm);
-    const double nd = row_nd(i);
-    const double D = dm > nd ? dm : nd;
-    if (D < dmin) {
-      dmin = D;
-      irow = i;
+    const double lmi = W.rlm[i];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const double dm = dabs_sub(lmi, qm[p]);
+      // rw_lr holds -inf for an empty lower side and +inf for an empty upper one
+      const double2 v = lr[p][i * ld];
+      const double dl = __dsub_rn(qn[p], v.x), dr = __dsub_rn(v.y, qn[p]);
+      const double nd = dl < dr ? dl : dr;
+      const double D = dm > nd ? dm : nd;
+      if (D < dmin[p]) {
+        dmin[p] = D;
+        irow[p] = i;
+      }
+      rows_mn[p] |= Mask(dm <= mn[p]) << i;
     }
-    rows_mn |= Mask(dm <= mn) << i;
   }
-  Mask cols_d = 0, cols_mn = 0;
+  Mask cols_d[P], cols_mn[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) cols_d[p] = cols_mn[p] = 0;
   for (int j = 0; j < W.NCl; ++j) {  // the columns within dmin and within mn
-    const double dn = dabs_sub(W.cln[j], qn);
-    cols_d |= Mask(dn <= dmin) << j;
-    cols_mn |= Mask(dn <= mn) << j;
-  }
-  int i = irow;
-  Mask cols = Mask(W.rmask[irow]) & cols_d;
-  if (!(mn <= dmin)) {
-    cols = 0;
-    for (Mask rr = rows_mn; rr && !cols; rr &= rr - 1) {
-      i = ffs(rr) - 1;
-      cols = Mask(W.rmask[i]) & cols_mn;
+    const double lnj = W.cln[j];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const double dn = dabs_sub(lnj, qn[p]);
+      cols_d[p] |= Mask(dn <= dmin[p]) << j;
+      cols_mn[p] |= Mask(dn <= mn[p]) << j;
     }
   }
-  const int j = ffs(cols) - 1;
-  *dmin_out = dmin;
-  const Mask before = (Mask(1) << j) - 1;
-  const int rank = kBits == 32 ? __popc(uint32_t(Mask(W.rmask[i]) & before))
-                               : __popcll(static_cast<unsigned long long>(Mask(W.rmask[i]) & before));
-  return W.rpos[W.roff[i] + rank];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    int i = irow[p];
+    Mask cols = Mask(W.rmask[i]) & cols_d[p];
+    if (!(mn[p] <= dmin[p])) {
+      cols = 0;
+      for (Mask rr = rows_mn[p]; rr && !cols; rr &= rr - 1) {
+        i = ffs(rr) - 1;
+        cols = Mask(W.rmask[i]) & cols_mn[p];
+      }
+    }
+    const int j = ffs(cols) - 1;
+    dmin_out[p] = dmin[p];
+    const Mask before = (Mask(1) << j) - 1;
+    const int rank = kBits == 32 ? __popc(uint32_t(Mask(W.rmask[i]) & before))
+                                 : __popcll(static_cast<unsigned long long>(Mask(W.rmask[i]) & before));
+    pos_out[p] = W.rpos[W.roff[i] + rank];
+  }
 }
 
 // One member class (every shipped preset; equal logs imply equal
@@ -293,59 +322,74 @@ __device__ __forceinline__ int member_rows(const RowSmem& W, double qm, double q
 // the members -- dmin and its first member (case A: mn <= dmin) and the
 // first member within mn (case B).  Returns the original candidate scan
 // index; *out_best = the distance as ordered |double| bits.
-template <int ROWS>  // 0 member pass, 1 rows (u32 masks), 2 rows (u64 masks)
-__device__ int nearest_point_one_class(const TablesDev& t, const PointSmem& S, const RowSmem& W,
-                                       double qm, double qn, double qk, uint64_t* out_best) {
-  const int G = t.G;
-  const int start = count_below(S.glk, G, qk);
-  auto dk = [&](int g) { return abs_bits(__dsub_rn(S.glk[g], qk)); };
-  const uint64_t dkL = start > 0 ? dk(start - 1) : ~0ull;
-  const uint64_t dkR = start < G ? dk(start) : ~0ull;
-  const uint64_t mn = dkL < dkR ? dkL : dkR;
+template <int ROWS, int P>  // ROWS: 0 member pass, 1 rows (u32 masks), 2 rows (u64 masks);
+                           // P queries (rows only) interleaved
+__device__ void nearest_point_one_class(const TablesDev& t, const PointSmem& S, const RowSmem& W,
+                                        const double* qm, const double* qn, const double* qk,
+                                        int* out_rec, uint64_t* out_best) {
+  const int G = t.G, Gp = pow2_above(G);
+  int start[P];
+  uint64_t dkL[P], mn[P];
+  double mnd[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    start[p] = count_below_p2(S.glk, Gp, qk[p]);
+    dkL[p] = start[p] > 0 ? abs_bits(__dsub_rn(S.glk[start[p] - 1], qk[p])) : ~0ull;
+    const uint64_t dkR = start[p] < G ? abs_bits(__dsub_rn(S.glk[start[p]], qk[p])) : ~0ull;
+    mn[p] = dkL[p] < dkR ? dkL[p] : dkR;
+    // distances are non-negative finite doubles, so FP64 order is the order
+    // of their |.| bits: compare them as doubles (DSETP)
+    mnd[p] = __longlong_as_double(static_cast<long long>(mn[p]));
+  }
   __syncwarp();  // every lane calls this (points_kernel): reconverge
-  // distances are non-negative finite doubles, so FP64 order is the order
-  // of their |.| bits: compare them as doubles (DSETP)
-  const double mnd = __longlong_as_double(static_cast<long long>(mn));
-  int pos;
-  uint64_t dmin;
+  int pos[P];
+  uint64_t dmin[P];
   if (ROWS) {
-    double dm;
-    pos = ROWS == 1 ? member_rows<uint32_t>(W, qm, qn, mnd, &dm)
-                    : member_rows<uint64_t>(W, qm, qn, mnd, &dm);
-    dmin = abs_bits(dm);
+    double dm[P];
+    if (ROWS == 1) member_rows<uint32_t, P>(W, qm, qn, mnd, dm, pos);
+    else member_rows<uint64_t, P>(W, qm, qn, mnd, dm, pos);
+#pragma unroll
+    for (int p = 0; p < P; ++p) dmin[p] = abs_bits(dm[p]);
   } else {
     const int CM = S.csize[0];
-    double dminf = __longlong_as_double(0x7FF0000000000000ll);  // +inf
-    int argmin = 0, first_mn = -1;
-    for (int j = 0; j < CM; ++j) {
-      const double d = fmax(fabs(__dsub_rn(S.lm[j], qm)), fabs(__dsub_rn(S.ln[j], qn)));
-      if (d < dminf) { dminf = d; argmin = j; }
-      if (first_mn < 0 && d <= mnd) first_mn = j;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      double dminf = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+      int argmin = 0, first_mn = -1;
+      for (int j = 0; j < CM; ++j) {
+        const double d = fmax(fabs(__dsub_rn(S.lm[j], qm[p])), fabs(__dsub_rn(S.ln[j], qn[p])));
+        if (d < dminf) { dminf = d; argmin = j; }
+        if (first_mn < 0 && d <= mnd[p]) first_mn = j;
+      }
+      dmin[p] = abs_bits(dminf);
+      pos[p] = mn[p] <= dmin[p] ? argmin : first_mn;
     }
-    dmin = abs_bits(dminf);
-    pos = mn <= dmin ? argmin : first_mn;
   }
-  int g;
-  uint64_t best;
-  if (mn <= dmin) {  // best == dmin: the leftmost group within dmin, member argmin
-    if (dkL <= dmin) {
-      g = start - 1;
-      while (g > 0 && dk(g - 1) <= dmin) --g;
-    } else {
-      g = start;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    auto dk = [&](int g) { return abs_bits(__dsub_rn(S.glk[g], qk[p])); };
+    int g;
+    uint64_t best;
+    if (mn[p] <= dmin[p]) {  // best == dmin: the leftmost group within dmin, member argmin
+      if (dkL[p] <= dmin[p]) {
+        g = start[p] - 1;
+        while (g > 0 && dk(g - 1) <= dmin[p]) --g;
+      } else {
+        g = start[p];
+      }
+      best = dmin[p];
+    } else {                 // best == mn: the leftmost nearest group, first member within mn
+      if (dkL[p] == mn[p]) {
+        g = start[p] - 1;
+        while (g > 0 && dk(g - 1) == mn[p]) --g;
+      } else {
+        g = start[p];
+      }
+      best = mn[p];
     }
-    best = dmin;
-  } else {           // best == mn: the leftmost nearest group, first member within mn
-    if (dkL == mn) {
-      g = start - 1;
-      while (g > 0 && dk(g - 1) == mn) --g;
-    } else {
-      g = start;
-    }
-    best = mn;
+    out_best[p] = best;
+    out_rec[p] = S.gidx[S.gstart[g] + pos[p]];
   }
-  *out_best = best;
-  return S.gidx[S.gstart[g] + pos];
 }
 
 // blocks / waves of compute.block_count / wave_count with a flag for u64
@@ -408,12 +452,14 @@ __global__ void __launch_bounds__(kThreads, PTS_MINB) points_kernel(TablesDev t,
   uint64_t* rmask = reinterpret_cast<uint64_t*>(lr + NLR);
   uint64_t* cmask = rmask + NR;
   double* rlm = reinterpret_cast<double*>(cmask + NCl);
-  double* cln = rlm + NR;
-  double* lm = cln + NCl;
+  double* cln = rlm + NR;                        // padded with +inf to pow2_above(NCl)
+  const int NClp = kRows ? pow2_above(NCl) : 0;
+  double* lm = cln + NClp;
   const int CMs = kRows ? 0 : t.CM;  // the row form needs no member list
   double* ln = lm + CMs;
-  double* glk = ln + CMs;
-  int32_t* gcls = reinterpret_cast<int32_t*>(glk + t.G);
+  double* glk = ln + CMs;                        // padded with +inf to pow2_above(G)
+  const int Gp = pow2_above(t.G);
+  int32_t* gcls = reinterpret_cast<int32_t*>(glk + Gp);
   int32_t* gstart = gcls + t.G;
   int32_t* cstart = gstart + t.G;
   int32_t* csize = cstart + t.NC;
@@ -424,10 +470,9 @@ __global__ void __launch_bounds__(kThreads, PTS_MINB) points_kernel(TablesDev t,
     rmask[j] = t.rw_mask[j];
     rlm[j] = t.rw_lm[j];
   }
-  for (int j = threadIdx.x; j < NCl; j += blockDim.x) {
-    cmask[j] = t.cl_mask[j];
-    cln[j] = t.cl_ln[j];
-  }
+  const double INF = __longlong_as_double(0x7FF0000000000000ll);
+  for (int j = threadIdx.x; j < NCl; j += blockDim.x) cmask[j] = t.cl_mask[j];
+  for (int j = threadIdx.x; j < NClp; j += blockDim.x) cln[j] = j < NCl ? t.cl_ln[j] : INF;
   for (int j = threadIdx.x; j <= NR && kRows; j += blockDim.x) roff[j] = t.rw_off[j];
   for (int j = threadIdx.x; j < NLR; j += blockDim.x)
     lr[j] = reinterpret_cast<const double2*>(t.rw_lr)[j];
@@ -436,8 +481,8 @@ __global__ void __launch_bounds__(kThreads, PTS_MINB) points_kernel(TablesDev t,
     lm[j] = t.cls_lm[j];
     ln[j] = t.cls_ln[j];
   }
+  for (int j = threadIdx.x; j < Gp; j += blockDim.x) glk[j] = j < t.G ? t.grp_lk[j] : INF;
   for (int j = threadIdx.x; j < t.G; j += blockDim.x) {
-    glk[j] = t.grp_lk[j];
     gcls[j] = t.grp_class[j];
     gstart[j] = t.grp_start[j];
   }
@@ -454,97 +499,132 @@ __global__ void __launch_bounds__(kThreads, PTS_MINB) points_kernel(TablesDev t,
   const PointSmem S{lm, ln, glk, gcls, gstart, cstart, csize, gidx};
   const RowSmem W{rlm, cln, rmask, cmask, roff, rpos, lr, NR, NCl};
   // warp-uniform trip count (every lane runs every iteration, the tail lanes
-  // idle), so the warp can be reconverged before the shared prediction tail
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = blockIdx.x * int64_t(blockDim.x) + (threadIdx.x & ~31); base < n;
+  // idle), so the warp can be reconverged before the shared prediction tail.
+  // A warp takes 32 * P consecutive ops per iteration, P per lane (op p of
+  // lane l = base + 32 p + l: coalesced), whose nearest searches run
+  // interleaved (independent FP64 chains per row step)
+  constexpr int P = NEARK >= 2 ? kPointsPerLane : 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x * P;
+  for (int64_t base = (blockIdx.x * int64_t(blockDim.x) + (threadIdx.x & ~31)) * P; base < n;
        base += stride) {
-    const int64_t i = base + (threadIdx.x & 31);
-    const bool valid = i < n;
-    const uint4 s = valid ? shapes[i] : make_uint4(0, 0, 0, 0);
-    const QueryLogs ql = query_logs(L, s);
-    int ci = -1, rec = -1;
-    int8_t match = -1;
-    double dist = 0.0;
-    // divergent steps (probe loops, searches) are followed by explicit warp
-    // reconvergence: without it the lanes leave a loop at different trips
-    // and run the following nearest search in separate passes
-    const bool zero = s.x == 0 || s.y == 0 || s.z == 0 || s.w == 0;
+    int64_t idx[P];
+    uint4 sh[P];
+    int ci[P], rec[P];
+    bool zero[P], hit[P], logs[P];
+    double qm[P], qn[P], qk[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      idx[p] = base + 32 * p + lane;
+      sh[p] = idx[p] < n ? shapes[idx[p]] : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint4 s = sh[p];
+      const QueryLogs ql = query_logs(L, s);
+      ci[p] = -1;
+      rec[p] = -1;
+      // divergent steps (probe loops, searches) are followed by explicit
+      // warp reconvergence: without it the lanes leave a loop at different
+      // trips and run the following nearest search in separate passes
+      zero[p] = s.x == 0 || s.y == 0 || s.z == 0 || s.w == 0;
 #if PTS_VARIANT == 3
-    const bool hit = false;  // diagnostic build: no exact lookup
+      hit[p] = false;  // diagnostic build: no exact lookup
 #else
-    const bool hit = !zero && (t.xh_mask >= 0 ? exact_hash(t, tags, s, &ci, &rec)
-                                              : exact_lookup(t, s.x, s.y, s.z, s.w, &ci, &rec));
+      hit[p] = !zero[p] && (t.xh_mask >= 0 ? exact_hash(t, tags, s, &ci[p], &rec[p])
+                                           : exact_lookup(t, s.x, s.y, s.z, s.w, &ci[p], &rec[p]));
 #endif
-    __syncwarp();
-    double qm = ql.m, qn = ql.n, qk = ql.k;
-    const bool logs = !zero && !hit && t.R > 0 && ql.ok;
+      qm[p] = ql.m;
+      qn[p] = ql.n;
+      qk[p] = ql.k;
+      logs[p] = !zero[p] && !hit[p] && t.R > 0 && ql.ok;
 #if PTS_VARIANT == 4
-    qm = double(s.y); qn = double(s.z); qk = double(s.w);  // diagnostic build: no log2 loads
+      qm[p] = double(s.y); qn[p] = double(s.z); qk[p] = double(s.w);  // diagnostic build: no log2 loads
 #endif
-    __syncwarp();
+      __syncwarp();
+    }
     // the nearest search runs in every lane (exact hits and invalid ops are
     // rare; the warp would run it for the others anyway) so it can keep the
     // warp converged; only the lanes that need it keep its answer
-    uint64_t best = 0;
-    int nrec = -1;
+    uint64_t best[P];
+    int nrec[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      best[p] = 0;
+      nrec[p] = -1;
+    }
 #if PTS_VARIANT == 1 || PTS_VARIANT == 5
-    nrec = int(s.x) & 7;  // diagnostic build: no nearest search
+#pragma unroll
+    for (int p = 0; p < P; ++p) nrec[p] = int(sh[p].x) & 7;  // diagnostic build: no nearest search
 #else
-    if (t.R > 0)
-      nrec = NEARK >= 2 ? nearest_point_one_class<NEARK - 2>(t, S, W, qm, qn, qk, &best)
-                        : nearest_point<NEARK == 1>(t, S, qm, qn, qk, &best);
-#endif
-    if (zero) {
-      match = -2;  // invalid coordinate
-    } else if (hit) {
-      match = 0;
-    } else if (t.R > 0) {
-      if (!logs) {
-        match = -2;  // no host log2 for this coordinate
+    if (t.R > 0) {
+      if constexpr (NEARK >= 2) {
+        nearest_point_one_class<NEARK - 2, P>(t, S, W, qm, qn, qk, nrec, best);
       } else {
-        rec = nrec;
-        ci = t.cand_curve[rec];
-        dist = __longlong_as_double(static_cast<long long>(best));
-        match = 1;
+#pragma unroll
+        for (int p = 0; p < P; ++p) nrec[p] = nearest_point<NEARK == 1>(t, S, qm[p], qn[p], qk[p], &best[p]);
       }
     }
-    __syncwarp();
-    PointResult r;
-    double thr = 0.0, bse = 0.0;
-#if PTS_VARIANT == 2 || PTS_VARIANT == 5
-    r.lat = qm + qk; r.waves = s.x;  // diagnostic build: no prediction tail
-    if (false) {
-#else
-    if (ci >= 0) {
 #endif
-      const double nd = __ull2double_rn(uint64_t(s.w));
-      thr = interp_thr(t, ci, nd);
-      bse = base_from_thr(t, ci, nd, thr);
-      if (!predict_point_checked(t, ci, s.x, s.y, s.z, s.w, bse, &r)) {
-        match = -3;  // block count past 2^64
-        ci = -1;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int64_t i = idx[p];
+      const uint4 s = sh[p];
+      int c = ci[p], rc = rec[p];
+      int8_t match = -1;
+      double dist = 0.0;
+      if (zero[p]) {
+        match = -2;  // invalid coordinate
+      } else if (hit[p]) {
+        match = 0;
+      } else if (t.R > 0) {
+        if (!logs[p]) {
+          match = -2;  // no host log2 for this coordinate
+        } else {
+          rc = nrec[p];
+          c = t.cand_curve[rc];
+          dist = __longlong_as_double(static_cast<long long>(best[p]));
+          match = 1;
+        }
       }
-    }
-    if (!valid) continue;
-    if (out_record) out_record[i] = rec;
-    if (out_dist) out_dist[i] = dist;
-    if (out_match) out_match[i] = match;
-    if (ci < 0) {
-      out_lat[i] = qnan();
-      if (out_curve) out_curve[i] = -1;
-      if (out_waves) out_waves[i] = 0;
-      if (out_detail)
-        for (int j = 0; j < 4; ++j) out_detail[4 * i + j] = qnan();
-      continue;
-    }
-    out_lat[i] = r.lat;
-    if (out_curve) out_curve[i] = ci;
-    if (out_waves) out_waves[i] = waves_u32(r.waves);
-    if (out_detail) {  // Prediction.components: base_us, new_throughput, wave_scale, waves
-      out_detail[4 * i] = bse;
-      out_detail[4 * i + 1] = thr;
-      out_detail[4 * i + 2] = wave_scale(t, ci, r.waves);
-      out_detail[4 * i + 3] = __ull2double_rn(r.waves);
+      __syncwarp();
+      PointResult r;
+      double thr = 0.0, bse = 0.0;
+#if PTS_VARIANT == 2 || PTS_VARIANT == 5
+      r.lat = qm[p] + qk[p]; r.waves = s.x;  // diagnostic build: no prediction tail
+      if (false) {
+#else
+      if (c >= 0) {
+#endif
+        const double nd = __ull2double_rn(uint64_t(s.w));
+        thr = interp_thr(t, c, nd);
+        bse = base_from_thr(t, c, nd, thr);
+        if (!predict_point_checked(t, c, s.x, s.y, s.z, s.w, bse, &r)) {
+          match = -3;  // block count past 2^64
+          c = -1;
+        }
+      }
+      if (i >= n) continue;
+      if (out_record) out_record[i] = rc;
+      if (out_dist) out_dist[i] = dist;
+      if (out_match) out_match[i] = match;
+      if (c < 0) {
+        out_lat[i] = qnan();
+        if (out_curve) out_curve[i] = -1;
+        if (out_waves) out_waves[i] = 0;
+        if (out_detail)
+          for (int j = 0; j < 4; ++j) out_detail[4 * i + j] = qnan();
+        continue;
+      }
+      out_lat[i] = r.lat;
+      if (out_curve) out_curve[i] = c;
+      if (out_waves) out_waves[i] = waves_u32(r.waves);
+      if (out_detail) {  // Prediction.components: base_us, new_throughput, wave_scale, waves
+        out_detail[4 * i] = bse;
+        out_detail[4 * i + 1] = thr;
+        out_detail[4 * i + 2] = wave_scale(t, c, r.waves);
+        out_detail[4 * i + 3] = __ull2double_rn(r.waves);
+      }
     }
   }
 }
@@ -594,7 +674,8 @@ int launch_points(const TablesDev& t, const uint32_t* shapes, int64_t n, const L
   const bool one = t.NC == 1 && t.lowest_wins;
   const bool rows = one && t.rw_n > 0;
   const int64_t NR = rows ? t.rw_n : 0, NCl = rows ? t.cl_n : 0;
-  const int64_t smem = 16ll * NR * (NCl + 1) + 16ll * (NR + NCl) + (rows ? 0 : 16ll * t.CM) + 8ll * t.G + 8ll * t.G +
+  const int64_t smem = 16ll * NR * (NCl + 1) + 16ll * NR + 8ll * NCl + (rows ? 8ll * pow2_above(int(NCl)) : 0) +
+                       (rows ? 0 : 16ll * t.CM) + 8ll * pow2_above(t.G) + 8ll * t.G +
                        8ll * t.NC + 4ll * t.R + (rows ? 4ll * (NR + 1 + t.CM) : 0) +
                        (t.xh_mask >= 0 && t.xh_mask < kTagSmemSlots ? 4ll * (t.xh_mask + 1) : 0) + 64;
   auto* fn = rows ? (t.rw_n <= 32 && t.cl_n <= 32 ? points_kernel<3> : points_kernel<4>)
