@@ -118,13 +118,13 @@ __global__ void __launch_bounds__(kSingleThreads, SINGLE_MINB) single_kernel(Tab
       const uint64_t v_b = in_b ? g.B[g.b_lo + i] : 0;
       double v_rd = 0.0, v_rm = 0.0, v_rt = 0.0;
       uint8_t v_rb = 0;
-      int32_t v_wc = -1;
+      WcParam v_wp{};
       if (in_c) {
         v_rd = t.ref_dur[i];
         v_rm = t.ref_dim[i];
         v_rt = t.ref_thr[i];
         v_rb = t.rowblock[i];
-        v_wc = t.wc_of[i];
+        v_wp = t.wcp_c[i];  // no dependent wc_of -> wcp load
       }
       if (in_g) { glk[i] = v_glk; gcur[i] = v_gc; }
       if (in_x) ex[i] = v_ex;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kSingleThreads, SINGLE_MINB) single_kernel(Tab
         c_ref[3 * i + 1] = v_rm;
         c_ref[3 * i + 2] = v_rt;
         c_rb[i] = v_rb;
-        if (v_wc >= 0) c_wp[i] = t.wcp[v_wc];
+        c_wp[i] = v_wp;
       }
     }
   }

@@ -70,6 +70,7 @@ struct TablesDev {
   const int32_t* g_curve = nullptr;    // curve of each candidate in GROUP order [R]
   const int32_t* g_cw = nullptr;       // [2R] (curve, wave class) in GROUP order
   const WcParam* wcp = nullptr;        // [NW]
+  const WcParam* wcp_c = nullptr;      // [C] wcp[wc_of[c]] per curve (zero: no samples)
   // groups [G]
   const double* grp_lk = nullptr;
   const int32_t* grp_start = nullptr;

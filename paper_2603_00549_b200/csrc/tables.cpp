@@ -260,6 +260,11 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
       }
     }
   }
+  // the same parameters per curve (zero for a curve without samples): one
+  // load instead of the wc_of -> wcp chain where a kernel stages them by curve
+  std::vector<WcParam> wcp_c(static_cast<size_t>(C));
+  for (int64_t c = 0; c < C; ++c)
+    if (wc_of[c] >= 0) wcp_c[c] = wcp[size_t(wc_of[c])];
   std::vector<int32_t> s_off(C + 1);
   for (int64_t c = 0; c <= C; ++c) s_off[c] = int32_t(v->sample_offsets[c]);
   std::vector<uint8_t> rowblock(C);
@@ -400,6 +405,7 @@ std::string build_tables(const pm2l_tables_view* v, TablesHost* out) {
   t.g_curve = blob.add(g_curve);
   t.g_cw = blob.add(g_cw);
   t.wcp = blob.add(wcp);
+  t.wcp_c = blob.add(wcp_c);
   t.grp_lk = blob.add(grp_lk);
   t.grp_start = blob.add(grp_start);
   {
@@ -459,6 +465,7 @@ TablesDev rebase(const TablesDev& o, const void* base) {
   t.g_idx = shift(o.g_idx, base); t.cand_curve = shift(o.cand_curve, base);
   t.g_curve = shift(o.g_curve, base);
   t.g_cw = shift(o.g_cw, base); t.wcp = shift(o.wcp, base);
+  t.wcp_c = shift(o.wcp_c, base);
   t.grp_lk = shift(o.grp_lk, base); t.grp_start = shift(o.grp_start, base);
   t.grp_size = shift(o.grp_size, base); t.grp_class = shift(o.grp_class, base);
   t.grp_curve0 = shift(o.grp_curve0, base); t.rec_k = shift(o.rec_k, base);
