@@ -926,7 +926,9 @@ int drain_to_host(SliceDevice& sd, const double* d_out, double* out, size_t byte
     // about half the host threads: the copy-out saturates host memory
     // bandwidth well before every core is busy (measured on the B200 host)
     const unsigned hc = std::thread::hardware_concurrency();
-    g_slice.pool.reset(new CopyPool(int(std::min(7u, hc > 3 ? hc / 2 - 1 : 0u))));
+    int workers = int(std::min(7u, hc > 3 ? hc / 2 - 1 : 0u));
+    if (const char* e = std::getenv("PM2L_COPY_THREADS")) workers = std::max(0, std::atoi(e) - 1);  // tuning
+    g_slice.pool.reset(new CopyPool(workers));
   }
   for (int i = 0; i < kStageBufs; ++i) {
     PM2L_CUDA(sd.stage[i].reserve(kStageChunk));
