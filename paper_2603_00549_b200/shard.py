@@ -147,30 +147,58 @@ def predict_range_device(prep, lo: int, hi: int, out=None, device: int = 0):
     return out
 
 
+def _range_checksum(t):
+    """Order-independent checksum of a float64 range: the sums of the low and
+    high 32-bit halves of its bit patterns (exact in int64 below 2^31 values)
+    -- the same pair wherever the bits travel, so rank 0 can check every
+    gathered range against its owner's."""
+    import torch
+    bits = t.contiguous().view(torch.int64)
+    return torch.stack([(bits & 0xFFFFFFFF).sum(), (bits >> 32 & 0xFFFFFFFF).sum()])
+
+
 def _nan_stats(local, lo: int):
-    """(first NaN as a global flat index or _NONE, NaN count) as a 2-vector
-    on the tensor's device (no host round trip)."""
+    """(first NaN as a global flat index or _NONE, NaN count, checksum lo,
+    checksum hi) as a 4-vector on the tensor's device (no host round trip)."""
     import torch
     nan = torch.isnan(local)
     count = nan.sum()
     idx = torch.arange(local.numel(), device=local.device, dtype=torch.int64)
     first = torch.where(nan, idx + lo, torch.full_like(idx, _NONE)).min() if local.numel() \
         else torch.tensor(_NONE, device=local.device)
-    return torch.stack([first.to(torch.int64), count.to(torch.int64)])
+    return torch.cat([torch.stack([first.to(torch.int64), count.to(torch.int64)]),
+                      _range_checksum(local).to(torch.int64)])
+
+
+def _exchange_stats(local, lo: int, group=None):
+    """All-gather of every rank's (first NaN, NaN count, checksum pair):
+    one collective, a (world, 4) int64 tensor on the tensor's device."""
+    import torch
+    dist = _dist()
+    mine = _nan_stats(local, lo)
+    world = dist.get_world_size(group)
+    allv = torch.empty(4 * world, dtype=torch.int64, device=mine.device)
+    dist.all_gather_into_tensor(allv, mine, group=group)
+    return allv.view(world, 4)
 
 
 def gather_unresolved(local, lo: int, group=None) -> Tuple[int, int]:
     """All-gather of (first NaN as a global flat index, NaN count) over the
     ranks: the global first unresolved point (-1 if none) and the total."""
-    import torch
-    dist = _dist()
-    mine = _nan_stats(local, lo)
-    world = dist.get_world_size(group)
-    allv = torch.empty(2 * world, dtype=torch.int64, device=mine.device)
-    dist.all_gather_into_tensor(allv, mine, group=group)
-    allv = allv.view(world, 2)
+    allv = _exchange_stats(local, lo, group)
     first_g = int(allv[:, 0].min().item())
     return (-1 if first_g == _NONE else first_g), int(allv[:, 1].sum().item())
+
+
+def verify_gathered(full, stats, shape) -> None:
+    """Rank 0: every gathered range's checksum equals the one its owner
+    all-gathered; raises on a mismatch."""
+    world = stats.shape[0]
+    for r in range(world):
+        r_lo, r_hi = flat_bounds(shape, world, r)
+        got = _range_checksum(full[r_lo:r_hi]).to(stats.device)
+        if not bool((got == stats[r, 2:]).all()):
+            raise RuntimeError(f"gathered range of rank {r} [{r_lo}, {r_hi}) fails its checksum")
 
 
 def gather_to_root(local, lo: int, hi: int, shape, group=None):
@@ -217,8 +245,12 @@ def predict_sharded(prep, group=None, gather: bool = False,
     else:
         local = torch.from_numpy(np.ascontiguousarray(predict(prep, lo, hi), dtype=np.float64))
         local = local.to(_tensor_device(group))
-    first, count = gather_unresolved(local, lo, group)
+    stats = _exchange_stats(local, lo, group)
+    first_g = int(stats[:, 0].min().item())
+    first, count = (-1 if first_g == _NONE else first_g), int(stats[:, 1].sum().item())
     full = gather_to_root(local, lo, hi, shape, group) if gather else None
+    if full is not None:
+        verify_gathered(full, stats, shape)
     return ShardResult(lo, hi, local, first, count, full)
 
 

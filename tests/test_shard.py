@@ -263,3 +263,29 @@ def test_topk_global_merges_by_value_then_index(world):
             ids, vals = o[k]
             assert np.array_equal(ids, ref[:k])
             assert np.array_equal(vals, allv[ref[:k]])
+
+
+def test_gathered_ranges_are_checked_against_their_owners_checksums():
+    """SURVEY §8e: the stats all-gather carries each rank's range checksum;
+    rank 0 checks every gathered range against it (a corrupted or misplaced
+    range is caught)."""
+    import torch
+    from paper_2603_00549_b200 import shard
+    shape = (2, 3, 5, 7)
+    world = 3
+    full = torch.from_numpy(np.random.default_rng(0).random(int(np.prod(shape))))
+    stats = torch.zeros(world, 4, dtype=torch.int64)
+    for r in range(world):
+        lo, hi = shard.flat_bounds(shape, world, r)
+        stats[r, 2:] = shard._range_checksum(full[lo:hi])
+    shard.verify_gathered(full, stats, shape)          # intact: passes
+    bad = full.clone()
+    lo1, _ = shard.flat_bounds(shape, world, 1)
+    bad[lo1] = np.nextafter(bad[lo1].item(), 2.0)      # one ulp in rank 1's range
+    with pytest.raises(RuntimeError, match="rank 1"):
+        shard.verify_gathered(bad, stats, shape)
+    # checksums are order-independent within a range but not across ranges
+    swapped = full.clone()
+    lo2, hi2 = shard.flat_bounds(shape, world, 2)
+    swapped[lo2:hi2] = torch.flip(full[lo2:hi2], [0])
+    shard.verify_gathered(swapped, stats, shape)
