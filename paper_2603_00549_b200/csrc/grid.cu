@@ -175,6 +175,27 @@ __global__ void __launch_bounds__(kThreads) all_curves_kernel(TablesDev t, GridD
   const int64_t slice = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
   const int64_t plane = g.nM * g.nN * g.nK;
   const int64_t row_off = int64_t(ib0 - g.b_lo) * plane + int64_t(row) * nK;
+  if (gl.kt == 2 && table) {
+    // two adjacent k per thread, one 16-byte streaming store per (curve,
+    // batch value): even k axis, 16-byte aligned output (plan_grid)
+    const int p0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
+    for (int j = 0; j < gl.kpt; ++j) {
+      const int ik = 2 * (p0 + j * int(blockDim.x) + tid);
+      if (ik >= nK) break;
+      for (int c = 0; c < t.C; ++c) {
+        const double2 base = *reinterpret_cast<const double2*>(base_tab + int64_t(c) * nK + ik);
+        const bool valid = curve_valid(t, c);
+        double* o = out + int64_t(c) * slice + row_off + ik;
+        for (int ib = 0; ib < nb; ++ib, o += plane) {
+          const double w = W[ib * t.C + c];
+          const double2 lat = valid ? make_double2(__dmul_rn(base.x, w), __dmul_rn(base.y, w))
+                                    : make_double2(qnan(), qnan());
+          __stcs(reinterpret_cast<double2*>(o), lat);
+        }
+      }
+    }
+    return;
+  }
   const int k0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
   for (int j = 0; j < gl.kpt; ++j) {
     const int ik = k0 + j * int(blockDim.x) + tid;
@@ -208,14 +229,18 @@ __global__ void nan_scan_kernel(const double* __restrict__ v, int64_t n,
   if ((threadIdx.x & 31) == 0 && mine != ~0ull) atomicMin(first, mine);
 }
 
-GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves) {
+GridLaunch plan_grid(const TablesDev& t, const GridDev& g, bool all_curves, bool aligned16 = false) {
   GridLaunch gl{};
   const int64_t rows = g.nM * g.nN;
   const int64_t nb = g.b_hi - g.b_lo;
   if (all_curves) {  // all_curves_kernel: (row, k tile, slab) CTAs of kThreads
     const int64_t target = int64_t(sm_count()) * 8;
+    // kt: k values per thread step (2: 16-byte pair stores on an even k
+    // axis; needs the W table, which the condition below guarantees: mode 0)
+    gl.kt = aligned16 && g.nK % 2 == 0 && t.all_gemm && (8ll * t.C * (nb + 1) <= 96 * 1024) ? 2 : 1;
     auto ktiles_for = [&](int kpt) {
-      return int((g.nK + int64_t(kpt) * kThreads - 1) / (int64_t(kpt) * kThreads));
+      const int64_t per = int64_t(kpt) * kThreads * gl.kt;
+      return int((g.nK + per - 1) / per);
     };
     gl.kpt = 4;
     int ktiles = ktiles_for(gl.kpt);
@@ -460,7 +485,7 @@ int launch_grid_all_curves(const TablesDev& t, const GridDev& g, double* ws, dou
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t card = (g.b_hi - g.b_lo) * g.nM * g.nN * g.nK;
   if (card == 0 || t.C == 0) return 0;
-  GridLaunch gl = plan_grid(t, g, true);
+  GridLaunch gl = plan_grid(t, g, true, (reinterpret_cast<uintptr_t>(out) & 15) == 0);
   if (!grid_dims_ok(g, gl) || t.C > 65535 || gl.tiles > 65535) return int(cudaErrorInvalidValue);
   launch_base_table(t, g, ws, nullptr, nullptr, s);
   const int64_t smem = gl.mode == 0 ? ((8ll * t.C + 15) & ~15ll) + 8ll * t.C * gl.bper : 0;
