@@ -178,19 +178,30 @@ __global__ void __launch_bounds__(kThreads) all_curves_kernel(TablesDev t, GridD
   if (gl.kt == 2 && table) {
     // two adjacent k per thread, one 16-byte streaming store per (curve,
     // batch value): even k axis, 16-byte aligned output (plan_grid)
+    // curve-major: a CTA writes each (curve, batch value) run of its k tile
+    // back to back (longer contiguous DRAM runs than k-major order)
     const int p0 = int(blockIdx.y) * gl.kpt * int(blockDim.x);
-    for (int j = 0; j < gl.kpt; ++j) {
-      const int ik = 2 * (p0 + j * int(blockDim.x) + tid);
-      if (ik >= nK) break;
-      for (int c = 0; c < t.C; ++c) {
-        const double2 base = *reinterpret_cast<const double2*>(base_tab + int64_t(c) * nK + ik);
-        const bool valid = curve_valid(t, c);
-        double* o = out + int64_t(c) * slice + row_off + ik;
-        for (int ib = 0; ib < nb; ++ib, o += plane) {
-          const double w = W[ib * t.C + c];
-          const double2 lat = valid ? make_double2(__dmul_rn(base.x, w), __dmul_rn(base.y, w))
-                                    : make_double2(qnan(), qnan());
-          __stcs(reinterpret_cast<double2*>(o), lat);
+    const int ik0 = 2 * (p0 + tid);
+    for (int c = 0; c < t.C; ++c) {
+      const bool valid = curve_valid(t, c);
+      double2 base[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int ik = ik0 + 2 * j * int(blockDim.x);
+        base[j] = j < gl.kpt && ik < nK ? *reinterpret_cast<const double2*>(base_tab + int64_t(c) * nK + ik)
+                                        : make_double2(0.0, 0.0);
+      }
+      double* o = out + int64_t(c) * slice + row_off + ik0;
+      for (int ib = 0; ib < nb; ++ib, o += plane) {
+        const double w = W[ib * t.C + c];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ik = ik0 + 2 * j * int(blockDim.x);
+          if (j < gl.kpt && ik < nK) {
+            const double2 lat = valid ? make_double2(__dmul_rn(base[j].x, w), __dmul_rn(base[j].y, w))
+                                      : make_double2(qnan(), qnan());
+            __stcs(reinterpret_cast<double2*>(o + 2 * j * int(blockDim.x)), lat);
+          }
         }
       }
     }

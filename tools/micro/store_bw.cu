@@ -1,9 +1,10 @@
-// Store-bandwidth microbenchmark (diagnostics): 80 MB of f64 written after a
+// Store-bandwidth microbenchmark (diagnostics): n f64 (argv[1], default 10 M: 80 MB) written after a
 // 256 MiB flush, by (1) STG.128 grid-stride, (2) STG.128 streaming (.cs),
 // (3) TMA bulk stores (cp.async.bulk.global.shared::cta) from shared memory.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o store_bw store_bw.cu
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __global__ void stg(double2* o, size_t n2, double v) {
@@ -34,8 +35,9 @@ __global__ void tma(double* o, size_t nchunks, double v) {
   }
 }
 
-int main() {
-  const size_t n = 10000000, bytes = n * 8;
+int main(int argc, char** argv) {
+  // argv[1]: doubles to write (default 10 M = C2's 80 MB; 120 M = mode X's 960 MB)
+  const size_t n = argc > 1 ? size_t(strtoull(argv[1], nullptr, 10)) : 10000000, bytes = n * 8;
   double *out, *flush;
   cudaMalloc(&out, bytes);
   cudaMalloc(&flush, size_t(256) << 20);
