@@ -199,7 +199,7 @@ def measured_peak_hbm():
 def profiled_traffic():
     """dram bytes per grid-kernel launch from the committed ncu capture."""
     try:
-        with open(os.path.join(ROOT, "profiles", "round2", "ncu_step_grid_r2b.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "round2", "ncu_step_grid_r2g.json")) as fh:
             return json.load(fh).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
