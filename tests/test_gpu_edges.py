@@ -198,3 +198,37 @@ def test_points_empty_batch_and_invalid_coordinates(gpu):
     l, c = lat.cpu().numpy(), cur.cpu().numpy()
     assert math.isfinite(l[0]) and c[0] >= 0
     assert np.all(np.isnan(l[1:])) and np.all(c[1:] == -1)
+
+
+def test_ffi_slice_is_thread_safe(gpu):
+    """pm2l_predict_grid_slice is documented synchronous and thread-safe
+    (include/pm2l.h): concurrent callers (ctypes drops the GIL) on different
+    tables and slices each get their own bit-exact result."""
+    import threading
+    names = ["matmul_bf16", "exact_mix_bf16", "cutlass_attn_bf16", "parity_fp32", "wide_fp32"]
+    names = [n for n in names if n in GRIDS]
+    jobs = []
+    for name in names:
+        prep = prepared(GRIDS[name])
+        t = dict(prep.tables())
+        axes = prep.axis_arrays()
+        n = len(axes[0]) * len(axes[1]) * len(axes[2]) * len(axes[3])
+        jobs.append((t, axes, oracle.grid(t, axes, 0, len(axes[0]), verify=False), n))
+    errors = []
+
+    def run(t, axes, want, n):
+        try:
+            for _ in range(5):
+                out = np.empty(n, np.float64)
+                ffi_slice(t, axes, 0, len(axes[0]), out)
+                if not np.array_equal(_bits(out), _bits(want)):
+                    errors.append("mismatch")
+        except Exception as exc:  # surfaced below
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=run, args=j) for j in jobs for _ in range(2)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors[:3]
