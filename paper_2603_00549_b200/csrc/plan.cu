@@ -90,7 +90,10 @@ struct PlanArgs {
 // rank(i) = #{j : mn_j > mn_i} + #{j < i : mn_j == mn_i}, the position in the
 // stable descending order of mn (std::stable_sort in the host planner).  A
 // warp counts for kRankPerWarp values at a time over lane-strided j.
-constexpr int kRankPerWarp = 2;
+#ifndef PM2L_RANK_PER_WARP
+#define PM2L_RANK_PER_WARP 1  // measured: 1 (125 rank CTAs for C2) > 2 > 4 > 8
+#endif
+constexpr int kRankPerWarp = PM2L_RANK_PER_WARP;
 constexpr int kRankPerCta = kRankPerWarp * (kPlanThreads / 32);
 
 __device__ void plan_k_rank(const TablesDev& t, const GridDev& g, const PlanArgs& a, int chunk,
