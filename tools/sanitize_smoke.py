@@ -7,7 +7,9 @@
   the verification outputs), plan_kernel, base_table_kernel, fixup_kernel,
   all_curves_kernel, points_kernel (row walk, member pass, general sweep),
   points_curve_kernel, membound_kernel, segment_fsum_kernel,
-  store_count/scan/encode_kernel, store_lookup_kernel, nan_scan.
+  store_count/scan/encode_kernel, store_lookup_kernel, nan_scan,
+  single_kernel (the flash-attention grid, exact hits at batch 96),
+  grid_error_kernel, partition_cut_kernel / partition_best_kernel.
 Every result is compared with the oracle so a sanitizer run also proves the
 launches did their work.  Exit status 0 on success.
 """
@@ -115,6 +117,17 @@ def main():
     assert np.array_equal(bits(lat), bits(olat))
     offs = np.array([0, 3, 3, 100, 1000], np.int64)
     assert np.array_equal(bits(segment_fsum(lat, offs)), bits(oracle.segment_fsum(lat, offs)))
+    # §8f row 4: interpolation-grid audit and the partition cut scan
+    from test_audit import AUDIT, _curve, _fixture, _fx, _truth
+    from paper_2603_00549_b200.curvefit import grid_error_report
+    from paper_2603_00549_b200.partition import partition_two_device
+    for rep in AUDIT["grid_error"][:3]:
+        r = grid_error_report(_curve(rep["kernel"]), _truth(rep), max_points=rep["max_points"])
+        assert r.max_rel_err.hex() == _fx(rep["max_rel_err"]).hex()
+    for p in AUDIT["partition"][:3]:
+        graph, ds_a, ds_b = _fixture([_fx(x) for x in p["lat_a"]], [_fx(x) for x in p["lat_b"]])
+        if not p["link"]:
+            assert partition_two_device(graph, ds_a, ds_b).cut_after_layer_index == p["cut"]
     print("sanitize_smoke: ok")
 
 
