@@ -4,7 +4,8 @@ memcheck (out-of-bounds / misaligned device accesses), racecheck
 (shared-memory hazards: the planner's rank sort, the sweep kernel's
 staircases, the points kernel's staged tables, the reductions) and
 synccheck (barrier / warp-sync misuse: the points kernel's __syncwarp
-reconvergence)."""
+reconvergence) and initcheck (device reads of never-written global memory:
+plan buffers, workspaces, staged tables)."""
 
 import os
 import shutil
@@ -25,7 +26,7 @@ def _sanitizer():
     pytest.fail("compute-sanitizer not found")
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_kernels_are_clean_under_compute_sanitizer(gpu, tool):
     cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "99", "--print-limit", "20"]
     if tool == "memcheck":
