@@ -881,7 +881,15 @@ class CopyPool {
 };
 
 constexpr int kStageBufs = 4;
-constexpr size_t kStageChunk = size_t(8) << 20;  // bytes per D2H chunk
+// bytes per D2H chunk (PM2L_STAGE_CHUNK_MB overrides it for tuning; read once)
+size_t stage_chunk() {
+  static const size_t v = [] {
+    const char* e = std::getenv("PM2L_STAGE_CHUNK_MB");
+    const long mb = e ? std::atol(e) : 0;
+    return size_t(mb > 0 && mb <= 64 ? mb : 8) << 20;
+  }();
+  return v;
+}
 
 struct SliceDevice {
   DeviceBuf out;                    // device result
@@ -931,6 +939,7 @@ int drain_to_host(SliceDevice& sd, const double* d_out, double* out, size_t byte
     if (const char* e = std::getenv("PM2L_COPY_THREADS")) workers = std::max(0, std::atoi(e) - 1);  // tuning
     g_slice.pool.reset(new CopyPool(workers));
   }
+  const size_t kStageChunk = stage_chunk();
   for (int i = 0; i < kStageBufs; ++i) {
     PM2L_CUDA(sd.stage[i].reserve(kStageChunk));
     if (!sd.ready[i]) PM2L_CUDA(cudaEventCreateWithFlags(&sd.ready[i], cudaEventDisableTiming));
