@@ -6,10 +6,13 @@
 //                        (compute.py:163-193)
 //   points_curve_kernel  predict_generic with an explicit curve (no resolution)
 //
-// Per op the nearest search uses the same decomposition as the grid kernel —
-// member classes and the outward k-group sweep — but without a shared row,
-// so D_j(m, n) is recomputed per op from the class members staged in shared
-// memory (broadcast reads: all lanes read the same member).
+// One op per lane.  The exact record comes from a hash whose slot tags sit in
+// shared memory; for one-class tables (every shipped preset) the nearest
+// search is the grid kernel's decision split into a k part (nearest k-group)
+// and a member part over the row decomposition of the class (distinct log m
+// rows x distinct log n columns, with each row's nearest present column per
+// column insertion point precomputed: TablesDev::rw_lr); other tables take
+// the k-group sweep over the member classes staged in shared memory.
 #include <algorithm>
 
 #include "common.cuh"
@@ -22,19 +25,17 @@
 #ifndef PTS_MINB
 #define PTS_MINB 4  // 64 registers: 4 CTAs per SM (measured best; 5 spills)
 #endif
-
 #ifndef PTS_PAIR
 #define PTS_PAIR 1  // 2 measured slower (spills at 64 registers, no gain at 80)
 #endif
-namespace {
-constexpr int kTagSmemSlots = 4096;  // exact-hash tags staged in shared memory up to 16 KB
-constexpr int kPointsPerLane = PTS_PAIR;  // one-class ops per lane per iteration (interleaved)
-}
 
 namespace pm2l {
 namespace {
 
 using namespace dev;
+
+constexpr int kTagSmemSlots = 4096;       // exact-hash tags staged in shared memory up to 16 KB
+constexpr int kPointsPerLane = PTS_PAIR;  // one-class ops per lane per iteration (interleaved)
 
 __device__ int exact_lookup(const TablesDev& t, uint64_t b, uint64_t m, uint64_t n, uint64_t k,
                             int* curve, int* record) {
