@@ -444,12 +444,10 @@ def predict_model_grid(template: Sequence[TemplateLayer], shapes, features, data
     the first (model, layer) that cannot be predicted."""
     from . import _device, _native
     from .compute import _log2_extension, _shapes_u32
-    from .membound import predict_membound_batch
     pred = _predictor(dataset, wm, membound_floor_us)
     L = len(template)
     shapes = np.asarray(shapes)
     n = shapes.shape[0] if shapes.ndim == 3 else np.asarray(features).shape[0]
-    lat = np.full((n, L), np.nan)
     by_triple: Dict[tuple, List[int]] = {}
     util: Dict[tuple, List[int]] = {}
     for l, t in enumerate(template):
@@ -460,37 +458,100 @@ def predict_model_grid(template: Sequence[TemplateLayer], shapes, features, data
             by_triple.setdefault((t.family, t.dtype, tr), []).append(l)
         else:
             raise UnresolvedLayer(f"layer {t.layer_id!r}: no predictor for family {t.family!r}")
-    dev = _device.device()
+    # one device pipeline (as ModelPredictor._predict_layers): one staged
+    # upload per input kind, every kernel back to back on the stream (one
+    # resolution + prediction batch per kernel triple, one membound batch,
+    # the scatter into model-major order, the exact per-model sums), one
+    # device->host copy of every output
+    rows = np.arange(n, dtype=np.int64)[:, None] * L
+    tri = []                     # (triple, layers, ops)
+    sh_parts, posc = [], []
     for triple, ls in by_triple.items():
-        *_, dt = pred.resolver.triple_tables(*triple)
-        s = _shapes_u32(shapes[:, ls, :].reshape(-1, 4))
-        d_s = _device.to_device(s, dev)
-        ext_c, ext_l, n_ext = _log2_extension(s, dev)
-        out = _device.empty(len(s), "float64", dev)
-        match = _device.empty(len(s), "int8", dev)
-        _native.check(_native.load().pm2l_points_predict_ext(
-            dt.handle, _native.ptr(d_s), len(s), _native.ptr(ext_c), _native.ptr(ext_l), n_ext,
-            _native.ptr(out), 0, 0, _native.ptr(match), 0, 0, 0,
-            _device.stream()), "pm2l_points_predict_ext")
-        match = _device.to_numpy(match)
-        if (match == -3).any():
-            j = int(np.nonzero(match == -3)[0][0])
-            raise ValidationError(f"model {j // len(ls)} layer {template[ls[j % len(ls)]].layer_id!r}: "
-                                  f"block count exceeds 2^64")
-        lat[:, ls] = _device.to_numpy(out).reshape(n, len(ls))
+        tri.append((triple, ls, n * len(ls)))
+        sh_parts.append(_shapes_u32(shapes[:, ls, :].reshape(-1, 4)))
+        posc.append((rows + np.asarray(ls, np.int64)[None, :]).ravel())
+    sh = np.concatenate(sh_parts) if sh_parts else np.zeros((0, 4), np.uint32)
+    nc = len(sh)
+    models, mids, posu, feats = [], [], [], []
     if util:
         f = np.asarray(features, dtype=np.float64)
-        models, mids, cols = [], [], []
         for mi, ((name, dt_), ls) in enumerate(util.items()):
             models.append(pred.membound_model(name, dt_))
             for l in ls:
-                cols.append(l)
-                mids.append(mi)
-        feats = np.concatenate([f[:, l, :] for l in cols])
-        ids = np.repeat(np.array(mids, np.int32), n)
-        ulat, _ = predict_membound_batch(models, feats, ids, [membound_floor_us] * len(models))
-        for j, l in enumerate(cols):
-            lat[:, l] = ulat[j * n:(j + 1) * n]
+                feats.append(f[:, l, :])
+                mids.append(np.full(n, mi, np.int64))
+                posu.append(rows[:, 0] + l)
+    nu = n * sum(len(ls) for ls in util.values())
+    ints = np.concatenate([sh.astype(np.int64).ravel()] + mids + posc + posu +
+                          [np.arange(0, n * L + 1, L, dtype=np.int64)])
+    floats = np.zeros(0, np.float64)
+    if nu:
+        floats = np.concatenate([np.concatenate(feats).ravel(),
+                                 np.array([m.weights for m in models], np.float64).ravel(),
+                                 np.array([m.intercept for m in models], np.float64),
+                                 np.full(len(models), membound_floor_us, np.float64)])
+    dev = _device.device()
+    t = _device.torch()
+    lib = _native.load()
+    s = _device.stream()
+    d_int = _staged_upload(ints, dev)
+    d_flt = _staged_upload(floats, dev) if nu else None
+    o = 4 * nc
+    d_mid = d_int[o:o + nu]
+    o += nu
+    d_posc = d_int[o:o + nc]
+    o += nc
+    d_posu = d_int[o:o + nu]
+    o += nu
+    d_off = d_int[o:o + n + 1]
+    # outputs in one f64 buffer: compute latencies, match codes (int8 in their
+    # own slot), membound latencies, the model-major layer latencies, totals
+    sizes = [nc, (nc + 7) // 8, nu, n * L, n]
+    starts = [0]
+    for z in sizes:
+        starts.append(starts[-1] + int(z))
+    buf = t.empty(int(starts[-1]), dtype=t.float64, device=dev)
+    bp = buf.data_ptr()
+    sl = lambda k: buf[starts[k]:starts[k + 1]]  # noqa: E731
+    lat_d = sl(3)
+    lat_d.fill_(float("nan"))
+    if nc:
+        d_sh = d_int[:4 * nc].to(t.int32)   # u32 descriptors (int32 bits)
+        ext_c, ext_l, n_ext = _log2_extension(sh, dev)
+        o = 0
+        for triple, ls, k in tri:
+            dt = pred.resolver.triple_tables(*triple)[4]
+            _native.check(lib.pm2l_points_predict_ext(
+                dt.handle, d_sh.data_ptr() + 16 * o, k, _native.ptr(ext_c), _native.ptr(ext_l),
+                n_ext, bp + 8 * (starts[0] + o), 0, 0, bp + 8 * starts[1] + o, 0, 0, 0, s),
+                "pm2l_points_predict_ext")
+            o += k
+        lat_d[d_posc] = sl(0)
+    if nu:
+        nf, nw, nm = 5 * nu, 5 * len(models), len(models)
+        ids = d_mid.to(t.int32)
+        base = d_flt.data_ptr()
+        _native.check(lib.pm2l_membound_predict(
+            base, ids.data_ptr(), nu, base + 8 * nf, base + 8 * (nf + nw),
+            base + 8 * (nf + nw + nm), nm, bp + 8 * starts[2], 0, s), "pm2l_membound_predict")
+        lat_d[d_posu] = sl(2)
+    if n:
+        _native.check(lib.pm2l_segment_fsum(bp + 8 * starts[3], d_off.data_ptr(), n,
+                                            bp + 8 * starts[4], s), "pm2l_segment_fsum")
+    host = _staged_download(buf)
+    v = lambda k, dt_: host[8 * starts[k]:8 * starts[k + 1]].view(dt_)  # noqa: E731
+    if nc:
+        match = v(1, np.int8)[:nc]
+        o = 0
+        for triple, ls, k in tri:
+            bad = np.nonzero(match[o:o + k] == -3)[0]
+            if len(bad):
+                j = int(bad[0])
+                raise ValidationError(f"model {j // len(ls)} layer {template[ls[j % len(ls)]].layer_id!r}: "
+                                      f"block count exceeds 2^64")
+            o += k
+    lat = v(3, np.float64).reshape(n, L).copy()
+    totals = v(4, np.float64).copy()
     bad = np.isnan(lat)
     if bad.any():
         i, l = np.argwhere(bad)[0]
@@ -504,5 +565,4 @@ def predict_model_grid(template: Sequence[TemplateLayer], shapes, features, data
         i, l = np.argwhere(bad)[0]
         raise ValidationError(f"model {int(i)} layer {template[l].layer_id!r}: latency_us must "
                               f"be finite and > 0, got {float(lat[i, l])!r}")
-    totals = segment_fsum(lat.ravel(), np.arange(0, n * L + 1, L, dtype=np.int64))
     return lat, totals
