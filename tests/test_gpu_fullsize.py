@@ -292,3 +292,30 @@ def test_c4_nas_grid_matches_reference_predict_model(gpu):
         assert r.total_latency_us.hex() == float(z["total"][i]).hex()
         assert [lp.prediction.latency_us.hex() for lp in r.per_layer] == \
             [float(x).hex() for x in z["lat"][i]]
+
+
+@pytest.mark.parametrize("ds_name,family,dtype,tmode", [
+    ("fp32", "matmul", "fp32", "nn"),        # 13-curve FP32 preset
+    ("fp32", "linear", "fp32", "tn"),
+    ("generic", "triton_mm", "fp32", "nn"),  # the generic preset's triton family
+])
+def test_c2_shaped_grid_other_tables_full(gpu, ds_name, family, dtype, tmode):
+    """The C2 grid shape (10 M points) against the other shipped presets:
+    whatever kernel path their tables take (lookup, single or general
+    sweep), device-planned and host-planned launches equal the reference's
+    compiled kernel point for point."""
+    import torch
+    from paper_2603_00549_b200 import _native, backend
+    prep = _prep(ds_name, family, dtype, tmode, _c2_axes())
+    ref = _reference(prep)
+    got = backend.predict_grid_device(prep).cpu().numpy()
+    assert np.array_equal(_bits(got), _bits(ref))
+    axes = [torch.from_numpy(np.ascontiguousarray(a, np.uint64).view(np.int64)).cuda()
+            for a in prep.axis_arrays()]
+    dp = _native.DeviceGridPlanner(prep.device_tables(0), *(len(a) for a in axes))
+    out = torch.empty(prep.grid.cardinality, dtype=torch.float64, device="cuda")
+    dp.launch(axes, out)
+    torch.cuda.synchronize()
+    assert dp.status() == 0
+    assert np.array_equal(_bits(out.cpu().numpy()), _bits(ref))
+    dp.close()
