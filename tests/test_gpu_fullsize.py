@@ -319,3 +319,39 @@ def test_c2_shaped_grid_other_tables_full(gpu, ds_name, family, dtype, tmode):
     assert dp.status() == 0
     assert np.array_equal(_bits(out.cpu().numpy()), _bits(ref))
     dp.close()
+
+
+@pytest.mark.parametrize("ds_name,family,dtype,tmode", [
+    ("fp32", "matmul", "fp32", "nn"),
+    ("fp32", "batched_matmul", "fp32", "nn"),
+    ("generic", "triton_mm", "fp32", "nn"),
+    ("generic_bf16", "flash_attention", "bf16", "nn"),
+])
+def test_points_mode_other_presets_match_oracle(gpu, ds_name, family, dtype, tmode):
+    """Explicit descriptors against the other shipped presets (their tables
+    take the row walk, the member pass or the general k-group sweep): 1 M
+    seeded ops with every recorded shape mixed in, all outputs vs the
+    oracle's ConfigResolver restatement."""
+    import torch
+    from paper_2603_00549_b200 import _native
+    prep = _prep(ds_name, family, dtype, tmode, _c2_axes())
+    rng = np.random.default_rng(11)
+    n = 1_000_000
+    shapes = np.stack([rng.integers(1, 300, n), rng.integers(1, 9000, n),
+                       rng.integers(1, 9000, n), rng.integers(1, 70000, n)], 1).astype(np.uint32)
+    rec = np.array([r.shape.as_tuple() for r in prep.records], np.uint32)
+    shapes[:len(rec)] = rec
+    s = torch.from_numpy(shapes).cuda()
+    outs = [torch.empty(n, dtype=x, device="cuda") for x in
+            (torch.float64, torch.int32, torch.int32, torch.int8, torch.int32, torch.float64)]
+    _native.check(_native.load().pm2l_points_predict(
+        prep.device_tables(0).handle, s.data_ptr(), n, *[o.data_ptr() for o in outs],
+        _native.stream_handle()), "points")
+    o_lat, o_cur, o_wav, o_mat, o_rec, o_dist = _oracle_points_threaded(prep.tables(), shapes)
+    lat, cur, wav, mat, rid, dist = (o.cpu().numpy() for o in outs)
+    assert np.array_equal(_bits(lat), _bits(o_lat))
+    assert np.array_equal(cur, o_cur)
+    assert np.array_equal(wav.view(np.uint32), o_wav)
+    assert np.array_equal(mat, o_mat)
+    assert np.array_equal(rid, o_rec)
+    assert np.array_equal(_bits(dist), _bits(o_dist))
