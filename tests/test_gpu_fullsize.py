@@ -355,3 +355,26 @@ def test_points_mode_other_presets_match_oracle(gpu, ds_name, family, dtype, tmo
     assert np.array_equal(mat, o_mat)
     assert np.array_equal(rid, o_rec)
     assert np.array_equal(_bits(dist), _bits(o_dist))
+
+
+def test_membound_c5_sized_batch_matches_oracle(gpu):
+    """tools/bench_modes.py 'membound' / C5's membound share: 5 M feature
+    vectors over 32 fitted-shape models (wide dynamic range, floors hit and
+    missed, negative weights) -- the left-to-right FMA chain and the floor
+    bit for bit against the oracle."""
+    from paper_2603_00549_b200.core import DType
+    from paper_2603_00549_b200.membound import MemBoundModel, predict_membound_batch
+    rng = np.random.default_rng(23)
+    n, nm = 5_000_000, 32
+    f = np.exp(rng.uniform(0, 40, (n, 5)))
+    ids = rng.integers(0, nm, n).astype(np.int32)
+    w = rng.uniform(-1e-9, 4e-9, (nm, 5))
+    b = rng.uniform(-5, 5, nm)
+    floors = rng.uniform(0.5, 3.0, nm)
+    models = [MemBoundModel(f"k{i}", DType.FP32, tuple(w[i]), float(b[i]), "d", 0.0, 0.0)
+              for i in range(nm)]
+    lat, flo = predict_membound_batch(models, f, ids, floors)
+    o_lat, o_flo = oracle.membound(f, ids, w, b, floors)
+    assert np.array_equal(_bits(lat), _bits(o_lat))
+    assert np.array_equal(flo, o_flo)
+    assert 0 < flo.mean() < 1   # both sides of the floor are exercised
