@@ -378,3 +378,24 @@ def test_membound_c5_sized_batch_matches_oracle(gpu):
     assert np.array_equal(_bits(lat), _bits(o_lat))
     assert np.array_equal(flo, o_flo)
     assert 0 < flo.mean() < 1   # both sides of the floor are exercised
+
+
+def test_segment_fsum_many_models_matches_math_fsum(gpu):
+    """Per-model totals at NAS-grid scale: 200 k segments of 0..40 terms
+    (empty, single-term, signed, wide dynamic range, exact cancellations)
+    equal math.fsum bit for bit (the reference's aggregate.py:193)."""
+    from paper_2603_00549_b200.aggregate import segment_fsum
+    rng = np.random.default_rng(29)
+    nseg = 200_000
+    lens = rng.integers(0, 41, nseg)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    n = int(off[-1])
+    v = rng.standard_normal(n) * np.exp(rng.uniform(-30, 30, n))
+    # exact cancellations in every 97th segment
+    for s in range(0, nseg, 97):
+        a, b = off[s], off[s + 1]
+        if b - a >= 2:
+            v[b - 1] = -v[a]
+    got = segment_fsum(v, off)
+    want = oracle.segment_fsum(v, off)
+    assert np.array_equal(_bits(got), _bits(want))
