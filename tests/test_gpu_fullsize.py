@@ -399,3 +399,18 @@ def test_segment_fsum_many_models_matches_math_fsum(gpu):
     got = segment_fsum(v, off)
     want = oracle.segment_fsum(v, off)
     assert np.array_equal(_bits(got), _bits(want))
+
+
+def test_c2_store_records_device_equal_host_encoder(gpu):
+    """§8f row 1 at C2 size: the 10 M store records (400 MB, big-endian
+    coordinates + latency) encoded on the device equal the host encoder's
+    bytes (digest compared)."""
+    import hashlib
+    from paper_2603_00549_b200 import backend
+    from paper_2603_00549_b200.nascache import encode_records, encode_records_device
+    prep = _prep("bf16", "matmul", "bf16", "nn", _c2_axes())
+    lat = backend.predict_grid_device(prep)
+    dev = encode_records_device(prep.grid, lat)
+    host = encode_records(prep.grid, lat.cpu().numpy())
+    assert dev.nbytes == host.nbytes == 40 * prep.grid.cardinality
+    assert hashlib.sha256(dev.tobytes()).digest() == hashlib.sha256(host.tobytes()).digest()
