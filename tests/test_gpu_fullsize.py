@@ -414,3 +414,29 @@ def test_c2_store_records_device_equal_host_encoder(gpu):
     host = encode_records(prep.grid, lat.cpu().numpy())
     assert dev.nbytes == host.nbytes == 40 * prep.grid.cardinality
     assert hashlib.sha256(dev.tobytes()).digest() == hashlib.sha256(host.tobytes()).digest()
+
+
+def test_c2_store_batched_lookup_returns_the_written_latencies(gpu, tmp_path):
+    """§8f row 2 at C2 size: the 10 M-record store written from the device
+    result; 1 M batched lookups (random points, the first and last record)
+    return exactly the latencies at those points, and an absent point raises
+    MissingEntry as CacheStore.lookup does."""
+    from paper_2603_00549_b200 import backend
+    from paper_2603_00549_b200.errors import MissingEntry
+    from paper_2603_00549_b200.nascache import CacheStore, encode_records_device, write_store
+    prep = _prep("bf16", "matmul", "bf16", "nn", _c2_axes())
+    lat_d = backend.predict_grid_device(prep)
+    path = str(tmp_path / "c2.store")
+    write_store(path, prep.grid, prep.dataset, records=encode_records_device(prep.grid, lat_d))
+    lat = lat_d.cpu().numpy()
+    shape = prep.grid.shape()
+    rng = np.random.default_rng(41)
+    idx = np.concatenate([[0, len(lat) - 1], rng.integers(0, len(lat), 1_000_000)])
+    coords = np.stack(np.unravel_index(idx, shape), 1)
+    axes = [np.asarray(prep.grid.axes[a], np.uint64) for a in ("batch", "m", "n", "k")]
+    pts = np.stack([axes[i][coords[:, i]] for i in range(4)], 1)
+    with CacheStore(path) as st:
+        got = st.lookup_many(pts)
+        assert np.array_equal(_bits(got), _bits(lat[idx]))
+        with pytest.raises(MissingEntry):
+            st.lookup_many(np.array([[3, 64, 96, 32]], np.uint64))   # batch 3 is not on the grid
