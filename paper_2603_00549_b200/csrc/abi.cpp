@@ -944,9 +944,38 @@ int drain_to_host(SliceDevice& sd, const double* d_out, double* out, size_t byte
     PM2L_CUDA(sd.stage[i].reserve(kStageChunk));
     if (!sd.ready[i]) PM2L_CUDA(cudaEventCreateWithFlags(&sd.ready[i], cudaEventDisableTiming));
   }
-  const size_t n = (bytes + kStageChunk - 1) / kStageChunk;
+  // chunk schedule: tapered at both ends so the host copy starts sooner and
+  // the last copy, which nothing overlaps, is short; PM2L_STAGE_TAPER (read
+  // once, tuning): 0 uniform C, 1 (default) or 2 levels of taper
+  static const int taper = [] {
+    const char* e = std::getenv("PM2L_STAGE_TAPER");
+    return e ? std::atoi(e) : 1;
+  }();
+  std::vector<size_t> lens;
+  {
+    const size_t C = kStageChunk;
+    size_t rest = bytes;
+    const bool tp = taper > 0 && bytes > 3 * C;
+    // level 1: head C/4, C/2; tail C/2, C/4, C/4.  level 2: head C/8, C/4,
+    // C/2; tail C/2, C/4, C/8, C/8
+    std::vector<size_t> head, tail;
+    if (tp && taper == 1) { head = {C / 4, C / 2}; tail = {C / 2, C / 4, C / 4}; }
+    if (tp && taper >= 2) { head = {C / 8, C / 4, C / 2}; tail = {C / 2, C / 4, C / 8, C / 8}; }
+    size_t tail_bytes = 0;
+    for (size_t h : tail) tail_bytes += h;
+    for (size_t h : head) { lens.push_back(h); rest -= h; }
+    while (rest > tail_bytes) {
+      const size_t l = std::min(C, rest - tail_bytes);
+      lens.push_back(l);
+      rest -= l;
+    }
+    for (size_t h : tail) lens.push_back(h);
+  }
+  std::vector<size_t> offs(lens.size());
+  for (size_t c = 0, o = 0; c < lens.size(); ++c) { offs[c] = o; o += lens[c]; }
+  const size_t n = lens.size();
   auto issue = [&](size_t c) -> int {
-    const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    const size_t off = offs[c], len = lens[c];
     const int b = int(c % kStageBufs);
     PM2L_CUDA(cudaMemcpyAsync(sd.stage[b].ptr, reinterpret_cast<const uint8_t*>(d_out) + off, len,
                               cudaMemcpyDeviceToHost, sd.stream));
@@ -964,7 +993,7 @@ int drain_to_host(SliceDevice& sd, const double* d_out, double* out, size_t byte
     const auto t0 = now();
     PM2L_CUDA(cudaEventSynchronize(sd.ready[b]));
     const auto t1 = now();
-    const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    const size_t off = offs[c], len = lens[c];
     g_slice.pool->copy(reinterpret_cast<uint8_t*>(out) + off, sd.stage[b].ptr, len);
     t_wait += std::chrono::duration<double, std::milli>(t1 - t0).count();
     t_copy += std::chrono::duration<double, std::milli>(now() - t1).count();
