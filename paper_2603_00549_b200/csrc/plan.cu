@@ -340,7 +340,10 @@ __device__ void plan_base(const TablesDev& t, const GridDev& g, const PlanArgs& 
   }
 }
 
-__global__ void __launch_bounds__(kPlanThreads) plan_kernel(TablesDev t, GridDev g, PlanArgs a) {
+#ifndef PM2L_PLAN_MINB
+#define PM2L_PLAN_MINB 1  // blocks per SM the register budget must allow (build macro, tuning)
+#endif
+__global__ void __launch_bounds__(kPlanThreads, PM2L_PLAN_MINB) plan_kernel(TablesDev t, GridDev g, PlanArgs a) {
   pdl_release();  // the grid kernel may launch and run its table prologue now
   extern __shared__ __align__(16) uint8_t smem[];
   const int b = blockIdx.x;
