@@ -340,10 +340,14 @@ __device__ void plan_base(const TablesDev& t, const GridDev& g, const PlanArgs& 
   }
 }
 
-#ifndef PM2L_PLAN_MINB
-#define PM2L_PLAN_MINB 1  // blocks per SM the register budget must allow (build macro, tuning)
+// PM2L_PLAN_MINB (build macro, tuning): blocks per SM the register budget
+// must allow; unset, the compiler picks (58 registers at 512 threads)
+#ifdef PM2L_PLAN_MINB
+#define PLAN_BOUNDS __launch_bounds__(kPlanThreads, PM2L_PLAN_MINB)
+#else
+#define PLAN_BOUNDS __launch_bounds__(kPlanThreads)
 #endif
-__global__ void __launch_bounds__(kPlanThreads, PM2L_PLAN_MINB) plan_kernel(TablesDev t, GridDev g, PlanArgs a) {
+__global__ void PLAN_BOUNDS plan_kernel(TablesDev t, GridDev g, PlanArgs a) {
   pdl_release();  // the grid kernel may launch and run its table prologue now
   extern __shared__ __align__(16) uint8_t smem[];
   const int b = blockIdx.x;
